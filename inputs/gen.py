@@ -1,0 +1,189 @@
+"""Seeded synthetic inputs (numpy, CPU) -- no arithmetic of the method lives here.
+
+These generators stand in for the paper's datasets (road_usa, LiveJournal,
+Twitter, Friendster, ... P:1145-1175, Table 2), which are not in
+the container: the five BASELINE.json configs, with the recipe of DESIGN.md
+§Inputs.  Every draw is a pure function of (seed, stream, index) through
+
+    mix(seed, stream, i) = splitmix64(seed * GOLD + stream * 2^40 + i)   (mod 2^64)
+
+so the CUDA generator (``inputs/csrc/gen.cu``) reproduces these bytes exactly,
+independent of launch configuration (tested in tests/test_gen_gpu.py).  The
+oracle consumes CSRs from here (small sizes) or the GPU generator's bytes
+(full sizes, after the byte-equality test at small sizes); the product library
+consumes them through device memory.
+
+CSR convention: symmetric, no self-loops, no duplicates,
+every list sorted ascending; int64 offsets[n+1], uint32 adj[m], m = number of
+directed entries (each undirected edge counted twice).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+M64 = (1 << 64) - 1
+GOLD = 0x9E3779B97F4A7C15
+
+ER_STREAM, GRID_STREAM, RMAT_STREAM, PERM_STREAM, QUERY_STREAM = 1, 2, 3, 4, 5
+
+# fixed-point thresholds: floor(p * 2^32)
+P55 = 2362232012            # Bernoulli(0.55) for the grid
+RMAT_T1 = 2448131358        # a            = 0.57
+RMAT_T2 = 3264175144        # a + b        = 0.76
+RMAT_T3 = 4080218931        # a + b + c    = 0.95
+
+
+def splitmix64(x: np.ndarray) -> np.ndarray:
+    with np.errstate(over="ignore"):
+        z = np.asarray(x, dtype=np.uint64) + np.uint64(GOLD)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+def mix(seed: int, stream: int, idx) -> np.ndarray:
+    base = np.uint64((seed * GOLD + (stream << 40)) & M64)
+    with np.errstate(over="ignore"):
+        return splitmix64(np.asarray(idx, dtype=np.uint64) + base)
+
+
+def lo32(r):
+    return r & np.uint64(0xFFFFFFFF)
+
+
+def hi32(r):
+    return r >> np.uint64(32)
+
+
+def scale_u32(x32, bound: int):
+    """(x32 * bound) >> 32 : uniform on [0, bound) from a 32-bit draw."""
+    with np.errstate(over="ignore"):
+        return (x32 * np.uint64(bound)) >> np.uint64(32)
+
+
+# ---------------------------------------------------------------------------
+def perm_params(seed: int, s: int):
+    """Three rounds of x ^= x >> ceil(s/2); x = x*K_i + c_i (mod 2^s), K_i odd."""
+    mask = (1 << s) - 1
+    r = [int(v) for v in mix(seed, PERM_STREAM, np.arange(6, dtype=np.uint64))]
+    ks = [(r[i] | 1) & mask for i in range(3)]
+    cs = [r[3 + i] & mask for i in range(3)]
+    return ks, cs, (s + 1) // 2, mask
+
+
+def permute(x, seed: int, s: int) -> np.ndarray:
+    """Seeded bijection on s-bit ids (Q17/Q18 reading: hubs scattered over ids)."""
+    ks, cs, h, mask = perm_params(seed, s)
+    x = np.asarray(x, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        for i in range(3):
+            x = x ^ (x >> np.uint64(h))
+            x = (x * np.uint64(ks[i]) + np.uint64(cs[i])) & np.uint64(mask)
+    return x
+
+
+def rmat_pairs(seed: int, s: int, first: int, count: int, permuted: bool = True):
+    """RMAT draws first..first+count-1 on 2^s vertices (Graph500 a,b,c = .57,.19,.19).
+
+    Level l (0-based, most significant first) uses the 32-bit half (l & 1) of
+    mix(seed, RMAT, i*L + l//2), L = ceil(s/2), and sets bit s-1-l of (u, v)."""
+    L = (s + 1) // 2
+    i = np.arange(first, first + count, dtype=np.uint64)
+    u = np.zeros(count, dtype=np.uint64)
+    v = np.zeros(count, dtype=np.uint64)
+    r = None
+    for lvl in range(s):
+        if lvl % 2 == 0:
+            with np.errstate(over="ignore"):
+                r = mix(seed, RMAT_STREAM, i * np.uint64(L) + np.uint64(lvl // 2))
+            x = lo32(r)
+        else:
+            x = hi32(r)
+        bit = np.uint64(1) << np.uint64(s - 1 - lvl)
+        ub = x >= np.uint64(RMAT_T2)                       # quadrants (1,0), (1,1)
+        vb = ((x >= np.uint64(RMAT_T1)) & (x < np.uint64(RMAT_T2))) | (x >= np.uint64(RMAT_T3))
+        u |= np.where(ub, bit, np.uint64(0))
+        v |= np.where(vb, bit, np.uint64(0))
+    if permuted:
+        u = permute(u, seed, s)
+        v = permute(v, seed, s)
+    return u, v
+
+
+def csr_from_directed_pairs(n: int, u, v):
+    """Symmetrise, drop self-loops, dedup, sort -> (offsets int64[n+1], adj uint32[m])."""
+    u = np.asarray(u, dtype=np.uint64)
+    v = np.asarray(v, dtype=np.uint64)
+    keep = u != v
+    u, v = u[keep], v[keep]
+    keys = np.concatenate([(u << np.uint64(32)) | v, (v << np.uint64(32)) | u])
+    keys = np.unique(keys)
+    src = (keys >> np.uint64(32)).astype(np.int64)
+    adj = (keys & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    off = np.zeros(n + 1, dtype=np.int64)
+    if src.size:
+        np.cumsum(np.bincount(src, minlength=n), out=off[1:])
+    return off, adj
+
+
+# ---------------------------------------------------------------------------
+def er(seed: int = 1, n0: int = 100_000, pairs: int = 400_000, isolated: int = 1_000):
+    """C1: `pairs` uniform draws on [0,n0) (u from low, v from high 32 bits of one draw)."""
+    r = mix(seed, ER_STREAM, np.arange(pairs, dtype=np.uint64))
+    u = scale_u32(lo32(r), n0)
+    v = scale_u32(hi32(r), n0)
+    return csr_from_directed_pairs(n0 + isolated, u, v)
+
+
+def grid(seed: int = 2, rows: int = 4096, cols: int = 4096, p32: int = P55):
+    """C2: id = r*cols + c; horizontal candidates first, then vertical; keep iff draw < p32."""
+    nh = rows * (cols - 1)
+    nv = (rows - 1) * cols
+    e = np.arange(nh + nv, dtype=np.uint64)
+    keep = lo32(mix(seed, GRID_STREAM, e)) < np.uint64(p32)
+    eh = e[:nh][keep[:nh]]
+    ev = e[nh:][keep[nh:]] - np.uint64(nh)
+    rr, cc = eh // np.uint64(cols - 1), eh % np.uint64(cols - 1)
+    hu = rr * np.uint64(cols) + cc
+    u = np.concatenate([hu, ev])
+    v = np.concatenate([hu + np.uint64(1), ev + np.uint64(cols)])
+    return csr_from_directed_pairs(rows * cols, u, v)
+
+
+def rmat(seed: int = 3, scale: int = 24, edge_factor: int = 16, permuted: bool = True):
+    """C3/C4: edge_factor * 2^scale RMAT draws, symmetrised/deduplicated/permuted."""
+    u, v = rmat_pairs(seed, scale, 0, edge_factor << scale, permuted)
+    return csr_from_directed_pairs(1 << scale, u, v)
+
+
+def incr_batch(seed: int, scale: int, b: int, n_ins: int, n_q: int):
+    """C5 batch b: n_ins RMAT-`scale` inserts (draws b*n_ins ..), n_q uniform query pairs.
+
+    Returns (inserts (n_ins,2) uint32, queries (n_q,2) uint32).  Self-loops and
+    duplicates are kept (legal no-op inserts, reading R16)."""
+    u, v = rmat_pairs(seed, scale, b * n_ins, n_ins, permuted=True)
+    n = 1 << scale
+    r = mix(seed, QUERY_STREAM, np.arange(b * n_q, (b + 1) * n_q, dtype=np.uint64))
+    a = scale_u32(lo32(r), n)
+    c = scale_u32(hi32(r), n)
+    ins = np.stack([u, v], axis=1).astype(np.uint32)
+    qs = np.stack([a, c], axis=1).astype(np.uint32)
+    return ins, qs
+
+
+def validate_csr(off, adj, n: int | None = None) -> None:
+    """Raise AssertionError unless (off, adj) is a valid symmetric sorted simple CSR."""
+    off = np.asarray(off, dtype=np.int64)
+    adj = np.asarray(adj, dtype=np.uint32)
+    n = off.size - 1 if n is None else n
+    assert off.size == n + 1 and off[0] == 0 and off[-1] == adj.size
+    assert np.all(np.diff(off) >= 0)
+    if adj.size == 0:
+        return
+    assert int(adj.max()) < n
+    src = np.repeat(np.arange(n, dtype=np.uint64), np.diff(off))
+    keys = (src << np.uint64(32)) | adj.astype(np.uint64)
+    assert np.all(np.diff(keys.astype(np.uint64)) > 0), "lists not strictly ascending (dup or unsorted)"
+    assert not np.any(src == adj), "self-loop"
+    rev = (adj.astype(np.uint64) << np.uint64(32)) | src
+    assert np.array_equal(np.sort(rev), keys), "not symmetric"
