@@ -1,0 +1,184 @@
+/*
+ * cc.h -- C ABI of the B200 connectivity hot path (ConnectIt, arXiv 2008.03909).
+ *
+ * libcc.so (paper_2008_03909_b200/libcc.so) exports exactly the functions
+ * declared here and in cc_bench.h.  Every signature uses plain pointers and
+ * sizes; there are no torch types.  Citations "P:n" are PAPER.md lines.
+ *
+ * Problem statement: given an undirected graph G = (V, E) with
+ * n = |V|, compute a connectivity labeling C with C(u) = C(v) iff u and v are
+ * in the same connected component, and a spanning forest with one tree per
+ * component.  Batch-incremental connectivity: process batches of
+ * Insert(u,v) and IsConnected(u,v) operations one batch after another.
+ *
+ * ---- Graph layout (all calls) ----------------------------------------------
+ *   offsets  int64_t[n+1], offsets[0] = 0, offsets[n] = m, non-decreasing.
+ *   adj      uint32_t[m]; the neighbours of v are adj[offsets[v] .. offsets[v+1]).
+ *   m counts DIRECTED adjacency entries (each undirected edge twice).
+ *   The graph must be SYMMETRIC (u in N(v) iff v in N(u)) for the giant-
+ *   component skip to be correct (Thm. A.1); pass
+ *   CC_FLAG_NO_SKIP otherwise -- the result is then the CC of the underlying
+ *   undirected graph.  Self-loops and duplicate entries are tolerated.
+ *   Neighbour order only changes which "first k" edges are sampled, never the
+ *   labels.  Ids are uint32 < n; n <= 0xFFFFFFFE (0xFFFFFFFF is the sentinel).
+ *
+ * ---- Memory, streams, ownership -----------------------------------------------
+ *   Array arguments may be DEVICE pointers (cudaMalloc / torch tensors) or
+ *   HOST pointers (pinned or pageable).  With device pointers every call is
+ *   stream-ordered and asynchronous on `stream` (a cudaStream_t; NULL = legacy
+ *   default stream) and performs no host synchronisation.  If ANY array
+ *   argument of a call is a host pointer, the call stages the host arrays
+ *   through library-owned device memory (host->device copies, compute,
+ *   device->host copies) and returns only after the results are in the host
+ *   buffers (it synchronises `stream`).
+ *   The caller owns every input and output buffer and must keep them alive
+ *   until the stream has passed the call.  The library owns only cc_incr
+ *   handles and transient scratch, allocated with cudaMallocAsync on `stream`
+ *   and freed on the same stream before the call returns.
+ *
+ * ---- Errors --------------------------------------------------------------------
+ *   Host-side argument checks run first and return before any launch:
+ *   CC_EINVAL (null pointer with n > 0, m < 0, bad opts), CC_ERANGE
+ *   (n > 0xFFFFFFFE, kout_k > 64).  n = 0 returns CC_OK with no work.
+ *   Malformed CSR (offsets not monotone, adj[i] >= n) is undefined behaviour
+ *   unless CC_FLAG_VALIDATE is set: then a validation kernel runs first (one
+ *   stream synchronisation) and CC_EINVAL is returned with outputs untouched.
+ *   CUDA failures return CC_ECUDA; cc_last_error() returns a thread-local
+ *   detail string.  On any error a cc_incr handle keeps its pre-call state.
+ */
+#ifndef CC_B200_CC_H
+#define CC_B200_CC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int cc_status;
+#define CC_OK       0
+#define CC_EINVAL  (-1)
+#define CC_ERANGE  (-2)
+#define CC_ENOMEM  (-3)
+#define CC_ECUDA   (-4)
+
+/* k-out edge choice (Alg. 4; variants P:3589-3599).
+ * AFFOREST: adjacency positions 0..k-1 ("first k neighbours", the north_star).
+ * HYBRID:   position 0 plus k-1 positions uniform with replacement (the
+ *           paper's default); draw j of vertex u is
+ *           ((lo32(mix(seed,16,u*64+j)) * deg(u)) >> 32) with
+ *           mix(s,t,i) = splitmix64(s*0x9E3779B97F4A7C15 + t*2^40 + i).      */
+#define CC_VARIANT_AFFOREST 0u
+#define CC_VARIANT_HYBRID   1u
+
+#define CC_FLAG_NO_SKIP     (1u << 0)  /* finish every vertex (no L_max skip)          */
+#define CC_FLAG_VALIDATE    (1u << 1)  /* check the CSR first (synchronises)                     */
+#define CC_FLAG_UF_ASYNC    (1u << 2)  /* UF-Async link rule instead of UF-Rem-CAS */
+#define CC_FLAG_HALVE       (1u << 3)  /* HalveAtomicOne instead of SplitAtomicOne */
+#define CC_FLAG_FIND_SPLIT  (1u << 4)  /* incremental queries use FindAtomicSplit  */
+#define CC_FLAG_NO_DEGSKIP  (1u << 5)  /* also finish vertices whose whole list was sampled      */
+#define CC_FLAG_NO_MIDCOMPRESS (1u << 6) /* skip the compress between k-out rounds               */
+
+/* Per-phase device times, filled when cc_opts.timings != NULL (the call then
+ * synchronises `stream` before returning).  Bench/diagnostics only.          */
+typedef struct {
+    float sample_ms;     /* H1 init + H2 k-out link + H3 sampling compress        */
+    float identify_ms;   /* H4 IdentifyFrequent                                    */
+    float finish_ms;     /* H5 finish link with the L_max skip                     */
+    float compress_ms;   /* H6 final compress (+ H7 forest compaction in SF mode)  */
+    float total_ms;
+} cc_timings;
+
+/* Work counters, accumulated (atomicAdd) into a DEVICE struct when
+ * cc_opts.counters != NULL.  Bench/diagnostics only.                         */
+typedef struct {
+    uint64_t pending_links;    /* H2 links that needed the CAS kernel               */
+    uint64_t worklist;         /* vertices examined by the finish (deg > k)          */
+    uint64_t finish_vertices;  /* non-L_max vertices whose lists were traversed      */
+    uint64_t finish_edges;     /* adjacency entries traversed by the finish          */
+    uint64_t finish_offsets;   /* offset pairs read by the finish                    */
+    uint64_t hooks;            /* successful root hooks (H2 CAS + H5)                */
+    uint64_t big_vertices;     /* finish vertices sent to the CTA-per-vertex queue   */
+    uint64_t reserved;
+} cc_counters;
+
+typedef struct {
+    uint32_t kout_k;           /* sampled edges per vertex; default 2; 0 = no sampling */
+    uint32_t kout_variant;     /* CC_VARIANT_*; default AFFOREST                       */
+    uint64_t seed;             /* hybrid picks + IdentifyFrequent draws; default 0     */
+    uint32_t samples;          /* IdentifyFrequent sample count; default 1024 (1..4096)*/
+    uint32_t flags;            /* CC_FLAG_*                                            */
+    /* test/bench hooks; NULL in production (no extra traffic, no syncs):          */
+    uint32_t*       sampled_out; /* DEVICE, n: copy of P after H3 (sampled labels)    */
+    uint32_t*       lmax_out;    /* DEVICE scalar: the L_max used                     */
+    const uint32_t* lmax_force;  /* DEVICE scalar or NULL: overrides H4;
+                                    0xFFFFFFFF = skip nothing                          */
+    cc_counters*    counters;    /* DEVICE                                             */
+    cc_timings*     timings;     /* HOST                                               */
+} cc_opts;
+
+/* Fill *o with the defaults above. */
+void cc_opts_default(cc_opts* o);
+
+/* Connectivity, Alg. 1 with k-out sampling (Alg. 4), IdentifyFrequent
+ * and the UF-Rem-CAS finish, then a full
+ * compress.  labels (out, n) is also the parent array, used in place:
+ * on return labels[v] = minimum vertex id of v's component (canonical). */
+cc_status cc_labels(const int64_t* offsets, const uint32_t* adj, uint32_t n, int64_t m,
+                    uint32_t* labels, const cc_opts* opts, void* stream);
+
+/* Spanning forest, Alg. 2 with the k-out forest rule
+ * and the root-based finish.  edges (out, capacity 2*n uint32):
+ * pairs (u, v) -- each an input edge with v in N(u) -- packed in ascending order
+ * of the hooked root's id (the Filter of P:2415 keeps array order).
+ * num_edges (out, one int64, same memory kind as edges) = n - #components.
+ * labels (out, n) may be NULL; if given it receives the canonical labels. */
+cc_status cc_spanning_forest(const int64_t* offsets, const uint32_t* adj, uint32_t n, int64_t m,
+                             uint32_t* edges, int64_t* num_edges, uint32_t* labels,
+                             const cc_opts* opts, void* stream);
+
+/* Batch-incremental connectivity, Alg. 3, UF-Rem-CAS +
+ * SplitAtomicOne on a persistent parent array owned by the
+ * handle.  Phase-concurrent order (type (3)): all inserts of a
+ * batch, then a device-wide barrier, then all queries -- so a query sees the
+ * inserts of every earlier batch AND of its own batch. */
+typedef struct cc_incr cc_incr;
+
+/* Create a handle over n vertices with no edges (P[v] = v).  opts may be NULL;
+ * only opts->flags (CC_FLAG_HALVE, CC_FLAG_UF_ASYNC, CC_FLAG_FIND_SPLIT,
+ * CC_FLAG_VALIDATE) is used.  *out receives the handle (host pointer). */
+cc_status cc_incr_create(uint32_t n, const cc_opts* opts, void* stream, cc_incr** out);
+
+/* inserts: 2*n_ins uint32, (u, v) interleaved; queries: 2*n_q uint32;
+ * answers (out): n_q uint8, answers[j] = 1 iff queries[j] endpoints are
+ * connected after all prior batches and this batch's inserts.  Self-loop and
+ * duplicate inserts are legal no-ops.  With CC_FLAG_VALIDATE on the handle,
+ * out-of-range ids return CC_EINVAL before any insert is applied. */
+cc_status cc_incr_batch(cc_incr* h, const uint32_t* inserts, int64_t n_ins,
+                        const uint32_t* queries, int64_t n_q, uint8_t* answers, void* stream);
+
+/* labels (out, n): canonical labels (min id per component) of the current state. */
+cc_status cc_incr_labels(cc_incr* h, uint32_t* labels, void* stream);
+
+/* Synchronises the handle's last stream, then frees it.  NULL is a no-op. */
+void cc_incr_destroy(cc_incr* h);
+
+/* Number of vertices of a handle (0 for NULL). */
+uint32_t cc_incr_num_vertices(const cc_incr* h);
+
+/* Human-readable name of a status; thread-local detail of the last failure. */
+const char* cc_status_str(cc_status s);
+const char* cc_last_error(void);
+
+/* Upper bound of the transient device scratch a call allocates (informational).
+ * op: 0 = cc_labels, 1 = cc_spanning_forest, 2 = cc_incr_create. */
+size_t cc_workspace_bytes(uint32_t n, int64_t m, uint32_t kout_k, int op);
+
+/* Library version string. */
+const char* cc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CC_B200_CC_H */

@@ -1,0 +1,255 @@
+// cc_abi.cu -- the extern "C" boundary of libcc.so (include/cc.h).
+//
+// Argument checks, host-buffer staging, error mapping.  The compute is in
+// cc_static.cu (cc_labels, cc_spanning_forest) and cc_incr.cu (cc_incr_*).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <vector>
+#include <string>
+
+#include "cc_internal.h"
+
+namespace ccb {
+
+std::atomic<uint64_t> g_launches{0};
+static thread_local std::string t_err;
+
+void set_error(const std::string& msg) { t_err = msg; }
+
+cc_status cuda_fail(cudaError_t e, const char* where)
+{
+    t_err = std::string(where) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+    if (e == cudaErrorMemoryAllocation) return CC_ENOMEM;
+    return CC_ECUDA;
+}
+
+int num_sms()
+{
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cached[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = v > 0 ? v : 148;
+    }
+    return cached[dev];
+}
+
+bool is_device_ptr(const void* p)
+{
+    if (!p) return true;                   // NULL: nothing to stage
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static void init_pool_once()
+{
+    static std::once_flag flag[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::call_once(flag[dev & 63], [dev]() {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;          // keep freed scratch cached across calls
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+}
+
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s)
+{
+    init_pool_once();
+    return cudaMallocAsync(p, std::max<size_t>(bytes, 16), s);
+}
+
+void scratch_free(void* p, cudaStream_t s)
+{
+    if (p) cudaFreeAsync(p, s);
+}
+
+// ---- host staging -----------------------------------------------------------
+struct Stage {
+    cudaStream_t s;
+    std::vector<void*> bufs;
+    ~Stage()
+    {
+        for (void* b : bufs) scratch_free(b, s);
+    }
+    template <class T>
+    cudaError_t in(const T* host, size_t count, T** dev)
+    {
+        void* d = nullptr;
+        cudaError_t e = scratch_alloc(&d, sizeof(T) * std::max<size_t>(count, 1), s);
+        if (e != cudaSuccess) return e;
+        bufs.push_back(d);
+        *dev = (T*)d;
+        if (host && count) return cudaMemcpyAsync(d, host, sizeof(T) * count, cudaMemcpyHostToDevice, s);
+        return cudaSuccess;
+    }
+};
+
+static cc_opts resolve(const cc_opts* o)
+{
+    cc_opts r;
+    cc_opts_default(&r);
+    if (o) r = *o;
+    if (r.samples == 0) r.samples = 1024;
+    return r;
+}
+
+static cc_status check_graph_args(const int64_t* off, const uint32_t* adj, uint32_t n, int64_t m,
+                                  const cc_opts& o)
+{
+    if (n > 0xFFFFFFFEu) { set_error("n > 0xFFFFFFFE"); return CC_ERANGE; }
+    if (m < 0) { set_error("m < 0"); return CC_EINVAL; }
+    if (o.kout_k > 64) { set_error("kout_k > 64"); return CC_ERANGE; }
+    if (o.kout_variant > CC_VARIANT_HYBRID) { set_error("unknown kout_variant"); return CC_EINVAL; }
+    if (o.samples > 4096) { set_error("samples > 4096"); return CC_ERANGE; }
+    if (n > 0 && !off) { set_error("offsets is NULL"); return CC_EINVAL; }
+    if (m > 0 && !adj) { set_error("adj is NULL"); return CC_EINVAL; }
+    return CC_OK;
+}
+
+}  // namespace ccb
+
+using namespace ccb;
+
+extern "C" {
+
+void cc_opts_default(cc_opts* o)
+{
+    if (!o) return;
+    std::memset(o, 0, sizeof(*o));
+    o->kout_k = 2;
+    o->kout_variant = CC_VARIANT_AFFOREST;
+    o->seed = 0;
+    o->samples = 1024;
+    o->flags = 0;
+}
+
+const char* cc_status_str(cc_status s)
+{
+    switch (s) {
+    case CC_OK: return "CC_OK";
+    case CC_EINVAL: return "CC_EINVAL";
+    case CC_ERANGE: return "CC_ERANGE";
+    case CC_ENOMEM: return "CC_ENOMEM";
+    case CC_ECUDA: return "CC_ECUDA";
+    default: return "CC_UNKNOWN";
+    }
+}
+
+const char* cc_last_error(void) { return t_err.c_str(); }
+
+const char* cc_version(void) { return "cc-b200 0.1 (sm_100a)"; }
+
+size_t cc_workspace_bytes(uint32_t n, int64_t m, uint32_t kout_k, int op)
+{
+    const size_t N = n, M = m < 0 ? 0 : (size_t)m;
+    if (op == 2) return 4 * N;
+    size_t b = 64 + 4 * N /*worklist*/ + 8 * std::min(N * kout_k, std::max(M, N) * kout_k) + 4 * (M / 4096 + 1);
+    if (op == 1) b += 8 * N + 4 * N + 12 * (N / 4096 + 1);
+    return b;
+}
+
+cc_status cc_labels(const int64_t* offsets, const uint32_t* adj, uint32_t n, int64_t m, uint32_t* labels,
+                    const cc_opts* opts, void* stream)
+{
+    const cc_opts o = resolve(opts);
+    cc_status rc = check_graph_args(offsets, adj, n, m, o);
+    if (rc) return rc;
+    if (n == 0) return CC_OK;
+    if (!labels) { set_error("labels is NULL"); return CC_EINVAL; }
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool dev = is_device_ptr(offsets) && is_device_ptr(adj) && is_device_ptr(labels);
+    if (dev) {
+        if (o.flags & CC_FLAG_VALIDATE) {
+            rc = validate_csr(offsets, adj, n, m, s);
+            if (rc) return rc;
+        }
+        return static_pipeline(offsets, adj, n, m, labels, nullptr, nullptr, false, o, s);
+    }
+    // host buffers: stage in, compute, stage out, synchronise
+    Stage st{s, {}};
+    const int64_t* d_off = offsets;
+    const uint32_t* d_adj = adj;
+    uint32_t* d_lab = labels;
+    if (!is_device_ptr(offsets)) CC_CUDA_TRY(st.in(offsets, (size_t)n + 1, (int64_t**)&d_off));
+    if (!is_device_ptr(adj)) CC_CUDA_TRY(st.in(adj, (size_t)m, (uint32_t**)&d_adj));
+    if (!is_device_ptr(labels)) CC_CUDA_TRY(st.in((const uint32_t*)nullptr, (size_t)n, &d_lab));
+    if (o.flags & CC_FLAG_VALIDATE) {
+        rc = validate_csr(d_off, d_adj, n, m, s);
+        if (rc) return rc;
+    }
+    rc = static_pipeline(d_off, d_adj, n, m, d_lab, nullptr, nullptr, false, o, s);
+    if (rc) return rc;
+    if (d_lab != labels)
+        CC_CUDA_TRY(cudaMemcpyAsync(labels, d_lab, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, s));
+    CC_CUDA_TRY(cudaStreamSynchronize(s));
+    return CC_OK;
+}
+
+cc_status cc_spanning_forest(const int64_t* offsets, const uint32_t* adj, uint32_t n, int64_t m, uint32_t* edges,
+                             int64_t* num_edges, uint32_t* labels, const cc_opts* opts, void* stream)
+{
+    const cc_opts o = resolve(opts);
+    cc_status rc = check_graph_args(offsets, adj, n, m, o);
+    if (rc) return rc;
+    if (!num_edges) { set_error("num_edges is NULL"); return CC_EINVAL; }
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n == 0) {
+        if (is_device_ptr(num_edges)) CC_CUDA_TRY(cudaMemsetAsync(num_edges, 0, sizeof(int64_t), s));
+        else *num_edges = 0;
+        return CC_OK;
+    }
+    if (!edges) { set_error("edges is NULL"); return CC_EINVAL; }
+    const bool dev = is_device_ptr(offsets) && is_device_ptr(adj) && is_device_ptr(edges) &&
+                     is_device_ptr(num_edges) && is_device_ptr(labels);
+    if (dev) {
+        if (o.flags & CC_FLAG_VALIDATE) {
+            rc = validate_csr(offsets, adj, n, m, s);
+            if (rc) return rc;
+        }
+        return static_pipeline(offsets, adj, n, m, labels, edges, num_edges, true, o, s);
+    }
+    Stage st{s, {}};
+    const int64_t* d_off = offsets;
+    const uint32_t* d_adj = adj;
+    uint32_t* d_edges = edges;
+    int64_t* d_ne = num_edges;
+    uint32_t* d_lab = labels;
+    if (!is_device_ptr(offsets)) CC_CUDA_TRY(st.in(offsets, (size_t)n + 1, (int64_t**)&d_off));
+    if (!is_device_ptr(adj)) CC_CUDA_TRY(st.in(adj, (size_t)m, (uint32_t**)&d_adj));
+    if (!is_device_ptr(edges)) CC_CUDA_TRY(st.in((const uint32_t*)nullptr, 2 * (size_t)n, &d_edges));
+    if (!is_device_ptr(num_edges)) CC_CUDA_TRY(st.in((const int64_t*)nullptr, 1, &d_ne));
+    if (labels && !is_device_ptr(labels)) CC_CUDA_TRY(st.in((const uint32_t*)nullptr, (size_t)n, &d_lab));
+    if (o.flags & CC_FLAG_VALIDATE) {
+        rc = validate_csr(d_off, d_adj, n, m, s);
+        if (rc) return rc;
+    }
+    rc = static_pipeline(d_off, d_adj, n, m, d_lab, d_edges, d_ne, true, o, s);
+    if (rc) return rc;
+    int64_t ne = 0;
+    CC_CUDA_TRY(cudaMemcpyAsync(&ne, d_ne, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CC_CUDA_TRY(cudaStreamSynchronize(s));
+    if (d_ne != num_edges) *num_edges = ne;
+    else CC_CUDA_TRY(cudaMemcpyAsync(num_edges, d_ne, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    if (d_edges != edges)
+        CC_CUDA_TRY(cudaMemcpyAsync(edges, d_edges, sizeof(uint32_t) * 2 * (size_t)ne, cudaMemcpyDeviceToHost, s));
+    if (labels && d_lab != labels)
+        CC_CUDA_TRY(cudaMemcpyAsync(labels, d_lab, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, s));
+    CC_CUDA_TRY(cudaStreamSynchronize(s));
+    return CC_OK;
+}
+
+}  // extern "C"

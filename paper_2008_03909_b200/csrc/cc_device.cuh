@@ -1,0 +1,169 @@
+// cc_device.cuh -- device primitives of the union-find hot path (sm_100a).
+//
+// B4 of DESIGN.md: relaxed device-scope parent loads, CAS, the UF-Rem-CAS
+// link with SplitAtomicOne / HalveAtomicOne, UF-Async, FindNaive.  Citations
+// P:n are PAPER.md lines; Rn are DESIGN.md readings.
+//
+// Memory model.  L1 is not coherent across SMs, so every read of the parent
+// array P inside a link/find loop that runs concurrently with hooks is an
+// ld.relaxed.gpu (served by L2, never by a stale L1 line); the paper marks
+// these reads with an asterisk (reading R5).  Correctness
+// rests on two invariants:
+//   (I1) P[x] <= x at all times, with equality exactly at roots: a hook writes
+//        pv < pu = ru, a split writes a grandparent w <= parent.  So every
+//        root is the minimum of its tree and the trees stay acyclic.
+//   (I2) a slot never increases, so there is no ABA: a stale (larger) value
+//        only makes a CAS fail or a walk take an extra step.
+#pragma once
+#include <cstdint>
+
+namespace ccb {
+
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p)
+{
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ uint32_t cas(uint32_t* p, uint32_t expect, uint32_t desired)
+{
+    return atomicCAS(p, expect, desired);
+}
+
+// Streaming loads that should not pollute L1 (read once).
+__device__ __forceinline__ int64_t ld_stream_i64(const int64_t* p)
+{
+    int64_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.s64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p)
+{
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+// FindNaive: walk to the root without writes.
+__device__ __forceinline__ uint32_t find_naive(const uint32_t* P, uint32_t x)
+{
+    uint32_t p = ld_relaxed(P + x);
+    while (p != x) {
+        x = p;
+        p = ld_relaxed(P + x);
+    }
+    return x;
+}
+
+// FindAtomicSplit (reading R4): CAS each node to its grandparent
+// and advance one step; returns the root.
+__device__ __forceinline__ uint32_t find_split(uint32_t* P, uint32_t u)
+{
+    uint32_t v = ld_relaxed(P + u);
+    uint32_t w = ld_relaxed(P + v);
+    while (v != w) {
+        cas(P + u, v, w);
+        u = v;
+        v = w;
+        w = ld_relaxed(P + v);
+    }
+    return v;
+}
+
+struct NoForest {
+    __device__ __forceinline__ void record(uint32_t, uint32_t, uint32_t) const {}
+};
+
+// Spanning-forest record: the edge whose CAS hooked root r is
+// stored at slot r.  Each root is hooked at most once (it never becomes a root
+// again, I2), so a plain store suffices.
+struct Forest {
+    uint2* F;
+    __device__ __forceinline__ void record(uint32_t r, uint32_t u, uint32_t v) const
+    {
+        F[r] = make_uint2(u, v);
+    }
+};
+
+// UF-Rem-CAS union (Alg. UF-Rem-CAS) with SplitAtomicOne
+// or HalveAtomicOne as the splice step, FindNaive
+// as the compress option.  Orientation (readings R1, R6): in each iteration
+// pu = P[ru], pv = P[rv]; equal parents => same tree; otherwise orient so that
+// pu > pv; if ru is a root, hook it under the snapshot pv by CAS, else take one
+// split/halve step on ru.  Returns true iff this call hooked a root.
+template <bool HALVE, class Rec>
+__device__ __forceinline__ bool link_rem(uint32_t* P, uint32_t u, uint32_t v, const Rec& rec)
+{
+    uint32_t ru = u, rv = v;
+    while (true) {
+        uint32_t pu = ld_relaxed(P + ru);
+        uint32_t pv = ld_relaxed(P + rv);
+        if (pu == pv) return false;
+        if (pu < pv) {
+            uint32_t t = ru; ru = rv; rv = t;
+            t = pu; pu = pv; pv = t;
+        }
+        if (ru == pu) {                              // ru is a root: hook it (pv < ru)
+            if (cas(P + ru, ru, pv) == ru) {
+                rec.record(ru, u, v);
+                return true;
+            }
+            continue;                                // lost a race: re-read
+        }
+        uint32_t w = ld_relaxed(P + pu);             // one splice step on ru
+        if (w != pu) cas(P + ru, pu, w);
+        ru = HALVE ? w : pu;
+    }
+}
+
+// UF-Async union (reading R2: the CAS targets the root slot).
+template <class Rec>
+__device__ __forceinline__ bool link_async(uint32_t* P, uint32_t u, uint32_t v, const Rec& rec)
+{
+    uint32_t ru = find_naive(P, u), rv = find_naive(P, v);
+    while (ru != rv) {
+        if (ru < rv) { uint32_t t = ru; ru = rv; rv = t; }
+        if (cas(P + ru, ru, rv) == ru) {
+            rec.record(ru, u, v);
+            return true;
+        }
+        ru = find_naive(P, ru);                      // roots only move up: restart from them
+        rv = find_naive(P, rv);
+    }
+    return false;
+}
+
+template <int MODE, class Rec>
+__device__ __forceinline__ bool link(uint32_t* P, uint32_t u, uint32_t v, const Rec& rec)
+{
+    if constexpr (MODE == 0) return link_rem<false>(P, u, v, rec);
+    else if constexpr (MODE == 1) return link_rem<true>(P, u, v, rec);
+    else return link_async(P, u, v, rec);
+}
+
+// Counter-based generator for the method's own draws (hybrid picks, the
+// IdentifyFrequent samples): mix(s,t,i) = splitmix64(s*GOLD + t*2^40 + i).
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x)
+{
+    uint64_t z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__host__ __device__ __forceinline__ uint64_t mix(uint64_t seed, uint64_t stream, uint64_t i)
+{
+    return splitmix64(seed * 0x9E3779B97F4A7C15ull + (stream << 40) + i);
+}
+
+__host__ __device__ __forceinline__ uint32_t uniform_below(uint64_t r, uint64_t bound)
+{
+    return (uint32_t)(((r & 0xFFFFFFFFull) * bound) >> 32);
+}
+
+constexpr uint64_t KOUT_STREAM = 16;
+constexpr uint64_t IDENT_STREAM = 17;
+
+}  // namespace ccb

@@ -1,0 +1,243 @@
+// cc_incr.cu -- batch-incremental connectivity (H8, H9).
+//
+// Alg. 3 with UF-Rem-CAS + SplitAtomicOne on a
+// persistent parent array P owned by the handle.  Each batch is processed in
+// the phase-concurrent order of type (3): one kernel applies all
+// inserts (each Insert(u,v) is a Union), the kernel boundary is the barrier,
+// then one kernel answers all IsConnected(a,b) queries as Find(a) == Find(b)
+// (reading R15).  Answers are therefore deterministic and bit-exact with the
+// sequential oracle.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "cc_device.cuh"
+#include "cc_internal.h"
+
+struct cc_incr {
+    uint32_t n;
+    uint32_t flags;
+    uint32_t* P;
+    int device;
+    cudaStream_t last;
+};
+
+namespace ccb {
+
+__global__ void __launch_bounds__(kBlock) k_iota(uint32_t* P, uint32_t n)
+{
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) P[i] = (uint32_t)i;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kBlock) k_insert(uint32_t* P, const uint2* __restrict__ ins, int64_t n_ins)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_ins) return;
+    const uint2 e = ins[i];
+    link<MODE>(P, e.x, e.y, NoForest{});
+}
+
+// Queries run after the insert kernel: no hook can happen concurrently, so
+// roots are fixed and FindNaive needs no L2-forced loads; with SPLIT the finds
+// also shorten paths (FindAtomicSplit) for later batches.
+template <bool SPLIT>
+__global__ void __launch_bounds__(kBlock) k_query(uint32_t* P, const uint2* __restrict__ q, int64_t n_q,
+                                                  uint8_t* __restrict__ ans)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_q) return;
+    const uint2 e = q[i];
+    uint32_t ra, rb;
+    if constexpr (SPLIT) {
+        ra = find_split(P, e.x);
+        rb = find_split(P, e.y);
+    } else {
+        ra = e.x;
+        for (uint32_t p = P[ra]; p != ra; p = P[ra]) ra = p;
+        rb = e.y;
+        for (uint32_t p = P[rb]; p != rb; p = P[rb]) rb = p;
+    }
+    ans[i] = ra == rb ? 1 : 0;
+}
+
+__global__ void k_check_ids(const uint32_t* ids, int64_t count, uint32_t n, unsigned int* err)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride)
+        if (ids[i] >= n) atomicOr(err, 1u);
+}
+
+// labels[v] = root(v); P itself is compressed too (no hook runs concurrently).
+__global__ void __launch_bounds__(kBlock) k_labels(uint32_t* P, uint32_t n, uint32_t* out)
+{
+    const uint64_t v64 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v64 >= n) return;
+    const uint32_t v = (uint32_t)v64;
+    const uint32_t p = P[v];
+    uint32_t r = p;
+    if (p != v) {
+        uint32_t q = P[r];
+        while (q != r) { r = q; q = P[r]; }
+        if (r != p) P[v] = r;
+    }
+    out[v] = r;
+}
+
+static unsigned nblocks(int64_t count) { return (unsigned)((count + kBlock - 1) / kBlock); }
+
+static cc_status insert_query(cc_incr* h, const uint32_t* ins, int64_t n_ins, const uint32_t* qs, int64_t n_q,
+                              uint8_t* ans, cudaStream_t s)
+{
+    if (h->flags & CC_FLAG_VALIDATE) {
+        unsigned int* err = nullptr;
+        CC_CUDA_TRY(scratch_alloc((void**)&err, sizeof(unsigned int), s));
+        CC_CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(unsigned int), s));
+        if (n_ins) {
+            k_check_ids<<<num_sms() * 4, kBlock, 0, s>>>(ins, 2 * n_ins, h->n, err);
+            CC_LAUNCH_CHECK("k_check_ids");
+        }
+        if (n_q) {
+            k_check_ids<<<num_sms() * 4, kBlock, 0, s>>>(qs, 2 * n_q, h->n, err);
+            CC_LAUNCH_CHECK("k_check_ids");
+        }
+        unsigned int e = 0;
+        CC_CUDA_TRY(cudaMemcpyAsync(&e, err, sizeof(e), cudaMemcpyDeviceToHost, s));
+        CC_CUDA_TRY(cudaStreamSynchronize(s));
+        scratch_free(err, s);
+        if (e) {
+            set_error("cc_incr_batch: vertex id >= n");
+            return CC_EINVAL;
+        }
+    }
+    if (n_ins > 0) {
+        const uint2* e = reinterpret_cast<const uint2*>(ins);
+        if (h->flags & CC_FLAG_UF_ASYNC) k_insert<2><<<nblocks(n_ins), kBlock, 0, s>>>(h->P, e, n_ins);
+        else if (h->flags & CC_FLAG_HALVE) k_insert<1><<<nblocks(n_ins), kBlock, 0, s>>>(h->P, e, n_ins);
+        else k_insert<0><<<nblocks(n_ins), kBlock, 0, s>>>(h->P, e, n_ins);
+        CC_LAUNCH_CHECK("k_insert");
+    }
+    // ---- kernel boundary: the insert/query barrier of type (3) ----
+    if (n_q > 0) {
+        const uint2* q = reinterpret_cast<const uint2*>(qs);
+        if (h->flags & CC_FLAG_FIND_SPLIT) k_query<true><<<nblocks(n_q), kBlock, 0, s>>>(h->P, q, n_q, ans);
+        else k_query<false><<<nblocks(n_q), kBlock, 0, s>>>(h->P, q, n_q, ans);
+        CC_LAUNCH_CHECK("k_query");
+    }
+    return CC_OK;
+}
+
+}  // namespace ccb
+
+using namespace ccb;
+
+extern "C" {
+
+cc_status cc_incr_create(uint32_t n, const cc_opts* opts, void* stream, cc_incr** out)
+{
+    if (!out) { set_error("out is NULL"); return CC_EINVAL; }
+    *out = nullptr;
+    if (n > 0xFFFFFFFEu) { set_error("n > 0xFFFFFFFE"); return CC_ERANGE; }
+    cudaStream_t s = (cudaStream_t)stream;
+    cc_incr* h = new (std::nothrow) cc_incr{};
+    if (!h) return CC_ENOMEM;
+    h->n = n;
+    h->flags = opts ? opts->flags : 0u;
+    h->last = s;
+    cudaGetDevice(&h->device);
+    cudaError_t e = cudaMalloc((void**)&h->P, sizeof(uint32_t) * std::max<size_t>(n, 1));
+    if (e != cudaSuccess) {
+        delete h;
+        return cuda_fail(e, "cc_incr_create: cudaMalloc");
+    }
+    if (n) {
+        k_iota<<<nblocks(n), kBlock, 0, s>>>(h->P, n);
+        count_launch();
+        e = cudaGetLastError();
+        if (e != cudaSuccess) {
+            cudaFree(h->P);
+            delete h;
+            return cuda_fail(e, "k_iota");
+        }
+    }
+    *out = h;
+    return CC_OK;
+}
+
+cc_status cc_incr_batch(cc_incr* h, const uint32_t* inserts, int64_t n_ins, const uint32_t* queries, int64_t n_q,
+                        uint8_t* answers, void* stream)
+{
+    if (!h) { set_error("handle is NULL"); return CC_EINVAL; }
+    if (n_ins < 0 || n_q < 0) { set_error("negative count"); return CC_EINVAL; }
+    if ((n_ins && !inserts) || (n_q && (!queries || !answers))) { set_error("NULL array"); return CC_EINVAL; }
+    cudaStream_t s = (cudaStream_t)stream;
+    h->last = s;
+    if (h->n == 0) {
+        if (n_ins || n_q) { set_error("ids >= n = 0"); return CC_EINVAL; }
+        return CC_OK;
+    }
+    const bool dev = (!n_ins || is_device_ptr(inserts)) && (!n_q || (is_device_ptr(queries) && is_device_ptr(answers)));
+    if (dev) return insert_query(h, inserts, n_ins, queries, n_q, answers, s);
+    // host buffers: stage
+    std::vector<void*> bufs;
+    auto release = [&]() { for (void* b : bufs) scratch_free(b, s); };
+    const uint32_t* d_ins = inserts;
+    const uint32_t* d_q = queries;
+    uint8_t* d_ans = answers;
+    auto stage_in = [&](const void* host, size_t bytes, void** dev_out) -> cudaError_t {
+        cudaError_t e = scratch_alloc(dev_out, bytes, s);
+        if (e != cudaSuccess) return e;
+        bufs.push_back(*dev_out);
+        return host ? cudaMemcpyAsync(*dev_out, host, bytes, cudaMemcpyHostToDevice, s) : cudaSuccess;
+    };
+    cudaError_t e = cudaSuccess;
+    if (n_ins && !is_device_ptr(inserts)) e = stage_in(inserts, 8 * (size_t)n_ins, (void**)&d_ins);
+    if (e == cudaSuccess && n_q && !is_device_ptr(queries)) e = stage_in(queries, 8 * (size_t)n_q, (void**)&d_q);
+    if (e == cudaSuccess && n_q && !is_device_ptr(answers)) e = stage_in(nullptr, (size_t)n_q, (void**)&d_ans);
+    if (e != cudaSuccess) { release(); return cuda_fail(e, "cc_incr_batch: staging"); }
+    cc_status rc = insert_query(h, d_ins, n_ins, d_q, n_q, d_ans, s);
+    if (rc == CC_OK && n_q && d_ans != answers) {
+        e = cudaMemcpyAsync(answers, d_ans, (size_t)n_q, cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) rc = cuda_fail(e, "cc_incr_batch: answers");
+    }
+    if (rc == CC_OK) {
+        e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) rc = cuda_fail(e, "cc_incr_batch: sync");
+    }
+    release();
+    return rc;
+}
+
+cc_status cc_incr_labels(cc_incr* h, uint32_t* labels, void* stream)
+{
+    if (!h) { set_error("handle is NULL"); return CC_EINVAL; }
+    if (h->n == 0) return CC_OK;
+    if (!labels) { set_error("labels is NULL"); return CC_EINVAL; }
+    cudaStream_t s = (cudaStream_t)stream;
+    h->last = s;
+    uint32_t* d = labels;
+    const bool dev = is_device_ptr(labels);
+    if (!dev) CC_CUDA_TRY(scratch_alloc((void**)&d, sizeof(uint32_t) * h->n, s));
+    k_labels<<<nblocks(h->n), kBlock, 0, s>>>(h->P, h->n, d);
+    CC_LAUNCH_CHECK("k_labels");
+    if (!dev) {
+        CC_CUDA_TRY(cudaMemcpyAsync(labels, d, sizeof(uint32_t) * h->n, cudaMemcpyDeviceToHost, s));
+        CC_CUDA_TRY(cudaStreamSynchronize(s));
+        scratch_free(d, s);
+    }
+    return CC_OK;
+}
+
+void cc_incr_destroy(cc_incr* h)
+{
+    if (!h) return;
+    cudaStreamSynchronize(h->last);
+    cudaFree(h->P);
+    delete h;
+}
+
+uint32_t cc_incr_num_vertices(const cc_incr* h) { return h ? h->n : 0u; }
+
+}  // extern "C"

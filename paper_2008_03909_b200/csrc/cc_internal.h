@@ -1,0 +1,50 @@
+// cc_internal.h -- host-side internals shared by the libcc.so translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <string>
+
+#include "../../include/cc.h"
+
+namespace ccb {
+
+// Thread-local detail string for cc_last_error().
+void set_error(const std::string& msg);
+cc_status cuda_fail(cudaError_t e, const char* where);
+
+// Cumulative count of kernels this library launched (bench evidence).
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+int num_sms();
+bool is_device_ptr(const void* p);
+
+// Stream-ordered scratch from the device's default memory pool (cached).
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s);
+void scratch_free(void* p, cudaStream_t s);
+
+constexpr int kBlock = 256;
+
+#define CC_CUDA_TRY(expr)                                         \
+    do {                                                          \
+        cudaError_t _e = (expr);                                  \
+        if (_e != cudaSuccess) return ::ccb::cuda_fail(_e, #expr); \
+    } while (0)
+
+// Launch-error check after a <<<>>> launch.
+#define CC_LAUNCH_CHECK(name)                                     \
+    do {                                                          \
+        ::ccb::count_launch();                                    \
+        cudaError_t _e = cudaGetLastError();                      \
+        if (_e != cudaSuccess) return ::ccb::cuda_fail(_e, name); \
+    } while (0)
+
+// Device pipeline entry points (device pointers only; validated args).
+cc_status static_pipeline(const int64_t* off, const uint32_t* adj, uint32_t n, int64_t m,
+                          uint32_t* labels, uint32_t* edges, int64_t* num_edges, bool sf,
+                          const cc_opts& o, cudaStream_t s);
+cc_status validate_csr(const int64_t* off, const uint32_t* adj, uint32_t n, int64_t m, cudaStream_t s);
+
+}  // namespace ccb

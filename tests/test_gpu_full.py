@@ -1,0 +1,77 @@
+"""Full-size BASELINE.json configs (C1-C5), in the launch configuration bench.py times.
+
+The graphs come from the CUDA generator (byte-identical to inputs/gen.py, see
+test_gpu_gen.py); the oracle runs on the host over the same bytes.  Labels and
+answers are compared element by element (bit-exact); forests by the validity
+triple.  These are minutes-long on one B200 + its host cores."""
+import time
+
+import numpy as np
+import pytest
+
+import inputs
+import oracle
+from tests.helpers import u32
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2008_03909_b200 as pkg  # noqa: E402
+from inputs import gpu as ggen  # noqa: E402
+
+
+def host(t, dtype):
+    return t.cpu().numpy().view(dtype)
+
+
+@pytest.mark.parametrize("cfg", [inputs.C1, inputs.C2, inputs.C3, inputs.C4], ids=lambda c: c.name)
+def test_static_config_bit_exact(cfg):
+    t0 = time.time()
+    d_off, d_adj = ggen.config_graph(cfg)
+    lab = pkg.connected_components(d_off, d_adj)
+    edges, lab2 = pkg.spanning_forest(d_off, d_adj)
+    torch.cuda.synchronize()
+    got = u32(lab)
+    got2 = u32(lab2)
+    E = u32(edges)
+    off = host(d_off, np.int64)
+    adj = host(d_adj, np.uint32)
+    del d_off, d_adj
+    torch.cuda.empty_cache()
+    t1 = time.time()
+    want = oracle.cc_bfs(off, adj)
+    t2 = time.time()
+    n = off.size - 1
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, (cfg.name, bad[:5], got[bad[:5]], want[bad[:5]])
+    assert np.array_equal(got2, want)
+    c = int(np.sum(want == np.arange(n)))
+    rc, idx = oracle.forest_check(off, adj, c, E)
+    assert rc == 0, (oracle.FOREST_ERRORS[rc], idx)
+    print(f"{cfg.name}: n={n} m={adj.size} components={c} gpu+copy {t1 - t0:.1f}s oracle {t2 - t1:.1f}s")
+
+
+def test_incremental_config_bit_exact():
+    cfg = inputs.C5
+    n = 1 << cfg.scale
+    inc = pkg.IncrementalCC(n)
+    ins = torch.empty((cfg.n_ins, 2), dtype=torch.int32, device="cuda")
+    qs = torch.empty((cfg.n_q, 2), dtype=torch.int32, device="cuda")
+    answers, h_ins, h_qs = [], [], []
+    for b in range(cfg.n_batches):
+        ggen.incr_batch(cfg.seed, cfg.scale, b, cfg.n_ins, cfg.n_q, ins, qs)
+        a = inc.batch(ins, qs)
+        answers.append(a.cpu().numpy())
+        h_ins.append(host(ins, np.uint32).copy())
+        h_qs.append(host(qs, np.uint32).copy())
+    lab = u32(inc.labels())
+    inc.close()
+    got = np.concatenate(answers)
+    want, want_lab = oracle.incr_run(n, list(zip(h_ins, h_qs)), want_labels=True)
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, bad[:5]
+    assert np.array_equal(lab, want_lab)
+    print(f"C5: {got.size} answers, {int(want.sum())} true")

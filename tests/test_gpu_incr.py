@@ -1,0 +1,120 @@
+"""GPU parity of the batch-incremental path (cc_incr_*) vs the sequential DSU oracle.
+
+Answers must be bit-exact (reading R15: a query sees all inserts of its own
+batch).  cc_incr_labels after the stream must equal the static oracle on the
+union of the inserts (cross-pins the static and incremental paths)."""
+import numpy as np
+import pytest
+
+import oracle
+from inputs import gen
+from tests.helpers import u32
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2008_03909_b200 as pkg  # noqa: E402
+from paper_2008_03909_b200 import cc  # noqa: E402
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint32).view(np.int32).reshape(-1, 2)).cuda()
+
+
+def run_stream(n, batches, flags=0):
+    inc = pkg.IncrementalCC(n, flags=flags)
+    outs = []
+    for ins, qs in batches:
+        a = inc.batch(dev(ins), dev(qs))
+        outs.append(a.cpu().numpy())
+    lab = u32(inc.labels())
+    inc.close()
+    return np.concatenate(outs) if outs else np.zeros(0, np.uint8), lab
+
+
+def static_labels(n, batches):
+    pairs = np.concatenate([np.asarray(b[0], dtype=np.uint32).reshape(-1, 2) for b in batches])
+    off, adj = oracle.csr_from_pairs(n, pairs)
+    return oracle.cc_bfs(off, adj)
+
+
+@pytest.mark.parametrize("flags", [0, cc.FLAG_HALVE, cc.FLAG_UF_ASYNC, cc.FLAG_FIND_SPLIT])
+@pytest.mark.parametrize("batch", [1, 10, 1000, 1 << 14])
+def test_stream_bit_exact(flags, batch):
+    scale = 12
+    n = 1 << scale
+    total = 3 * (1 << 14) if batch >= 1000 else 400
+    n_ins = max(1, int(batch * 0.9))
+    n_q = max(1, batch - n_ins)
+    nb = max(1, total // batch)
+    batches = [gen.incr_batch(seed=5, scale=scale, b=b, n_ins=n_ins, n_q=n_q) for b in range(nb)]
+    want, want_lab = oracle.incr_run(n, batches, want_labels=True)
+    got, lab = run_stream(n, batches, flags)
+    assert np.array_equal(got, want), (flags, batch, np.nonzero(got != want)[0][:5])
+    assert np.array_equal(lab, want_lab)
+    assert np.array_equal(lab, static_labels(n, batches))
+
+
+def test_true_heavy_stream():
+    """Half the queries are endpoints of earlier inserts (guaranteed 1), half join
+    random vertices of the current giant -- catches an 'always 0' bug."""
+    rng = np.random.default_rng(4)
+    n = 1 << 13
+    batches = []
+    prev = np.zeros((0, 2), dtype=np.uint32)
+    for b in range(40):
+        ins, _ = gen.incr_batch(seed=6, scale=13, b=b, n_ins=2000, n_q=1)
+        pool = np.concatenate([prev, ins])
+        pick = pool[rng.integers(0, pool.shape[0], 300)]
+        mixed = np.stack([pick[:, 0], pool[rng.integers(0, pool.shape[0], 300), 1]], 1)
+        qs = np.concatenate([pick, mixed, rng.integers(0, n, (50, 2)).astype(np.uint32)])
+        batches.append((ins, qs))
+        prev = pool
+    want, _ = oracle.incr_run(n, batches)
+    got, _ = run_stream(n, batches)
+    assert np.array_equal(got, want)
+    assert want.mean() > 0.5
+
+
+def test_closed_forms_and_monotone():
+    n = 64
+    batches = [
+        (np.array([[0, 1], [1, 2]]), np.array([[0, 2], [3, 3], [0, 3]])),
+        (np.array([[2, 3], [5, 5], [5, 5]]), np.array([[0, 3], [5, 9], [3, 0], [5, 5]])),
+        (np.zeros((0, 2), int), np.array([[0, 2], [0, 3], [63, 63], [62, 63]])),
+        (np.array([[62, 63]]), np.zeros((0, 2), int)),
+        (np.zeros((0, 2), int), np.array([[62, 63]])),
+    ]
+    got, lab = run_stream(n, batches)
+    assert got.tolist() == [1, 1, 0, 1, 0, 1, 1, 1, 1, 1, 0, 1]
+    assert lab[3] == 0 and lab[63] == 62
+
+
+def test_validate_and_errors():
+    inc = pkg.IncrementalCC(100, flags=cc.FLAG_VALIDATE)
+    with pytest.raises(cc.CCError):
+        inc.batch(dev([[1, 2], [3, 100]]), dev([[0, 1]]))
+    # the failed batch applied nothing
+    a = inc.batch(dev([[5, 6]]), dev([[1, 2], [5, 6]]))
+    assert a.cpu().tolist() == [0, 1]
+    inc.close()
+
+
+def test_host_buffers():
+    n = 1 << 10
+    batches = [gen.incr_batch(seed=8, scale=10, b=b, n_ins=300, n_q=100) for b in range(5)]
+    want, want_lab = oracle.incr_run(n, batches, want_labels=True)
+    h = cc.Incr(n)
+    outs = []
+    for ins, qs in batches:
+        ans = np.zeros(qs.shape[0], dtype=np.uint8)
+        h.batch(np.ascontiguousarray(ins), ins.shape[0], np.ascontiguousarray(qs), qs.shape[0], ans)
+        outs.append(ans)
+    lab = np.zeros(n, dtype=np.uint32)
+    h.labels(lab)
+    h.close()
+    assert np.array_equal(np.concatenate(outs), want)
+    assert np.array_equal(lab, want_lab)

@@ -1,0 +1,271 @@
+"""GPU parity of the static path (cc_labels, cc_spanning_forest) vs the CPU oracle.
+
+Bit-exact: labels are compared raw (canonical min-id form, reading R13) to
+oracle.cc_bfs.  Forests: the oracle's validity triple plus bit-exact labels.
+All calls go through the C ABI (libcc.so via paper_2008_03909_b200.cc).
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle
+from inputs import gen
+from tests.helpers import csr, fixtures, to_dev, u32
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2008_03909_b200 as pkg  # noqa: E402
+from paper_2008_03909_b200 import cc  # noqa: E402
+
+OPTION_GRID = [
+    dict(k=2, variant="afforest", flags=0),
+    dict(k=0, variant="afforest", flags=0),
+    dict(k=1, variant="afforest", flags=0),
+    dict(k=3, variant="afforest", flags=0),
+    dict(k=2, variant="hybrid", flags=0, seed=7),
+    dict(k=3, variant="hybrid", flags=0, seed=11),
+    dict(k=2, variant="afforest", flags=cc.FLAG_HALVE),
+    dict(k=2, variant="afforest", flags=cc.FLAG_UF_ASYNC),
+    dict(k=2, variant="afforest", flags=cc.FLAG_NO_SKIP),
+    dict(k=2, variant="afforest", flags=cc.FLAG_NO_DEGSKIP | cc.FLAG_NO_MIDCOMPRESS),
+    dict(k=64, variant="afforest", flags=0),
+]
+
+
+def run_labels(off, adj, **kw):
+    d_off, d_adj = to_dev(off, adj)
+    lab = pkg.connected_components(d_off, d_adj, **kw)
+    torch.cuda.synchronize()
+    return u32(lab)
+
+
+def small_graphs():
+    G = [(name, off, adj) for name, off, adj in fixtures()]
+    G.append(("er_small", *gen.er(seed=3, n0=5000, pairs=6000, isolated=37)))
+    G.append(("er_sparse", *gen.er(seed=4, n0=20000, pairs=9000, isolated=5)))
+    G.append(("grid_ragged", *gen.grid(seed=5, rows=67, cols=131)))
+    G.append(("rmat10", *gen.rmat(seed=6, scale=10)))
+    G.append(("rmat13_unperm", *gen.rmat(seed=7, scale=13, permuted=False)))
+    return G
+
+
+@pytest.mark.parametrize("opt", OPTION_GRID, ids=lambda o: f"k{o['k']}-{o['variant']}-f{o['flags']}")
+def test_labels_bit_exact_small(opt):
+    for name, off, adj in small_graphs():
+        want = oracle.cc_bfs(off, adj)
+        got = run_labels(off, adj, **opt)
+        assert np.array_equal(got, want), (name, opt, np.nonzero(got != want)[0][:5])
+
+
+@pytest.mark.parametrize("scale", [12, 15])
+def test_labels_rmat_several_tiles(scale):
+    off, adj = gen.rmat(seed=8, scale=scale)
+    want = oracle.cc_bfs(off, adj)
+    for opt in OPTION_GRID[:6]:
+        assert np.array_equal(run_labels(off, adj, **opt), want), opt
+
+
+def test_labels_grid_and_er_mid():
+    for off, adj in (gen.grid(seed=2, rows=512, cols=384), gen.er(seed=1)):
+        want = oracle.cc_bfs(off, adj)
+        for opt in (OPTION_GRID[0], OPTION_GRID[1], OPTION_GRID[4]):
+            assert np.array_equal(run_labels(off, adj, **opt), want), opt
+
+
+# ---------------------------------------------------------------------------
+def test_sampled_labels_are_cc_of_the_sampled_edges():
+    """H2+H3: after the sampling compress, P is height-one (Def. 3.1)
+    and -- by the min-root invariant -- equals the canonical CC labels of the
+    sampled edge set (Alg. 4); H4 returns the mode of the seeded samples."""
+    graphs = [gen.rmat(seed=9, scale=12), gen.grid(seed=3, rows=100, cols=77), gen.er(seed=2, n0=3000, pairs=4000)]
+    graphs += [(o, a) for _, o, a in fixtures()]
+    for off, adj in graphs:
+        n = off.size - 1
+        for k, variant, seed in [(1, "afforest", 0), (2, "afforest", 0), (3, "afforest", 0), (2, "hybrid", 5),
+                                 (4, "hybrid", 99)]:
+            d_off, d_adj = to_dev(off, adj)
+            sampled = torch.empty(n, dtype=torch.int32, device="cuda")
+            lmax = torch.empty(1, dtype=torch.int32, device="cuda")
+            lab = pkg.connected_components(d_off, d_adj, k=k, variant=variant, seed=seed, sampled_out=sampled,
+                                           lmax_out=lmax)
+            E = oracle.kout_sample_edges(off, adj, k, variant, seed)
+            o2, a2 = oracle.csr_from_pairs(n, E)
+            want_s = oracle.cc_bfs(o2, a2)
+            got_s = u32(sampled)
+            assert np.array_equal(got_s, want_s), (k, variant)
+            assert np.array_equal(got_s[got_s], got_s)                   # height-one
+            assert int(u32(lmax)[0]) == oracle.identify_frequent(want_s, 1024, seed)
+            assert np.array_equal(u32(lab), oracle.cc_bfs(off, adj))
+
+
+def test_lmax_forcing_changes_nothing():
+    off, adj = gen.rmat(seed=10, scale=12)
+    n = off.size - 1
+    want = oracle.cc_bfs(off, adj)
+    roots = np.unique(want)
+    for forced in [int(roots[0]), int(roots[-1]), int(roots[len(roots) // 2]), 0xFFFFFFFF, n - 1, 12345 % n]:
+        f = torch.tensor([np.uint32(forced).view(np.int32)], dtype=torch.int32, device="cuda")
+        for k in (0, 1, 2):
+            d_off, d_adj = to_dev(off, adj)
+            lab = pkg.connected_components(d_off, d_adj, k=k, lmax_force=f)
+            assert np.array_equal(u32(lab), want), (forced, k)
+
+
+def test_permutation_and_list_order_metamorphic():
+    off, adj = gen.rmat(seed=12, scale=11, permuted=False)
+    n = off.size - 1
+    base = oracle.cc_bfs(off, adj)
+    rng = np.random.default_rng(0)
+    pi = rng.permutation(n).astype(np.uint32)
+    src = np.repeat(np.arange(n, dtype=np.uint32), np.diff(off))
+    o2, a2 = gen.csr_from_directed_pairs(n, pi[src], pi[adj])
+    got = run_labels(o2, a2)
+    # canonical labels of the permuted graph = canon(pi(base labels))
+    want = oracle.canon(base[np.argsort(pi)])
+    assert np.array_equal(got, want)
+    # shuffle every adjacency list (first-k edges change; labels must not)
+    a3 = adj.copy()
+    for v in range(n):
+        seg = a3[off[v]:off[v + 1]]
+        rng.shuffle(seg)
+    for k in (1, 2, 3):
+        assert np.array_equal(run_labels(off, a3, k=k), base)
+
+
+def test_host_buffers_equal_device():
+    off, adj = gen.rmat(seed=13, scale=11)
+    n = off.size - 1
+    out = np.zeros(n, dtype=np.uint32)
+    cc.cc_labels(off, adj, n, adj.size, out, cc.make_opts())
+    assert np.array_equal(out, oracle.cc_bfs(off, adj))
+    edges = np.zeros(2 * n, dtype=np.uint32)
+    ne = np.zeros(1, dtype=np.int64)
+    lab = np.zeros(n, dtype=np.uint32)
+    cc.cc_spanning_forest(off, adj, n, adj.size, edges, ne, lab, cc.make_opts())
+    c = int(np.sum(lab == np.arange(n)))
+    assert np.array_equal(lab, oracle.cc_bfs(off, adj))
+    assert oracle.forest_check(off, adj, c, edges[:2 * ne[0]])[0] == 0
+
+
+def test_validate_flag_rejects_malformed():
+    off, adj = gen.rmat(seed=14, scale=8)
+    n = off.size - 1
+    bad = adj.copy()
+    bad[3] = n + 5
+    d_off, d_adj = to_dev(off, bad)
+    lab = torch.empty(n, dtype=torch.int32, device="cuda")
+    with pytest.raises(cc.CCError):
+        cc.cc_labels(d_off, d_adj, n, bad.size, lab, cc.make_opts(flags=cc.FLAG_VALIDATE))
+    off2 = off.copy()
+    off2[n // 2] = off2[n // 2 + 1] + 1
+    d_off, d_adj = to_dev(off2, adj)
+    with pytest.raises(cc.CCError):
+        cc.cc_labels(d_off, d_adj, n, adj.size, lab, cc.make_opts(flags=cc.FLAG_VALIDATE))
+    d_off, d_adj = to_dev(off, adj)
+    cc.cc_labels(d_off, d_adj, n, adj.size, lab, cc.make_opts(flags=cc.FLAG_VALIDATE))
+    assert np.array_equal(u32(lab), oracle.cc_bfs(off, adj))
+
+
+def test_empty_and_degenerate_abi():
+    # n = 0: OK, no work
+    z = torch.zeros(1, dtype=torch.int64, device="cuda")
+    cc.cc_labels(z, None, 0, 0, None)
+    num = torch.full((1,), 7, dtype=torch.int64, device="cuda")
+    cc.cc_spanning_forest(z, None, 0, 0, None, num)
+    assert int(num.item()) == 0
+    # m = 0: identity
+    off = np.zeros(1001, dtype=np.int64)
+    got = run_labels(off, np.zeros(0, dtype=np.uint32))
+    assert np.array_equal(got, np.arange(1000, dtype=np.uint32))
+
+
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("opt", [OPTION_GRID[0], OPTION_GRID[1], OPTION_GRID[4], OPTION_GRID[6], OPTION_GRID[7]],
+                         ids=lambda o: f"k{o['k']}-{o['variant']}-f{o['flags']}")
+def test_spanning_forest_valid(opt):
+    for name, off, adj in small_graphs():
+        n = off.size - 1
+        want = oracle.cc_bfs(off, adj)
+        c = int(np.sum(want == np.arange(n)))
+        d_off, d_adj = to_dev(off, adj)
+        edges, lab = pkg.spanning_forest(d_off, d_adj, **opt)
+        E = u32(edges).reshape(-1, 2)
+        rc, bad = oracle.forest_check(off, adj, c, E)
+        assert rc == 0, (name, opt, oracle.FOREST_ERRORS[rc], bad)
+        assert np.array_equal(u32(lab), want), name
+        # each slot holds the edge that hooked root r: emitted in ascending slot order,
+        # and the hooked slot (the larger root) is never a final root
+        assert E.shape[0] == n - c
+
+
+def test_spanning_forest_without_labels():
+    off, adj = gen.grid(seed=6, rows=90, cols=70)
+    n = off.size - 1
+    d_off, d_adj = to_dev(off, adj)
+    edges, lab = pkg.spanning_forest(d_off, d_adj, with_labels=False)
+    assert lab is None
+    want = oracle.cc_bfs(off, adj)
+    c = int(np.sum(want == np.arange(n)))
+    assert oracle.forest_check(off, adj, c, u32(edges))[0] == 0
+
+
+def test_repeat_stress_random_options():
+    """Races must never change the answer: repeat with random k, variant, seed, flags."""
+    off, adj = gen.er(seed=21, n0=30000, pairs=45000, isolated=11)
+    want = oracle.cc_bfs(off, adj)
+    rng = np.random.default_rng(1)
+    d_off, d_adj = to_dev(off, adj)
+    flags_pool = [0, cc.FLAG_HALVE, cc.FLAG_UF_ASYNC, cc.FLAG_NO_SKIP, cc.FLAG_NO_MIDCOMPRESS, cc.FLAG_NO_DEGSKIP]
+    for it in range(200):
+        k = int(rng.integers(0, 5))
+        variant = ["afforest", "hybrid"][int(rng.integers(0, 2))]
+        fl = int(rng.choice(flags_pool)) | int(rng.choice(flags_pool))
+        lab = pkg.connected_components(d_off, d_adj, k=k, variant=variant, seed=int(rng.integers(0, 1 << 30)),
+                                       flags=fl)
+        assert np.array_equal(u32(lab), want), (it, k, variant, fl)
+
+
+def test_counters_and_timings():
+    off, adj = gen.rmat(seed=15, scale=12)
+    n = off.size - 1
+    d_off, d_adj = to_dev(off, adj)
+    ctr = torch.zeros(8, dtype=torch.int64, device="cuda")
+    t = cc.Timings()
+    lab = torch.empty(n, dtype=torch.int32, device="cuda")
+    cc.cc_labels(d_off, d_adj, n, adj.size, lab, cc.make_opts(counters=ctr, timings=t))
+    c = dict(zip(cc.COUNTER_FIELDS, ctr.cpu().tolist()))
+    deg = np.diff(off)
+    assert c["pending_links"] == int(np.minimum(deg, 2).sum()) - int(
+        sum(1 for v in range(n) if deg[v] > 0 and adj[off[v]] < v))
+    assert c["finish_vertices"] <= int((deg > 2).sum())
+    assert t.total_ms > 0
+    assert np.array_equal(u32(lab), oracle.cc_bfs(off, adj))
+
+
+def test_microbenchmarks():
+    off, adj = gen.rmat(seed=16, scale=11)
+    n = off.size - 1
+    d_off, d_adj = to_dev(off, adj)
+    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    cc.map_edges(d_off, d_adj, n, out)
+    assert np.array_equal(u32(out), np.diff(off).astype(np.uint32))
+    x = np.random.default_rng(0).integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+    dx = torch.from_numpy(x.view(np.int32)).cuda()
+    cc.gather_edges(d_off, d_adj, n, dx, out)
+    src = np.repeat(np.arange(n), np.diff(off))
+    want = np.zeros(n, dtype=np.uint64)
+    np.add.at(want, src, x[adj].astype(np.uint64))
+    assert np.array_equal(u32(out), (want & 0xFFFFFFFF).astype(np.uint32))
+    s = torch.zeros(1, dtype=torch.int32, device="cuda")
+    cc.random_gather(dx, n, 10000, 3, s)
+    idx = ((oracle.splitmix64(np.arange(10000, dtype=np.uint64) + np.uint64(3)) & np.uint64(0xFFFFFFFF))
+           * np.uint64(n)) >> np.uint64(32)
+    assert int(u32(s)[0]) == int(x[idx.astype(np.int64)].astype(np.uint64).sum() & 0xFFFFFFFF)
+    dst = torch.empty_like(dx)
+    cc.copy(dx, dst, n - n % 4)
+    assert torch.equal(dst[: n - n % 4], dx[: n - n % 4])
