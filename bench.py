@@ -1,0 +1,451 @@
+#!/usr/bin/env python
+"""bench.py -- the driver contract for the ConnectIt connectivity hot path on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+
+A step is one cc_labels call (H1-H6: init, k-out sampling, IdentifyFrequent,
+finish, compress) on the resident synthetic graph of BASELINE.json config
+`--config` (default 4 = RMAT scale 27, configs[3]; the metric names no config,
+so the largest single-GPU one is the workload).  `value` is GTEPS =
+directed edges / second summed over ranks (each rank runs an independent
+replica: the north_star path is one GPU, "replicas only").
+`--config 5` times the incremental stream (256 batches) instead, in Gops/s.
+
+Prints ONE JSON line on rank 0 (see DESIGN.md §Measurement for every key).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CPU_SAMPLE_SCALE = 23            # oracle sample: RMAT scale 23, same a/b/c/d as C4
+HBM_FALLBACK_GBS = 6650.0        # B200_PROFILING.md fallback if MEASURED_PEAKS.json is absent
+CONTRACT_GBS = 8000.0            # BASELINE.json bar: % of 8 TB/s
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--k", type=int, default=2)
+    p.add_argument("--variant", default="afforest", choices=["afforest", "hybrid"])
+    p.add_argument("--flags", type=int, default=0)
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-scale", type=int, default=CPU_SAMPLE_SCALE)
+    p.add_argument("--l2-fetch", type=int, default=-1, help="cudaLimitMaxL2FetchGranularity (bytes) or -1")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing (replicas: the only collectives are barrier + max of the timings)
+def dist_setup():
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    return rank, ws
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def reduce_max(x: float, ws: int) -> float:
+    """Max over ranks (device-timed numbers are aggregated as the max, never wall clock)."""
+    if ws == 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def aggregate_value(units_per_rank: float, max_seconds: float, ws: int) -> float:
+    """Whole-job throughput: units all ranks processed / the slowest rank's time."""
+    return units_per_rank * ws / max_seconds
+
+
+# ---------------------------------------------------------------------------
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.2)
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.count(",") >= 5]
+        os.unlink(self.f.name)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[2 + i] and "Not" not in r[2 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def peaks():
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel: str):
+    """dram read+write bytes per launch from a committed `ncu --set full` capture, if any."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        return d.get(kernel)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+def cpu_oracle_sample(scale: int, use_gpu_gen: bool):
+    """Time the oracle (as it stands, 1 thread) on an RMAT-`scale` sample of the C4 recipe."""
+    import numpy as np
+
+    import oracle
+    from inputs import gen
+    if use_gpu_gen:
+        from inputs import gpu as ggen
+        d_off, d_adj = ggen.rmat(4, scale)
+        off = d_off.cpu().numpy()
+        adj = d_adj.cpu().numpy().view(np.uint32)
+        del d_off, d_adj
+    else:
+        off, adj = gen.rmat(4, scale)
+    t0 = time.perf_counter()
+    lab = oracle.cc_bfs(off, adj)
+    dt = time.perf_counter() - t0
+    return adj.size, dt, off, adj, lab
+
+
+def run_reference(a, rank, ws):
+    """--impl reference: the CPU oracle on the box's host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    import torch
+    use_gpu = torch.cuda.is_available()
+    import inputs
+    cfg = inputs.BY_INDEX[a.config]
+    times, m = [], 0
+    for i in range(a.warmup + a.steps):
+        m, dt, *_ = cpu_oracle_sample(a.cpu_scale, use_gpu)
+        if i >= a.warmup:
+            times.append(dt)
+    t = sum(times) / len(times)
+    value = m / t / 1e9
+    sample = f"oracle.cc_bfs (sequential BFS, 1 thread) on RMAT scale {a.cpu_scale} (C4 recipe a/b/c/d=.57/.19/.19/.05, ef 16, seed 4), m={m}"
+    line = {"impl": "reference", "metric": "connectivity edges/sec (GTEPS)", "value": value, "unit": "GTEPS",
+            "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic", "config": {"workload": cfg.name, "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def byte_model(off_h_deg_pos, n, m, k, ctr, sampled, final, skip_prefix):
+    """Algorithmic bytes per launch of each kernel.
+
+    Counts only what the implemented design must move (SURVEY §8(d) honesty
+    rules): 4 B per uint32 read/written, 8 B per int64 offset."""
+    import numpy as np
+    npos, sum_mink = off_h_deg_pos
+    pend = ctr["pending_links"]
+    fin_v, fin_e = ctr["finish_vertices"], ctr["finish_edges"]
+    relab = int(np.count_nonzero(final != sampled))          # H6 label writes
+    nonroot = int(np.count_nonzero(sampled != np.arange(n, dtype=np.uint32)))
+    B = {
+        # offsets (n+1) + first-k adj entries + P write + pending writes + finish bitmap
+        "k_sample_init": 8 * (n + 1) + 4 * sum_mink + 4 * n + 8 * pend + n // 8,
+        # P read + one first-level parent read per non-isolated vertex (upper bound of the non-roots)
+        "k_compress_mid": 4 * n + 4 * npos,
+        # pending read + P[u], P[v] gathers + hook CAS
+        "k_link_pending": 8 * pend + 8 * pend + 4 * ctr["sample_hooks"],
+        "k_identify": 4 * 1024,
+        # fused H3 + H5 scan: P read + bitmap + compress writes + candidate queue writes
+        "k_finish": 4 * n + n // 8 + 4 * ctr["compress_writes"] + 4 * fin_v,
+        # H5 edge work: queue read + offsets pair + adj + P[v] gather per edge + hook CAS
+        "k_finish_proc": 4 * fin_v + 16 * fin_v + 8 * fin_e + 4 * ctr["finish_hooks"],
+        # P read + changed-label writes
+        "k_compress_H6": 4 * n + 4 * relab,
+    }
+    B["finish_phase"] = B["k_finish"] + B["k_finish_proc"] + B["k_compress_H6"]
+    B["sampling_phase"] = B["k_sample_init"] + B["k_compress_mid"] + B["k_link_pending"]
+    return B, {"relabelled": relab, "sampled_nonroots": nonroot, "mid_nonroots_bound": npos}
+
+
+def run_ours(a, rank, ws):
+    import numpy as np
+    import torch
+
+    import inputs
+    from inputs import gpu as ggen
+    from paper_2008_03909_b200 import cc
+
+    cfg = inputs.BY_INDEX[a.config]
+    l2_fetch_prev = cc.set_l2_fetch(a.l2_fetch) if a.l2_fetch >= 0 else None
+    if cfg.kind == "incr":
+        return run_ours_incr(a, rank, ws, cfg)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    tg = time.time()
+    d_off, d_adj = ggen.config_graph(cfg)
+    torch.cuda.synchronize()
+    gen_s = time.time() - tg
+    n, m = d_off.numel() - 1, d_adj.numel()
+    labels = torch.empty(n, dtype=torch.int32, device=dev)
+    variant = cc.VARIANT_AFFOREST if a.variant == "afforest" else cc.VARIANT_HYBRID
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = torch.empty(2 * l2 // 4 + 1024, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def call(marks=None, **kw):
+        o = cc.make_opts(k=a.k, variant=variant, flags=a.flags, marks=marks, **kw)
+        cc.cc_labels(d_off, d_adj, n, m, labels, o, stream)
+
+    # ---- diagnostics run (untimed): counters + sampled labels for the byte model
+    ctr_t = torch.zeros(8, dtype=torch.int64, device=dev)
+    sampled_t = torch.empty(n, dtype=torch.int32, device=dev)
+    call(counters=ctr_t)              # counters of the production path (H3 fused into k_finish)
+    call(sampled_out=sampled_t)       # sampled labels (this debug call runs H3 as its own pass)
+    torch.cuda.synchronize()
+    ctr = dict(zip(cc.COUNTER_FIELDS, ctr_t.cpu().tolist()))
+    sampled = sampled_t.cpu().numpy().view(np.uint32)
+    final = labels.cpu().numpy().view(np.uint32)
+    deg = torch.diff(d_off)
+    sum_mink = int(torch.clamp(deg, max=a.k).sum().item())
+    nonisolated = int((deg > 0).sum().item())
+    del sampled_t, deg
+    skip_prefix = a.k if a.variant == "afforest" else min(a.k, 1)
+    B, extra = byte_model((nonisolated, sum_mink), n, m, a.k, ctr, sampled, final, skip_prefix)
+    components = int(np.count_nonzero(final == np.arange(n, dtype=np.uint32)))
+
+    # ---- warm-up
+    for _ in range(a.warmup):
+        flush.zero_()
+        call()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, each bracketed by its own events; L2 flushed between steps
+    clk = Clocks(torch.cuda.current_device())
+    clk.start()
+    marks = [[torch.cuda.Event(enable_timing=True) for _ in range(cc.NUM_MARKS)] for _ in range(a.steps)]
+    for row in marks:
+        for e in row:
+            e.record(stream)          # materialise the lazily created events
+    torch.cuda.synchronize()
+    barrier(ws)
+    torch.cuda.synchronize()
+    outer = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    l0 = cc.launch_count()
+    for i in range(a.steps):
+        flush.zero_()
+        outer[i][0].record(stream)
+        call(marks=[e.cuda_event for e in marks[i]])
+        outer[i][1].record(stream)
+    torch.cuda.synchronize()
+    barrier(ws)
+    torch.cuda.synchronize()
+    launches = cc.launch_count() - l0
+    clocks = clk.stop()
+    step_ms = [outer[i][0].elapsed_time(outer[i][1]) for i in range(a.steps)]
+    kern_ms = {}
+    for j in range(1, cc.NUM_MARKS):
+        kern_ms[cc.MARK_NAMES[j]] = statistics.mean(marks[i][j - 1].elapsed_time(marks[i][j]) for i in range(a.steps))
+    mean_ms = statistics.mean(step_ms)
+    max_ms = reduce_max(mean_ms, ws)
+    value = aggregate_value(m, max_ms * 1e-3, ws) / 1e9
+
+    peak, peak_src = peaks()
+    kernels = {}
+    for kname, t in kern_ms.items():
+        if kname in B and t > 0:
+            gbs = B[kname] / (t * 1e-3) / 1e9
+            kernels[kname] = {"ms": round(t, 5), "bytes": int(B[kname]), "GB/s": round(gbs, 1),
+                              "frac": round(gbs / peak, 4), "share": round(t / mean_ms, 4)}
+    dom = max(kernels, key=lambda k: kernels[k]["ms"])
+    dk = kernels[dom]
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": dk["GB/s"], "peak": peak, "unit": "GB/s",
+                "frac": dk["frac"], "traffic": ncu_traffic(dom), "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": dk["bytes"], "launch_ms": dk["ms"]}
+    fin_ms = kern_ms["k_finish"] + kern_ms["k_finish_proc"] + kern_ms["k_compress_H6"]
+    fin_gbs = B["finish_phase"] / (fin_ms * 1e-3) / 1e9
+    smp_ms = sum(kern_ms[x] for x in ("k_sample_init", "k_compress_mid", "k_link_pending"))
+    finish = {"scope": "H3 compress fused with the H5 scan (k_finish) + H5 edge work (k_finish_proc, "
+                       "k_finish_big) + H6 (k_compress_H6)", "ms": round(fin_ms, 5), "bytes": int(B["finish_phase"]), "GB/s": round(fin_gbs, 1),
+              "frac_of_8TBs": round(fin_gbs / CONTRACT_GBS, 4), "frac_of_measured": round(fin_gbs / peak, 4)}
+    sampling = {"ms": round(smp_ms, 5), "bytes": int(B["sampling_phase"]),
+                "GB/s": round(B["sampling_phase"] / (smp_ms * 1e-3) / 1e9, 1)}
+
+    line = {"metric": "connectivity edges/sec (GTEPS)", "value": round(value, 4), "unit": "GTEPS",
+            "n_gpus": ws, "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(max_ms, 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic",
+            "config": {"workload": cfg.name, "n": n, "m_directed": m, "kout_k": a.k, "variant": a.variant,
+                       "flags": a.flags, "seed": cfg.seed, "components": components,
+                       "l2": f"flushed between steps (write {flush.numel() * 4 >> 20} MiB > L2 {l2 >> 20} MiB); "
+                             f"CSR {(8 * (n + 1) + 4 * m) / 1e9:.1f} GB > L2",
+                       "parallelism": f"replicas x{ws}", "gen_s": round(gen_s, 2),
+                       "l2_fetch_granularity": a.l2_fetch if a.l2_fetch >= 0 else "driver default"},
+            "roofline": roofline, "finish": finish, "sampling": sampling, "kernels": kernels,
+            "counters": ctr, "byte_model_extra": extra, "gpu_launches": int(launches), "clocks": clocks}
+
+    # ---- e2e: the same metric through the C ABI with HOST (pinned) buffers
+    if not a.no_e2e and a.e2e_steps > 0:
+        h_off = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
+        h_adj = torch.empty(m, dtype=torch.int32, pin_memory=True)
+        h_lab = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        h_off.copy_(d_off)
+        h_adj.copy_(d_adj)
+        torch.cuda.synchronize()
+        ts = []
+        for i in range(1 + a.e2e_steps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            cc.cc_labels(h_off.data_ptr(), h_adj.data_ptr(), n, m, h_lab.data_ptr(),
+                         cc.make_opts(k=a.k, variant=variant, flags=a.flags), stream)
+            e1.record(stream)
+            e1.synchronize()
+            if i > 0:
+                ts.append(e0.elapsed_time(e1))
+        e2e_ms = reduce_max(statistics.mean(ts), ws)
+        ok = bool(np.array_equal(h_lab.numpy().view(np.uint32), final))
+        line["e2e"] = {"value": round(aggregate_value(m, e2e_ms * 1e-3, ws) / 1e9, 4), "unit": "GTEPS",
+                       "h2d_bytes_per_step": 8 * (n + 1) + 4 * m, "d2h_bytes_per_step": 4 * n,
+                       "ms_per_step": round(e2e_ms, 3), "steps": a.e2e_steps, "labels_match_device_path": ok}
+        del h_off, h_adj, h_lab
+
+    # ---- cpu_baseline: the oracle on the host cores (rank 0, N = 1 only)
+    if not a.no_cpu_baseline and rank == 0 and ws == 1:
+        del flush
+        torch.cuda.empty_cache()
+        m_s, dt, off_s, adj_s, lab_s = cpu_oracle_sample(a.cpu_scale, True)
+        # parity of the product on the same sample (bit-exact labels)
+        so, sa = torch.from_numpy(off_s).to(dev), torch.from_numpy(adj_s.view(np.int32)).to(dev)
+        sl = torch.empty(off_s.size - 1, dtype=torch.int32, device=dev)
+        cc.cc_labels(so, sa, off_s.size - 1, adj_s.size, sl, cc.make_opts(k=a.k, variant=variant, flags=a.flags))
+        par = bool(np.array_equal(sl.cpu().numpy().view(np.uint32), lab_s))
+        line["cpu_baseline"] = {"value": round(m_s / dt / 1e9, 5), "unit": "GTEPS", "cores": 1, "kind": "oracle",
+                                "sample": f"oracle.cc_bfs (sequential BFS, 1 thread) on RMAT scale {a.cpu_scale} "
+                                          f"(C4 recipe, seed 4), m={m_s}, {dt:.2f} s",
+                                "host_cores": os.cpu_count(), "gpu_labels_bit_exact_on_sample": par}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def run_ours_incr(a, rank, ws, cfg):
+    """--config 5: 256 batches of (943,718 inserts, 104,858 queries) on n = 2^26."""
+    import torch
+
+    from inputs import gpu as ggen
+    from paper_2008_03909_b200 import cc
+    n = 1 << cfg.scale
+    nb = cfg.n_batches
+    ins = torch.empty((nb, cfg.n_ins, 2), dtype=torch.int32, device="cuda")
+    qs = torch.empty((nb, cfg.n_q, 2), dtype=torch.int32, device="cuda")
+    for b in range(nb):
+        ggen.incr_batch(cfg.seed, cfg.scale, b, cfg.n_ins, cfg.n_q, ins[b], qs[b])
+    ans = torch.empty((nb, cfg.n_q), dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def stream_once(ev=None):
+        h = cc.Incr(n)
+        for b in range(nb):
+            if ev is not None:
+                ev[b][0].record(stream)
+            h.batch(ins[b], cfg.n_ins, qs[b], cfg.n_q, ans[b])
+            if ev is not None:
+                ev[b][1].record(stream)
+        torch.cuda.synchronize()
+        h.close()
+
+    for _ in range(a.warmup):
+        stream_once()
+    clk = Clocks(torch.cuda.current_device())
+    clk.start()
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(nb)] for _ in range(a.steps)]
+    barrier(ws)
+    torch.cuda.synchronize()
+    l0 = cc.launch_count()
+    for s in range(a.steps):
+        stream_once(evs[s])
+    barrier(ws)
+    launches = cc.launch_count() - l0
+    clocks = clk.stop()
+    per_stream = [sum(evs[s][b][0].elapsed_time(evs[s][b][1]) for b in range(nb)) for s in range(a.steps)]
+    batch_ms = sorted(evs[s][b][0].elapsed_time(evs[s][b][1]) for s in range(a.steps) for b in range(nb))
+    mean_ms = reduce_max(statistics.mean(per_stream), ws)
+    ops = nb * (cfg.n_ins + cfg.n_q)
+    line = {"metric": "incremental connectivity ops/sec", "value": round(aggregate_value(ops, mean_ms * 1e-3, ws) / 1e9, 4),
+            "unit": "Gops/s", "n_gpus": ws, "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(mean_ms, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": cfg.name, "n": n, "batches": nb, "inserts_per_batch": cfg.n_ins,
+                       "queries_per_batch": cfg.n_q, "l2": "P (256 MiB) > L2"},
+            "inserts_per_s": round(nb * cfg.n_ins / (mean_ms * 1e-3), 1),
+            "batch_ms": {"p50": batch_ms[len(batch_ms) // 2], "p99": batch_ms[int(len(batch_ms) * 0.99)]},
+            "gpu_launches": int(launches), "clocks": clocks}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    rank, ws = dist_setup()
+    if a.impl == "reference":
+        run_reference(a, rank, ws)
+    else:
+        run_ours(a, rank, ws)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

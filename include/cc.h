@@ -93,14 +93,14 @@ typedef struct {
 /* Work counters, accumulated (atomicAdd) into a DEVICE struct when
  * cc_opts.counters != NULL.  Bench/diagnostics only.                         */
 typedef struct {
-    uint64_t pending_links;    /* H2 links that needed the CAS kernel               */
-    uint64_t worklist;         /* vertices examined by the finish (deg > k)          */
-    uint64_t finish_vertices;  /* non-L_max vertices whose lists were traversed      */
+    uint64_t pending_links;    /* H2 links left to the CAS kernel (k_link_pending)    */
+    uint64_t worklist;         /* vertices marked for the finish (list not all sampled)*/
+    uint64_t finish_vertices;  /* marked vertices with root != L_max, lists traversed */
     uint64_t finish_edges;     /* adjacency entries traversed by the finish          */
-    uint64_t finish_offsets;   /* offset pairs read by the finish                    */
-    uint64_t hooks;            /* successful root hooks (H2 CAS + H5)                */
+    uint64_t sample_hooks;     /* successful root hooks in k_link_pending (H2)       */
+    uint64_t finish_hooks;     /* successful root hooks in the finish (H5)           */
     uint64_t big_vertices;     /* finish vertices sent to the CTA-per-vertex queue   */
-    uint64_t reserved;
+    uint64_t compress_writes;  /* slots rewritten by the fused H3 compress (k_finish)*/
 } cc_counters;
 
 typedef struct {
@@ -116,7 +116,24 @@ typedef struct {
                                     0xFFFFFFFF = skip nothing                          */
     cc_counters*    counters;    /* DEVICE                                             */
     cc_timings*     timings;     /* HOST                                               */
+    void**          marks;       /* HOST array of CC_NUM_MARKS cudaEvent_t created by
+                                    the caller, or NULL: recorded on `stream` at the
+                                    kernel boundaries below, no synchronisation       */
 } cc_opts;
+
+/* Kernel-boundary marks of cc_labels / cc_spanning_forest (cc_opts.marks[i] is
+ * recorded after the named step; a skipped step records a zero-length span).  */
+#define CC_MARK_START       0   /* before the first kernel                        */
+#define CC_MARK_INIT        1   /* k_sample_init: H1 + first k-out round          */
+#define CC_MARK_MIDCOMPRESS 2   /* compress between k-out rounds                  */
+#define CC_MARK_LINK        3   /* k_link_pending: remaining k-out links (H2)     */
+#define CC_MARK_SAMPLED     4   /* separate H3 compress, only with sampled_out    */
+#define CC_MARK_IDENTIFY    5   /* IdentifyFrequent (H4)                          */
+#define CC_MARK_FINISH      6   /* k_finish: H3 compress fused with the H5 scan   */
+#define CC_MARK_FINISH_BIG  7   /* k_finish_proc + k_finish_big: H5 edge work     */
+#define CC_MARK_COMPRESS    8   /* final compress (H6)                            */
+#define CC_MARK_FOREST      9   /* forest filter (H7; zero-length in cc_labels)   */
+#define CC_NUM_MARKS       10
 
 /* Fill *o with the defaults above. */
 void cc_opts_default(cc_opts* o);

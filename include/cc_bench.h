@@ -37,6 +37,11 @@ cc_status cc_bench_random_gather(const uint32_t* x, uint64_t len, uint64_t count
 /* dst[i] = src[i] for i < words (uint32): the streaming copy ceiling. */
 cc_status cc_bench_copy(const uint32_t* src, uint32_t* dst, uint64_t words, void* stream);
 
+/* Set the device-wide cudaLimitMaxL2FetchGranularity (bytes, 0..128) of the
+ * current context; returns the previous value in *prev (may be NULL).  A
+ * measurement knob for the random-access kernels (32 B = one sector). */
+cc_status cc_bench_set_l2_fetch(int bytes, int* prev);
+
 /* Cumulative number of kernels libcc.so has launched in this process
  * (bench evidence for "gpu_launches"; host-side counter, no GPU access). */
 uint64_t cc_bench_launch_count(void);

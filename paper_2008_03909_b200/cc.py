@@ -34,7 +34,7 @@ EXPORTS = [
     "cc_incr_labels", "cc_incr_destroy", "cc_incr_num_vertices", "cc_status_str", "cc_last_error",
     "cc_workspace_bytes", "cc_version",
     "cc_bench_map_edges", "cc_bench_gather_edges", "cc_bench_random_gather", "cc_bench_copy",
-    "cc_bench_launch_count",
+    "cc_bench_launch_count", "cc_bench_set_l2_fetch",
 ]
 
 
@@ -46,15 +46,21 @@ class Timings(ctypes.Structure):
         return {f: float(getattr(self, f)) for f, _ in self._fields_}
 
 
-COUNTER_FIELDS = ["pending_links", "worklist", "finish_vertices", "finish_edges", "finish_offsets", "hooks",
-                  "big_vertices", "reserved"]
+COUNTER_FIELDS = ["pending_links", "worklist", "finish_vertices", "finish_edges", "sample_hooks", "finish_hooks",
+                  "big_vertices", "compress_writes"]
 
 
 class Opts(ctypes.Structure):
     _fields_ = [("kout_k", ctypes.c_uint32), ("kout_variant", ctypes.c_uint32), ("seed", ctypes.c_uint64),
                 ("samples", ctypes.c_uint32), ("flags", ctypes.c_uint32),
                 ("sampled_out", ctypes.c_void_p), ("lmax_out", ctypes.c_void_p), ("lmax_force", ctypes.c_void_p),
-                ("counters", ctypes.c_void_p), ("timings", ctypes.POINTER(Timings))]
+                ("counters", ctypes.c_void_p), ("timings", ctypes.POINTER(Timings)),
+                ("marks", ctypes.POINTER(ctypes.c_void_p))]
+
+
+NUM_MARKS = 10
+MARK_NAMES = ["start", "k_sample_init", "k_compress_mid", "k_link_pending", "k_compress_H3_debug", "k_identify",
+              "k_finish", "k_finish_proc", "k_compress_H6", "k_forest"]
 
 
 class CCError(RuntimeError):
@@ -92,6 +98,7 @@ def load() -> ctypes.CDLL:
         "cc_bench_random_gather": (ctypes.c_int, [P, U64, U64, U64, P, P]),
         "cc_bench_copy": (ctypes.c_int, [P, P, U64, P]),
         "cc_bench_launch_count": (U64, []),
+        "cc_bench_set_l2_fetch": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -127,12 +134,16 @@ def _stream(stream):
 
 
 def make_opts(k=2, variant=VARIANT_AFFOREST, seed=0, samples=1024, flags=0, sampled_out=None, lmax_out=None,
-              lmax_force=None, counters=None, timings: Timings | None = None) -> Opts:
+              lmax_force=None, counters=None, timings: Timings | None = None, marks=None) -> Opts:
     o = Opts()
     o.kout_k, o.kout_variant, o.seed, o.samples, o.flags = k, variant, seed, samples, flags
     o.sampled_out, o.lmax_out, o.lmax_force = _ptr(sampled_out), _ptr(lmax_out), _ptr(lmax_force)
     o.counters = _ptr(counters)
     o.timings = ctypes.pointer(timings) if timings is not None else None
+    if marks is not None:        # list of NUM_MARKS raw cudaEvent_t handles
+        arr = (ctypes.c_void_p * NUM_MARKS)(*marks)
+        o._marks_keepalive = arr
+        o.marks = ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p))
     return o
 
 
@@ -194,6 +205,12 @@ def random_gather(x, length, count, seed, out, stream=None):
 
 def copy(src, dst, words, stream=None):
     _check(load().cc_bench_copy(_ptr(src), _ptr(dst), words, _stream(stream)), "copy")
+
+
+def set_l2_fetch(nbytes: int) -> int:
+    prev = ctypes.c_int()
+    _check(load().cc_bench_set_l2_fetch(nbytes, ctypes.byref(prev)), "set_l2_fetch")
+    return prev.value
 
 
 def launch_count() -> int:

@@ -111,6 +111,15 @@ cc_status cc_bench_copy(const uint32_t* src, uint32_t* dst, uint64_t words, void
     return CC_OK;
 }
 
+cc_status cc_bench_set_l2_fetch(int bytes, int* prev)
+{
+    size_t old = 0;
+    CC_CUDA_TRY(cudaDeviceGetLimit(&old, cudaLimitMaxL2FetchGranularity));
+    if (prev) *prev = (int)old;
+    CC_CUDA_TRY(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)bytes));
+    return CC_OK;
+}
+
 uint64_t cc_bench_launch_count(void) { return g_launches.load(); }
 
 }  // extern "C"

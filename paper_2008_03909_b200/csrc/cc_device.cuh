@@ -93,13 +93,14 @@ struct Forest {
 // pu = P[ru], pv = P[rv]; equal parents => same tree; otherwise orient so that
 // pu > pv; if ru is a root, hook it under the snapshot pv by CAS, else take one
 // split/halve step on ru.  Returns true iff this call hooked a root.
+// link_rem_from: the same loop entered with the first two parent reads
+// (pu = P[u], pv = P[v]) already done by the caller (batched loads).
 template <bool HALVE, class Rec>
-__device__ __forceinline__ bool link_rem(uint32_t* P, uint32_t u, uint32_t v, const Rec& rec)
+__device__ __forceinline__ bool link_rem_from(uint32_t* P, uint32_t u, uint32_t v, uint32_t pu, uint32_t pv,
+                                              const Rec& rec)
 {
     uint32_t ru = u, rv = v;
     while (true) {
-        uint32_t pu = ld_relaxed(P + ru);
-        uint32_t pv = ld_relaxed(P + rv);
         if (pu == pv) return false;
         if (pu < pv) {
             uint32_t t = ru; ru = rv; rv = t;
@@ -110,12 +111,22 @@ __device__ __forceinline__ bool link_rem(uint32_t* P, uint32_t u, uint32_t v, co
                 rec.record(ru, u, v);
                 return true;
             }
-            continue;                                // lost a race: re-read
+            pu = ld_relaxed(P + ru);                 // lost a race: re-read
+            pv = ld_relaxed(P + rv);
+            continue;
         }
         uint32_t w = ld_relaxed(P + pu);             // one splice step on ru
         if (w != pu) cas(P + ru, pu, w);
         ru = HALVE ? w : pu;
+        pu = ld_relaxed(P + ru);
+        pv = ld_relaxed(P + rv);
     }
+}
+
+template <bool HALVE, class Rec>
+__device__ __forceinline__ bool link_rem(uint32_t* P, uint32_t u, uint32_t v, const Rec& rec)
+{
+    return link_rem_from<HALVE>(P, u, v, ld_relaxed(P + u), ld_relaxed(P + v), rec);
 }
 
 // UF-Async union (reading R2: the CAS targets the root slot).

@@ -3,22 +3,23 @@
 // Alg. 1 / Alg. 2 on one B200, stream-ordered with
 // no host synchronisation: L_max and every queue length stay in device memory.
 //
-//   K0 sample_init   H1 P[v] = v fused with the first k-out round: each vertex
-//                    u with first neighbour v0 < u sets P[u] = v0 by a plain
-//                    store (u is still a singleton root and only u writes
-//                    slot u in this kernel, so this IS Union(u, v0) of
-//                    Alg. 4 P:3952 with the min orientation of R1).  All other
-//                    sampled edges (v0 > u, j = 1..k-1) go to a pending list;
-//                    vertices whose list was not fully sampled go to the
-//                    finish worklist (degree skip).
-//   Kc compress      pointer-jumping compress ("fully compress"; H3/H6)
-//   K1 link_pending  UF-Rem-CAS links of the pending sampled edges (H2)
-//   K4 identify      IdentifyFrequent over S seeded samples (R9)
-//   K5 finish        Union over the lists of worklist vertices whose sampled
-//                    label != L_max, degree-binned
-//                    thread / warp / CTA-per-vertex
-//   K7 forest        Filter of Alg. 2: compact non-sentinel slots in
-//                    slot order
+//   K0 k_sample_init  H1 P[v] = v fused with the first k-out round: each vertex
+//                     u with first neighbour v0 < u sets P[u] = v0 by a plain
+//                     store (u is still a singleton root and only u writes
+//                     slot u in this kernel, so this IS Union(u, v0) of
+//                     Alg. 4 P:3952 with the min orientation of R1).  All other
+//                     sampled edges (v0 > u, j = 1..k-1) go to a pending list;
+//                     a bitmap marks vertices whose list was not wholly sampled
+//                     (degree skip).
+//   Kc k_compress     pointer-jumping compress ("fully compress"; H6)
+//   K1 k_link_pending UF-Rem-CAS links of the pending sampled edges (H2)
+//   K4 k_identify     IdentifyFrequent over S seeded samples (R9)
+//   K5 k_finish       ONE pass over P fusing the sampling compress (H3) with
+//                     the finish (H5): every vertex is compressed to its root
+//                     r; a marked vertex with r != L_max has its list unioned
+//                     (P:4091-4100), degree-binned lane / warp / CTA-queue
+//   K7 forest         Filter of Alg. 2: compact non-sentinel slots in
+//                     slot order
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -31,7 +32,7 @@ namespace ccb {
 
 struct Ctl {
     unsigned long long pend_count;
-    unsigned long long wl_count;
+    unsigned long long cand_count;
     unsigned long long big_count;
     unsigned int lmax;
     unsigned int err;
@@ -66,53 +67,131 @@ __device__ __forceinline__ void warp_count(uint64_t* ctr, uint32_t c)
 }
 
 // ---------------------------------------------------------------------------
-// K0: H1 + first k-out round + pending list + finish worklist.
+// K0: H1 + first k-out round + pending list + finish bitmap.
+//
+// Each warp owns a tile of 256 consecutive vertices, 8 per lane (vertex
+// wbase + 32*j + lane), so every offsets/P access is a coalesced warp
+// transaction and each lane keeps 8 independent first-neighbour loads in
+// flight (Little's law: tens of KB per SM outstanding).  Pending links are
+// appended in vertex order within a block with ONE atomicAdd per block (a
+// per-warp atomic on a single address serialised the first version at L2).
+// The finish bitmap has bit (u & 31) of word u >> 5 set iff deg(u) > full_deg.
+constexpr int kV = 8;                        // vertices per lane
+constexpr int kWarpTile = 32 * kV;           // 256 vertices per warp
+constexpr int kBlockTile = kWarpTile * (kBlock / 32);
+
 template <bool HYBRID, bool SF>
-__global__ void __launch_bounds__(kBlock) k_sample_init(
+__global__ void __launch_bounds__(kBlock, 3) k_sample_init(
     const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, uint32_t n, uint32_t k,
     uint64_t seed, uint32_t full_deg, uint32_t* __restrict__ P, uint2* __restrict__ F,
-    uint2* __restrict__ pend, uint32_t* __restrict__ wl, Ctl* ctl, cc_counters* cnt)
+    uint2* __restrict__ pend, uint32_t* __restrict__ bm, Ctl* ctl, cc_counters* cnt)
 {
-    const uint64_t u64 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool valid = u64 < n;
-    const uint32_t u = (uint32_t)u64;
-    int64_t b = 0, e = 0;
-    if (valid) {
-        b = ld_stream_i64(off + u);
-        e = ld_stream_i64(off + u + 1);
+    __shared__ uint32_t s_wtot[kBlock / 32];
+    __shared__ unsigned long long s_wbase[kBlock / 32];
+    const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint64_t wbase = (uint64_t)blockIdx.x * kBlockTile + (uint64_t)w * kWarpTile;
+
+    int64_t o[kV];
+    uint32_t d[kV];                              // list length, saturated at 2^32-1
+#pragma unroll
+    for (int j = 0; j < kV; ++j) {
+        const uint64_t u = wbase + 32 * j + lane;
+        o[j] = ld_stream_i64(off + (u < n ? u : n));
     }
-    const int64_t d = e - b;
-    uint32_t p = u;
-    uint32_t v0 = 0;
-    uint32_t npend = 0;
-    if (valid && d > 0 && k > 0) {
-        v0 = ld_stream_u32(adj + b);
-        if (v0 < u) {
-            p = v0;                                    // Union(u, v0): hook singleton root u
-            if (SF) F[u] = make_uint2(u, v0);          // forest edge at the hooked root
-        } else if (v0 > u) {
-            npend = 1;
+    const int64_t last = ld_stream_i64(off + (wbase + kWarpTile < n ? wbase + kWarpTile : n));
+#pragma unroll
+    for (int j = 0; j < kV; ++j) {
+        const int64_t nx = __shfl_down_sync(0xffffffffu, o[j], 1);
+        const int64_t first_next = __shfl_sync(0xffffffffu, j + 1 < kV ? o[(j + 1) % kV] : last, 0);
+        const int64_t e = lane == 31 ? (j + 1 < kV ? first_next : last) : nx;
+        const uint64_t u = wbase + 32 * j + lane;
+        d[j] = u < n ? (uint32_t)min(e - o[j], (int64_t)0xFFFFFFFF) : 0u;
+    }
+    // the first two sampled neighbours of every vertex, all loads in flight together
+    uint32_t v0[kV], v1[kV];
+#pragma unroll
+    for (int j = 0; j < kV; ++j) {
+        const uint64_t u = wbase + 32 * j + lane;
+        v0[j] = (d[j] > 0 && k > 0) ? __ldg(adj + o[j]) : kSentinel;
+        uint32_t i1 = 1;
+        if (HYBRID && d[j] > 0) i1 = uniform_below(mix(seed, KOUT_STREAM, u * 64 + 1), d[j]);
+        v1[j] = (k > 1 && (HYBRID ? d[j] > 0 : d[j] > 1)) ? __ldg(adj + o[j] + i1) : kSentinel;
+    }
+    uint32_t c[kV];
+    uint32_t bits = 0, nwl = 0;
+#pragma unroll
+    for (int j = 0; j < kV; ++j) {
+        const uint64_t u = wbase + 32 * j + lane;
+        uint32_t np = 0;
+        if (v0[j] != kSentinel)
+            np = (v0[j] > (uint32_t)u ? 1u : 0u) + (HYBRID ? k : min(k, d[j])) - 1u;
+        c[j] = np;
+        const bool mark = u < n && d[j] > full_deg;
+        nwl += mark;
+        const uint32_t word = __ballot_sync(0xffffffffu, mark);
+        if (lane == (unsigned)j) bits = word;
+    }
+    if (lane < (unsigned)kV && wbase + 32 * lane < n) bm[(wbase >> 5) + lane] = bits;
+#pragma unroll
+    for (int j = 0; j < kV; ++j) {
+        const uint64_t u = wbase + 32 * j + lane;
+        if (u < n) {
+            uint32_t p = (uint32_t)u;
+            if (v0[j] < (uint32_t)u) {
+                p = v0[j];                              // Union(u, v0): hook singleton root u
+                if (SF) F[u] = make_uint2((uint32_t)u, v0[j]);   // forest edge at the hooked root
+            }
+            P[u] = p;
         }
-        const int64_t kk = HYBRID ? (int64_t)k : min((int64_t)k, d);
-        npend += (uint32_t)(kk - 1);
     }
-    if (valid) P[u] = p;
-    // pending sampled edges
-    unsigned long long pos = warp_append(&ctl->pend_count, npend);
-    if (npend) {
-        if (v0 > u) pend[pos++] = make_uint2(u, v0);
-        const int64_t kk = HYBRID ? (int64_t)k : min((int64_t)k, d);
-        for (int64_t j = 1; j < kk; ++j) {
-            int64_t i = HYBRID ? (int64_t)uniform_below(mix(seed, KOUT_STREAM, (uint64_t)u * 64 + j), (uint64_t)d)
-                               : j;
-            pend[pos++] = make_uint2(u, ld_stream_u32(adj + b + i));
+    // exclusive positions in vertex order: warp scans per j, then block, then one atomic
+    uint32_t ex[kV];
+    uint32_t run = 0;
+#pragma unroll
+    for (int j = 0; j < kV; ++j) {
+        uint32_t incl = c[j];
+#pragma unroll
+        for (int o2 = 1; o2 < 32; o2 <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o2);
+            if (lane >= (unsigned)o2) incl += t;
+        }
+        ex[j] = run + incl - c[j];
+        run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) s_wtot[w] = run;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long acc = 0;
+        for (int i = 0; i < kBlock / 32; ++i) {
+            s_wbase[i] = acc;
+            acc += s_wtot[i];
+        }
+        const unsigned long long pb = acc ? atomicAdd(&ctl->pend_count, acc) : 0ull;
+        for (int i = 0; i < kBlock / 32; ++i) s_wbase[i] += pb;
+    }
+    __syncthreads();
+    const unsigned long long pbase = s_wbase[w];
+    uint32_t npt = 0;
+#pragma unroll
+    for (int j = 0; j < kV; ++j) {
+        const uint64_t u = wbase + 32 * j + lane;
+        const uint32_t np = c[j];
+        npt += np;
+        if (np) {
+            unsigned long long pos = pbase + ex[j];
+            if (v0[j] > (uint32_t)u) pend[pos++] = make_uint2((uint32_t)u, v0[j]);
+            const uint32_t kk = HYBRID ? k : min(k, d[j]);
+            if (kk > 1) pend[pos++] = make_uint2((uint32_t)u, v1[j]);
+            for (uint32_t jj = 2; jj < kk; ++jj) {        // k > 2: the rest, loaded here
+                const uint32_t i = HYBRID ? uniform_below(mix(seed, KOUT_STREAM, u * 64 + jj), d[j]) : jj;
+                pend[pos++] = make_uint2((uint32_t)u, __ldg(adj + o[j] + i));
+            }
         }
     }
-    // finish worklist: lists not wholly unioned by the sampling
-    const uint32_t inwl = (valid && d > (int64_t)full_deg) ? 1u : 0u;
-    unsigned long long wpos = warp_append(&ctl->wl_count, inwl);
-    if (inwl) wl[wpos] = u;
-    if (cnt) warp_count(&cnt->pending_links, npend);
+    if (cnt) {
+        warp_count(&cnt->pending_links, npt);
+        warp_count(&cnt->worklist, nwl);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -121,42 +200,144 @@ __global__ void __launch_bounds__(kBlock) k_sample_init(
 // not; plain (L1-cacheable) loads are therefore safe and let the hot giant
 // root stay in L1.  Blocks run roughly in ascending id order and P[x] < x, so
 // most parents are already compressed when their children are visited.
-__global__ void __launch_bounds__(kBlock) k_compress(uint32_t* P, uint32_t n, uint32_t* out)
+// Each thread owns 2 x uint4 = 8 slots (2 x 16 B loads in flight per thread)
+// and writes a uint4 back only if one of its slots changed.
+constexpr int kCV = 8;                                   // slots per thread
+constexpr int kCTile = kBlock * kCV;                     // 2048 slots per block
+
+__device__ __forceinline__ uint32_t root_plain(const uint32_t* P, uint32_t r)
+{
+    uint32_t q = P[r];
+    while (q != r) {
+        r = q;
+        q = P[r];
+    }
+    return r;
+}
+
+// Roots of 8 slots with their first-level gathers issued together (8
+// independent loads in flight instead of 8 dependent walks); deeper walks,
+// rare after a compress, continue one slot at a time.
+__device__ __forceinline__ void roots8(const uint32_t* P, const uint32_t (&vv)[8], const uint32_t (&pp)[8],
+                                       uint32_t (&rr)[8])
+{
+    uint32_t q[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) q[s] = pp[s] == vv[s] ? pp[s] : P[pp[s]];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) rr[s] = q[s] == pp[s] ? pp[s] : root_plain(P, q[s]);
+}
+
+__device__ __forceinline__ uint32_t nchanged4(uint4 a, uint4 b)
+{
+    return (a.x != b.x) + (a.y != b.y) + (a.z != b.z) + (a.w != b.w);
+}
+
+__global__ void __launch_bounds__(kBlock) k_compress(uint32_t* P, uint32_t n, uint32_t* out, cc_counters* cnt)
+{
+    const uint64_t base = (uint64_t)blockIdx.x * kCTile;
+    uint32_t writes = 0;
+    if (base + kCTile <= n) {
+        const uint64_t i0 = base + 4 * (uint64_t)threadIdx.x, i1 = i0 + 4 * kBlock;
+        const uint4 a = reinterpret_cast<const uint4*>(P)[i0 >> 2];
+        const uint4 c = reinterpret_cast<const uint4*>(P)[i1 >> 2];
+        const uint32_t pp[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+        uint32_t vv[8], rr[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) vv[j] = (uint32_t)((j < 4 ? i0 : i1) + (j & 3));
+        roots8(P, vv, pp, rr);
+        const uint4 r0 = make_uint4(rr[0], rr[1], rr[2], rr[3]), r1 = make_uint4(rr[4], rr[5], rr[6], rr[7]);
+        const uint32_t c0 = nchanged4(r0, a), c1 = nchanged4(r1, c);
+        writes += c0 + c1;
+        if (c0) reinterpret_cast<uint4*>(P)[i0 >> 2] = r0;
+        if (c1) reinterpret_cast<uint4*>(P)[i1 >> 2] = r1;
+        if (out) {
+            reinterpret_cast<uint4*>(out)[i0 >> 2] = r0;
+            reinterpret_cast<uint4*>(out)[i1 >> 2] = r1;
+        }
+    } else {
+        for (uint64_t v64 = base + threadIdx.x; v64 < n; v64 += kBlock) {      // ragged tail
+            const uint32_t v = (uint32_t)v64;
+            const uint32_t p = P[v];
+            const uint32_t r = p == v ? v : root_plain(P, p);
+            if (r != p) { P[v] = r; ++writes; }
+            if (out) out[v] = r;
+        }
+    }
+    if (cnt) warp_count(&cnt->compress_writes, writes);
+}
+
+// scalar variant for buffers that are not 16-byte aligned
+__global__ void __launch_bounds__(kBlock) k_compress_scalar(uint32_t* P, uint32_t n, uint32_t* out, cc_counters* cnt)
 {
     const uint64_t v64 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v64 >= n) return;
-    const uint32_t v = (uint32_t)v64;
-    const uint32_t p = P[v];
-    uint32_t r = p;
-    if (p != v) {
-        uint32_t q = P[r];
-        while (q != r) {
-            r = q;
-            q = P[r];
-        }
-        if (r != p) P[v] = r;
+    uint32_t writes = 0;
+    if (v64 < n) {
+        const uint32_t v = (uint32_t)v64;
+        const uint32_t p = P[v];
+        const uint32_t r = p == v ? v : root_plain(P, p);
+        if (r != p) { P[v] = r; writes = 1; }
+        if (out) out[v] = r;
     }
-    if (out) out[v] = r;
+    if (cnt) warp_count(&cnt->compress_writes, writes);
+}
+
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+static cc_status launch_compress(uint32_t* P, uint32_t n, uint32_t* out, cc_counters* cnt, cudaStream_t s,
+                                 const char* what)
+{
+    if (aligned16(P) && aligned16(out))
+        k_compress<<<(unsigned)(((uint64_t)n + kCTile - 1) / kCTile), kBlock, 0, s>>>(P, n, out, cnt);
+    else
+        k_compress_scalar<<<(unsigned)(((uint64_t)n + kBlock - 1) / kBlock), kBlock, 0, s>>>(P, n, out, cnt);
+    CC_LAUNCH_CHECK(what);
+    return CC_OK;
 }
 
 // ---------------------------------------------------------------------------
-// K1: UF-Rem-CAS links of the pending sampled edges.
+// K1: UF-Rem-CAS links of the pending sampled edges.  Each thread takes 4
+// links spaced one grid apart (coalesced pair loads) and issues their first
+// parent reads together (8 independent loads in flight); most links end at
+// that first test (equal parents), the rest continue in link_rem_from.  The
+// __syncwarp re-converges the warp so the next group's loads are issued as
+// whole-warp transactions again.
+constexpr int kLB = 4;
+
 template <int MODE, bool SF>
 __global__ void __launch_bounds__(kBlock) k_link_pending(
     uint32_t* P, const uint2* __restrict__ pend, const Ctl* ctl, uint2* F, cc_counters* cnt)
 {
     const unsigned long long total = ctl->pend_count;
-    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x;
-    for (; base < total; base += stride) {
-        const unsigned long long i = base + threadIdx.x;
-        uint32_t hooked = 0;
-        if (i < total) {
-            const uint2 pr = pend[i];
-            if constexpr (SF) hooked = link<MODE>(P, pr.x, pr.y, Forest{F});
-            else hooked = link<MODE>(P, pr.x, pr.y, NoForest{});
+    const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
+    const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    for (unsigned long long base = 0; base < total; base += nthreads * kLB) {
+        uint2 pr[kLB];
+        uint32_t pu[kLB], pv[kLB];
+#pragma unroll
+        for (int q = 0; q < kLB; ++q) {
+            const unsigned long long i = base + q * nthreads + tid;
+            pr[q] = i < total ? pend[i] : make_uint2(0u, 0u);
         }
-        if (cnt) warp_count(&cnt->hooks, hooked);
+#pragma unroll
+        for (int q = 0; q < kLB; ++q) {
+            pu[q] = ld_relaxed(P + pr[q].x);
+            pv[q] = ld_relaxed(P + pr[q].y);
+        }
+        uint32_t hooked = 0;
+#pragma unroll
+        for (int q = 0; q < kLB; ++q) {
+            if (pu[q] == pv[q]) continue;
+            if constexpr (MODE == 2) {
+                if constexpr (SF) hooked += link_async(P, pr[q].x, pr[q].y, Forest{F});
+                else hooked += link_async(P, pr[q].x, pr[q].y, NoForest{});
+            } else {
+                if constexpr (SF) hooked += link_rem_from<MODE == 1>(P, pr[q].x, pr[q].y, pu[q], pv[q], Forest{F});
+                else hooked += link_rem_from<MODE == 1>(P, pr[q].x, pr[q].y, pu[q], pv[q], NoForest{});
+            }
+        }
+        __syncwarp();
+        if (cnt) warp_count(&cnt->sample_hooks, hooked);
     }
 }
 
@@ -236,75 +417,149 @@ __global__ void __launch_bounds__(1024) k_identify(const uint32_t* P, uint32_t n
 }
 
 // ---------------------------------------------------------------------------
-// K5: finish.  Each warp takes 32 worklist entries; a lane keeps
-// its vertex if the vertex's sampled label is not L_max.  Short lists (after
-// dropping the afforest-sampled prefix) are walked by their own lane, medium
-// lists by the whole warp (ballot/shuffle; an edge whose endpoint already sits
-// directly under u's root is skipped without a link), long lists are queued
-// for k_finish_big (one CTA per vertex).
-template <int MODE, bool SF>
-__global__ void __launch_bounds__(kBlock) k_finish(
-    const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, uint32_t* P,
-    const uint32_t* __restrict__ wl, Ctl* ctl, uint32_t skip_prefix, bool no_skip, uint32_t* big,
-    uint2* F, cc_counters* cnt)
+// K5: the finish fused with the sampling compress (H3).
+//
+// One coalesced pass over P (2 x uint4 per thread, like k_compress): every
+// slot is compressed to its root r (H3, Def. 3.1's height-one labelling), and
+// a vertex whose bitmap bit is set (its list was not wholly sampled) and whose
+// root is not L_max has its remaining list unioned.  The skip test is the
+// dynamic one of reading R10: r was v's root at some point, so r == L_max
+// proves v connected to L_max; every edge (v, y) out of a skipped v is either
+// inside L_max's component or applied from y, which is then not skipped
+// (P:2090-2100).  Hooks of other warps run concurrently with this pass; the
+// compress store P[v] = r stays sound because r < v is a member of v's tree
+// at store time and trees only merge (no splice, reading R3), and v is not a
+// root (only non-root slots are rewritten; a non-root never becomes a root).
+//
+// Candidates are appended (warp-aggregated) to a queue that k_finish_proc
+// degree-bins: lists (after the afforest-sampled prefix) of <= kSmallDeg
+// entries are walked by their own lane, lists up to kBigDeg by the whole warp
+// (ballot/shuffle; an edge whose endpoint already hangs directly under u's
+// root is skipped without a link), longer lists are queued for k_finish_big
+// (one CTA per vertex).  Keeping the edge work out of the scan keeps the scan
+// a lean streaming kernel (no spills, full occupancy).
+template <bool VEC>
+__global__ void __launch_bounds__(kBlock) k_finish(uint32_t* P, const uint32_t* __restrict__ bm, uint32_t n,
+                                                   Ctl* ctl, bool no_skip, uint32_t* cq, cc_counters* cnt)
 {
-    const unsigned long long total = ctl->wl_count;
     const uint32_t lmax = no_skip ? kSentinel : ctl->lmax;
+    const uint64_t base = (uint64_t)blockIdx.x * kCTile;
+    const uint64_t i0 = base + 4 * (uint64_t)threadIdx.x, i1 = i0 + 4 * kBlock;
+    const bool full = VEC && base + kCTile <= n;
+    uint32_t vv[kCV], pp[kCV], rr[kCV];
+#pragma unroll
+    for (int s = 0; s < kCV; ++s) vv[s] = (uint32_t)((s < 4 ? i0 : i1) + (s & 3));
+    if (full) {
+        const uint4 a = reinterpret_cast<const uint4*>(P)[i0 >> 2];
+        const uint4 c = reinterpret_cast<const uint4*>(P)[i1 >> 2];
+        pp[0] = a.x; pp[1] = a.y; pp[2] = a.z; pp[3] = a.w;
+        pp[4] = c.x; pp[5] = c.y; pp[6] = c.z; pp[7] = c.w;
+    } else {
+#pragma unroll
+        for (int s = 0; s < kCV; ++s) pp[s] = (uint64_t)((s < 4 ? i0 : i1) + (s & 3)) < n ? P[vv[s]] : vv[s];
+    }
+    const uint32_t w0 = i0 < n ? bm[i0 >> 5] : 0u;
+    const uint32_t w1 = i1 < n ? bm[i1 >> 5] : 0u;
+    uint32_t writes = 0;
+    roots8(P, vv, pp, rr);
+#pragma unroll
+    for (int s = 0; s < kCV; ++s) writes += rr[s] != pp[s];
+    if (full) {                                          // H3 compress writes
+        if (rr[0] != pp[0] || rr[1] != pp[1] || rr[2] != pp[2] || rr[3] != pp[3])
+            reinterpret_cast<uint4*>(P)[i0 >> 2] = make_uint4(rr[0], rr[1], rr[2], rr[3]);
+        if (rr[4] != pp[4] || rr[5] != pp[5] || rr[6] != pp[6] || rr[7] != pp[7])
+            reinterpret_cast<uint4*>(P)[i1 >> 2] = make_uint4(rr[4], rr[5], rr[6], rr[7]);
+    } else {
+#pragma unroll
+        for (int s = 0; s < kCV; ++s)
+            if (rr[s] != pp[s]) P[vv[s]] = rr[s];           // rr != pp only for in-range slots
+    }
+    uint32_t cm = 0;                                     // candidate slots of this thread
+#pragma unroll
+    for (int s = 0; s < kCV; ++s) {
+        const uint64_t v64 = (s < 4 ? i0 : i1) + (s & 3);
+        const uint32_t word = s < 4 ? w0 : w1;
+        if (v64 < n && ((word >> (vv[s] & 31)) & 1u) && rr[s] != lmax) cm |= 1u << s;
+    }
+    if (__any_sync(0xffffffffu, cm != 0)) {
+        const unsigned long long pos = warp_append(&ctl->cand_count, __popc(cm));
+        uint32_t k2 = 0;
+#pragma unroll
+        for (int s = 0; s < kCV; ++s)
+            if (cm >> s & 1u) cq[pos + k2++] = vv[s];
+    }
+    if (cnt) warp_count(&cnt->compress_writes, writes);
+}
+
+// k_finish_proc: the H5 edge work of the queued candidates.  A warp takes 32
+// candidates, prefix-sums their list lengths (after the afforest-sampled
+// prefix) and sweeps the concatenated lists 32 edges at a time, each lane
+// finding its edge's owner by a binary search over the prefix (shuffles), so
+// every lane has an independent link in flight whatever the degree mix; an
+// edge whose endpoint already hangs directly under the owner's root is
+// skipped without a link.  Lists longer than kBigDeg go to k_finish_big.
+template <int MODE, bool SF>
+__global__ void __launch_bounds__(kBlock) k_finish_proc(
+    const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, uint32_t* P,
+    const uint32_t* __restrict__ cq, Ctl* ctl, uint32_t skip_prefix, uint32_t* big, uint2* F, cc_counters* cnt)
+{
+    const unsigned long long total = ctl->cand_count;
     const unsigned lane = threadIdx.x & 31;
     const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
     for (unsigned long long base = warp * 32; base < total; base += nwarps * 32) {
         const unsigned long long i = base + lane;
-        uint32_t u = 0;
-        bool proc = false;
-        if (i < total) {
-            u = wl[i];
-            proc = ld_relaxed(P + u) != lmax;
-        }
+        const bool cand = i < total;
+        const uint32_t u = cand ? cq[i] : 0u;
         int64_t b = 0, e = 0;
-        if (proc) {
+        if (cand) {
             b = off[u];
             e = off[u + 1];
-            b += min((int64_t)skip_prefix, e - b);     // afforest: first k edges already unioned
+            b += min((int64_t)skip_prefix, e - b);     // afforest: the first k edges were unioned
         }
         const int64_t d = e - b;
-        const bool small = proc && d <= kSmallDeg;
-        const bool medium = proc && d > kSmallDeg && d <= kBigDeg;
-        const bool isbig = proc && d > kBigDeg;
+        const bool isbig = d > kBigDeg;
+        const uint32_t ru = cand && !isbig && d > 0 ? find_naive(P, u) : 0u;
         if (cnt) {
-            warp_count(&cnt->finish_vertices, proc ? 1u : 0u);
-            warp_count(&cnt->finish_offsets, proc ? 1u : 0u);
-            warp_count(&cnt->finish_edges, proc ? (uint32_t)min(d, (int64_t)0xFFFFFFFF) : 0u);
+            warp_count(&cnt->finish_vertices, cand ? 1u : 0u);
+            warp_count(&cnt->finish_edges, cand ? (uint32_t)min(d, (int64_t)0xFFFFFFFF) : 0u);
             warp_count(&cnt->big_vertices, isbig ? 1u : 0u);
         }
-        unsigned long long bpos = warp_append(&ctl->big_count, isbig ? 1u : 0u);
+        const unsigned long long bpos = warp_append(&ctl->big_count, isbig ? 1u : 0u);
         if (isbig) big[bpos] = u;
+        const uint32_t dd = isbig ? 0u : (uint32_t)d;   // <= kBigDeg
+        uint32_t incl = dd;                             // inclusive prefix of list lengths
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (unsigned)o) incl += t;
+        }
+        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t excl = incl - dd;
         uint32_t hooks = 0;
-        if (small) {
-            for (int64_t x = b; x < e; ++x) {
-                const uint32_t v = adj[x];
-                if constexpr (SF) hooks += link<MODE>(P, u, v, Forest{F});
-                else hooks += link<MODE>(P, u, v, NoForest{});
+        for (uint32_t t0 = 0; t0 < tot; t0 += 32) {
+            const uint32_t t = t0 + lane;
+            // owner = the last lane whose exclusive prefix is <= t
+            int lo = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const uint32_t pe = __shfl_sync(0xffffffffu, excl, lo + step);
+                if (pe <= t) lo += step;
             }
-        }
-        unsigned mm = __ballot_sync(0xffffffffu, medium);
-        while (mm) {
-            const int src = __ffs(mm) - 1;
-            mm &= mm - 1;
-            const uint32_t mu = __shfl_sync(0xffffffffu, u, src);
-            const int64_t mb = __shfl_sync(0xffffffffu, b, src);
-            const int64_t me = __shfl_sync(0xffffffffu, e, src);
-            uint32_t ru = 0;
-            if (lane == 0) ru = find_naive(P, mu);
-            ru = __shfl_sync(0xffffffffu, ru, 0);
-            for (int64_t x = mb + lane; x < me; x += 32) {
-                const uint32_t v = adj[x];
-                if (ld_relaxed(P + v) == ru) continue;  // v hangs directly under u's root
-                if constexpr (SF) hooks += link<MODE>(P, mu, v, Forest{F});
-                else hooks += link<MODE>(P, mu, v, NoForest{});
+            const uint32_t ou = __shfl_sync(0xffffffffu, u, lo);
+            const uint32_t orr = __shfl_sync(0xffffffffu, ru, lo);
+            const int64_t ob = __shfl_sync(0xffffffffu, b, lo);
+            const uint32_t oex = __shfl_sync(0xffffffffu, excl, lo);
+            if (t < tot) {
+                const uint32_t v = adj[ob + (t - oex)];
+                if (ld_relaxed(P + v) != orr) {
+                    if constexpr (SF) hooks += link<MODE>(P, ou, v, Forest{F});
+                    else hooks += link<MODE>(P, ou, v, NoForest{});
+                }
             }
+            __syncwarp();
         }
-        if (cnt) warp_count(&cnt->hooks, hooks);
+        if (cnt) warp_count(&cnt->finish_hooks, hooks);
     }
 }
 
@@ -332,7 +587,7 @@ __global__ void __launch_bounds__(512) k_finish_big(const int64_t* __restrict__ 
             if constexpr (SF) hooks += link<MODE>(P, u, v, Forest{F});
             else hooks += link<MODE>(P, u, v, NoForest{});
         }
-        if (cnt) warp_count(&cnt->hooks, hooks);
+        if (cnt) warp_count(&cnt->finish_hooks, hooks);
     }
 }
 
@@ -478,10 +733,12 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
     const uint64_t pend_cap = std::max<uint64_t>(
         1, HYBRID ? (uint64_t)k * std::min<uint64_t>(n, (uint64_t)m) : std::min<uint64_t>((uint64_t)n * k, (uint64_t)m));
     const uint64_t big_cap = std::max<uint64_t>(1, std::min<uint64_t>(n, (uint64_t)m / kBigDeg + 1));
+    const uint64_t bm_words = ((uint64_t)n + 31) / 32;
     const uint32_t nfb = (uint32_t)(((uint64_t)n + kFTile - 1) / kFTile);
 
     Ctl* ctl = nullptr;
-    uint32_t* wl = nullptr;
+    uint32_t* bm = nullptr;
+    uint32_t* cq = nullptr;
     uint2* pend = nullptr;
     uint32_t* big = nullptr;
     uint2* F = nullptr;
@@ -492,7 +749,8 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
 
     auto cleanup = [&]() {
         scratch_free(ctl, s);
-        scratch_free(wl, s);
+        scratch_free(bm, s);
+        scratch_free(cq, s);
         scratch_free(pend, s);
         scratch_free(big, s);
         scratch_free(F, s);
@@ -501,7 +759,8 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
     };
     auto body = [&]() -> cc_status {
         CC_CUDA_TRY(scratch_alloc((void**)&ctl, sizeof(Ctl), s));
-        CC_CUDA_TRY(scratch_alloc((void**)&wl, sizeof(uint32_t) * (size_t)n, s));
+        CC_CUDA_TRY(scratch_alloc((void**)&bm, sizeof(uint32_t) * bm_words, s));
+        CC_CUDA_TRY(scratch_alloc((void**)&cq, sizeof(uint32_t) * (size_t)n, s));
         if (k > 0) CC_CUDA_TRY(scratch_alloc((void**)&pend, sizeof(uint2) * pend_cap, s));
         CC_CUDA_TRY(scratch_alloc((void**)&big, sizeof(uint32_t) * big_cap, s));
         if (SF) {
@@ -514,39 +773,62 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
         if (o.timings)
             for (auto& e : ev) CC_CUDA_TRY(cudaEventCreate(&e));
         if (o.timings) CC_CUDA_TRY(cudaEventRecord(ev[0], s));
-
-        const uint32_t nblk = (uint32_t)(((uint64_t)n + kBlock - 1) / kBlock);
-        // H1 + H2 (first round)
-        k_sample_init<HYBRID, SF><<<nblk, kBlock, 0, s>>>(off, adj, n, k, o.seed, full_deg, P, F, pend, wl, ctl,
+        auto mark = [&](int i) -> cudaError_t {
+            return o.marks ? cudaEventRecord((cudaEvent_t)o.marks[i], s) : cudaSuccess;
+        };
+        CC_CUDA_TRY(mark(CC_MARK_START));
+        // H1 + H2 (first round) + finish bitmap
+        const uint32_t nblk0 = (uint32_t)(((uint64_t)n + kBlockTile - 1) / kBlockTile);
+        k_sample_init<HYBRID, SF><<<nblk0, kBlock, 0, s>>>(off, adj, n, k, o.seed, full_deg, P, F, pend, bm, ctl,
                                                           o.counters);
         CC_LAUNCH_CHECK("k_sample_init");
+        CC_CUDA_TRY(mark(CC_MARK_INIT));
+        // shorten the first-round chains before the CAS links (grid-like inputs)
+        if (k > 0 && !(o.flags & CC_FLAG_NO_MIDCOMPRESS)) {
+            cc_status r = launch_compress(P, n, nullptr, nullptr, s, "k_compress(mid)");
+            if (r) return r;
+        }
+        CC_CUDA_TRY(mark(CC_MARK_MIDCOMPRESS));
+        // H2: the remaining sampled edges
         if (k > 0) {
-            if (!(o.flags & CC_FLAG_NO_MIDCOMPRESS)) {
-                k_compress<<<nblk, kBlock, 0, s>>>(P, n, nullptr);
-                CC_LAUNCH_CHECK("k_compress(mid)");
-            }
             k_link_pending<MODE, SF><<<sms * 8, kBlock, 0, s>>>(P, pend, ctl, F, o.counters);
             CC_LAUNCH_CHECK("k_link_pending");
-            k_compress<<<nblk, kBlock, 0, s>>>(P, n, nullptr);     // H3: height-one (Def. 3.1)
-            CC_LAUNCH_CHECK("k_compress(H3)");
         }
-        if (o.sampled_out)
+        CC_CUDA_TRY(mark(CC_MARK_LINK));
+        // H3 as its own pass only when the caller asks for the sampled labels
+        // (otherwise it is fused into k_finish)
+        if (o.sampled_out) {
+            cc_status r = launch_compress(P, n, nullptr, nullptr, s, "k_compress(H3)");
+            if (r) return r;
             CC_CUDA_TRY(cudaMemcpyAsync(o.sampled_out, P, sizeof(uint32_t) * (size_t)n, cudaMemcpyDeviceToDevice, s));
+        }
+        CC_CUDA_TRY(mark(CC_MARK_SAMPLED));
         if (o.timings) CC_CUDA_TRY(cudaEventRecord(ev[1], s));
-        // H4
+        // H4 (roots of the sampled forest; identical before or after H3)
         k_identify<<<1, 1024, 0, s>>>(P, n, o.seed, o.samples, o.lmax_force, ctl, o.lmax_out);
         CC_LAUNCH_CHECK("k_identify");
+        CC_CUDA_TRY(mark(CC_MARK_IDENTIFY));
         if (o.timings) CC_CUDA_TRY(cudaEventRecord(ev[2], s));
-        // H5
-        k_finish<MODE, SF><<<sms * 16, kBlock, 0, s>>>(off, adj, P, wl, ctl, skip_prefix, no_skip, big, F,
-                                                       o.counters);
-        CC_LAUNCH_CHECK("k_finish");
+        // H3 + H5
+        {
+            const unsigned nb = (unsigned)(((uint64_t)n + kCTile - 1) / kCTile);
+            if (aligned16(P)) k_finish<true><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters);
+            else k_finish<false><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters);
+            CC_LAUNCH_CHECK("k_finish");
+        }
+        CC_CUDA_TRY(mark(CC_MARK_FINISH));
+        k_finish_proc<MODE, SF><<<sms * 8, kBlock, 0, s>>>(off, adj, P, cq, ctl, skip_prefix, big, F, o.counters);
+        CC_LAUNCH_CHECK("k_finish_proc");
         k_finish_big<MODE, SF><<<sms * 2, 512, 0, s>>>(off, adj, P, big, ctl, skip_prefix, F, o.counters);
         CC_LAUNCH_CHECK("k_finish_big");
+        CC_CUDA_TRY(mark(CC_MARK_FINISH_BIG));
         if (o.timings) CC_CUDA_TRY(cudaEventRecord(ev[3], s));
         // H6
-        k_compress<<<nblk, kBlock, 0, s>>>(P, n, labels_out);
-        CC_LAUNCH_CHECK("k_compress(H6)");
+        {
+            cc_status r = launch_compress(P, n, labels_out, nullptr, s, "k_compress(H6)");
+            if (r) return r;
+        }
+        CC_CUDA_TRY(mark(CC_MARK_COMPRESS));
         // H7
         if (SF) {
             k_forest_count<<<nfb, kBlock, 0, s>>>(F, n, fcnt);
@@ -556,6 +838,7 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
             k_forest_write<<<nfb, kBlock, 0, s>>>(F, n, foff, edges);
             CC_LAUNCH_CHECK("k_forest_write");
         }
+        CC_CUDA_TRY(mark(CC_MARK_FOREST));
         if (o.timings) {
             CC_CUDA_TRY(cudaEventRecord(ev[4], s));
             CC_CUDA_TRY(cudaEventSynchronize(ev[4]));
