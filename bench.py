@@ -250,7 +250,7 @@ def run_ours(a, rank, ws):
         cc.cc_labels(d_off, d_adj, n, m, labels, o, stream)
 
     # ---- diagnostics run (untimed): counters + sampled labels for the byte model
-    ctr_t = torch.zeros(8, dtype=torch.int64, device=dev)
+    ctr_t = torch.zeros(len(cc.COUNTER_FIELDS), dtype=torch.int64, device=dev)
     sampled_t = torch.empty(n, dtype=torch.int32, device=dev)
     call(counters=ctr_t)              # counters of the production path (H3 fused into k_finish)
     call(sampled_out=sampled_t)       # sampled labels (this debug call runs H3 as its own pass)

@@ -78,7 +78,9 @@ typedef int cc_status;
 #define CC_FLAG_HALVE       (1u << 3)  /* HalveAtomicOne instead of SplitAtomicOne */
 #define CC_FLAG_FIND_SPLIT  (1u << 4)  /* incremental queries use FindAtomicSplit  */
 #define CC_FLAG_NO_DEGSKIP  (1u << 5)  /* also finish vertices whose whole list was sampled      */
-#define CC_FLAG_NO_MIDCOMPRESS (1u << 6) /* skip the compress between k-out rounds               */
+#define CC_FLAG_NO_MIDCOMPRESS (1u << 6) /* never run the compress between k-out rounds        */
+#define CC_FLAG_MIDCOMPRESS (1u << 7)  /* always run it (default: a 1024-sample probe of the
+                                          round-0 chain depth decides, on the device)        */
 
 /* Per-phase device times, filled when cc_opts.timings != NULL (the call then
  * synchronises `stream` before returning).  Bench/diagnostics only.          */
@@ -101,13 +103,16 @@ typedef struct {
     uint64_t finish_hooks;     /* successful root hooks in the finish (H5)           */
     uint64_t big_vertices;     /* finish vertices sent to the CTA-per-vertex queue   */
     uint64_t compress_writes;  /* slots rewritten by the fused H3 compress (k_finish)*/
+    uint64_t link_steps;       /* Rem-loop iterations of k_link_pending's walked links*/
+    uint64_t cas_failures;     /* hook CAS that lost a race in k_link_pending        */
+    uint64_t probe_deep;       /* probe samples whose round-0 chain exceeded 8 steps */
 } cc_counters;
 
 typedef struct {
     uint32_t kout_k;           /* sampled edges per vertex; default 2; 0 = no sampling */
     uint32_t kout_variant;     /* CC_VARIANT_*; default AFFOREST                       */
     uint64_t seed;             /* hybrid picks + IdentifyFrequent draws; default 0     */
-    uint32_t samples;          /* IdentifyFrequent sample count; default 1024 (1..4096)*/
+    uint32_t samples;          /* IdentifyFrequent sample count; default 1024 (1..2048)*/
     uint32_t flags;            /* CC_FLAG_*                                            */
     /* test/bench hooks; NULL in production (no extra traffic, no syncs):          */
     uint32_t*       sampled_out; /* DEVICE, n: copy of P after H3 (sampled labels)    */

@@ -16,7 +16,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcc.so")
+# CC_LIBCC_PATH overrides the library (A/B measurements of build variants only)
+LIB_PATH = os.environ.get("CC_LIBCC_PATH") or os.path.join(_HERE, "libcc.so")
 
 CC_OK, CC_EINVAL, CC_ERANGE, CC_ENOMEM, CC_ECUDA = 0, -1, -2, -3, -4
 VARIANT_AFFOREST, VARIANT_HYBRID = 0, 1
@@ -27,6 +28,7 @@ FLAG_HALVE = 1 << 3
 FLAG_FIND_SPLIT = 1 << 4
 FLAG_NO_DEGSKIP = 1 << 5
 FLAG_NO_MIDCOMPRESS = 1 << 6
+FLAG_MIDCOMPRESS = 1 << 7
 
 # every symbol include/cc.h and include/cc_bench.h declare
 EXPORTS = [
@@ -47,7 +49,8 @@ class Timings(ctypes.Structure):
 
 
 COUNTER_FIELDS = ["pending_links", "worklist", "finish_vertices", "finish_edges", "sample_hooks", "finish_hooks",
-                  "big_vertices", "compress_writes"]
+                  "big_vertices", "compress_writes",
+                  "link_steps", "cas_failures", "probe_deep"]
 
 
 class Opts(ctypes.Structure):

@@ -22,7 +22,11 @@ namespace ccb {
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p)
 {
     uint32_t v;
+#ifdef CC_LD_CG
+    asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+#else
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+#endif
     return v;
 }
 
@@ -93,14 +97,26 @@ struct Forest {
 // pu = P[ru], pv = P[rv]; equal parents => same tree; otherwise orient so that
 // pu > pv; if ru is a root, hook it under the snapshot pv by CAS, else take one
 // split/halve step on ru.  Returns true iff this call hooked a root.
+// Optional per-thread statistics of the loop (diagnostic counters only).
+struct NoStat {
+    __device__ __forceinline__ void step() {}
+    __device__ __forceinline__ void casfail() {}
+};
+struct Stat {
+    uint32_t steps = 0, fails = 0;
+    __device__ __forceinline__ void step() { ++steps; }
+    __device__ __forceinline__ void casfail() { ++fails; }
+};
+
 // link_rem_from: the same loop entered with the first two parent reads
 // (pu = P[u], pv = P[v]) already done by the caller (batched loads).
-template <bool HALVE, class Rec>
+template <bool HALVE, class Rec, class St = NoStat>
 __device__ __forceinline__ bool link_rem_from(uint32_t* P, uint32_t u, uint32_t v, uint32_t pu, uint32_t pv,
-                                              const Rec& rec)
+                                              const Rec& rec, St* st = nullptr)
 {
     uint32_t ru = u, rv = v;
     while (true) {
+        if (st) st->step();
         if (pu == pv) return false;
         if (pu < pv) {
             uint32_t t = ru; ru = rv; rv = t;
@@ -111,15 +127,29 @@ __device__ __forceinline__ bool link_rem_from(uint32_t* P, uint32_t u, uint32_t 
                 rec.record(ru, u, v);
                 return true;
             }
+            if (st) st->casfail();
             pu = ld_relaxed(P + ru);                 // lost a race: re-read
             pv = ld_relaxed(P + rv);
             continue;
         }
         uint32_t w = ld_relaxed(P + pu);             // one splice step on ru
         if (w != pu) cas(P + ru, pu, w);
+        // SplitAtomicOne continues from pu, whose parent w was just read: reuse
+        // it (and the snapshot pv) instead of re-reading -- each is a value the
+        // slot held during this call, which is all the loop needs (I1, I2).
+#ifdef CC_LINK_NO_REUSE
         ru = HALVE ? w : pu;
         pu = ld_relaxed(P + ru);
         pv = ld_relaxed(P + rv);
+#else
+        if (HALVE) {
+            ru = w;
+            pu = ld_relaxed(P + ru);
+        } else {
+            ru = pu;
+            pu = w;
+        }
+#endif
     }
 }
 

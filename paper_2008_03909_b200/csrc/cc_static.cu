@@ -36,10 +36,10 @@ struct Ctl {
     unsigned long long big_count;
     unsigned int lmax;
     unsigned int err;
+    unsigned int skip_mid;      // set by k_probe: the round-0 chains are short
 };
 
 constexpr uint32_t kSentinel = 0xFFFFFFFFu;
-constexpr int kSmallDeg = 8;      // <= : one lane walks the list
 constexpr int kBigDeg = 4096;     // >  : one CTA per vertex (second kernel)
 
 // Exclusive warp prefix of c and one atomicAdd per warp; every lane must call.
@@ -217,7 +217,9 @@ __device__ __forceinline__ uint32_t root_plain(const uint32_t* P, uint32_t r)
 
 // Roots of 8 slots with their first-level gathers issued together (8
 // independent loads in flight instead of 8 dependent walks); deeper walks,
-// rare after a compress, continue one slot at a time.
+// rare after a compress, continue one slot at a time.  (A level-by-level
+// variant that batches every level measured slower on C4: more registers
+// and a serial live-mask loop for little extra parallelism.)
 __device__ __forceinline__ void roots8(const uint32_t* P, const uint32_t (&vv)[8], const uint32_t (&pp)[8],
                                        uint32_t (&rr)[8])
 {
@@ -233,43 +235,50 @@ __device__ __forceinline__ uint32_t nchanged4(uint4 a, uint4 b)
     return (a.x != b.x) + (a.y != b.y) + (a.z != b.z) + (a.w != b.w);
 }
 
-__global__ void __launch_bounds__(kBlock) k_compress(uint32_t* P, uint32_t n, uint32_t* out, cc_counters* cnt)
+__global__ void __launch_bounds__(kBlock) k_compress(uint32_t* P, uint32_t n, uint32_t* out, cc_counters* cnt,
+                                                     const Ctl* gate)
 {
-    const uint64_t base = (uint64_t)blockIdx.x * kCTile;
+    if (gate && gate->skip_mid) return;
     uint32_t writes = 0;
-    if (base + kCTile <= n) {
-        const uint64_t i0 = base + 4 * (uint64_t)threadIdx.x, i1 = i0 + 4 * kBlock;
-        const uint4 a = reinterpret_cast<const uint4*>(P)[i0 >> 2];
-        const uint4 c = reinterpret_cast<const uint4*>(P)[i1 >> 2];
-        const uint32_t pp[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
-        uint32_t vv[8], rr[8];
+    const uint64_t ntiles = ((uint64_t)n + kCTile - 1) / kCTile;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {    // tiles in ascending waves
+        const uint64_t base = tile * kCTile;
+        if (base + kCTile <= n) {
+            const uint64_t i0 = base + 4 * (uint64_t)threadIdx.x, i1 = i0 + 4 * kBlock;
+            const uint4 a = reinterpret_cast<const uint4*>(P)[i0 >> 2];
+            const uint4 c = reinterpret_cast<const uint4*>(P)[i1 >> 2];
+            const uint32_t pp[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+            uint32_t vv[8], rr[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) vv[j] = (uint32_t)((j < 4 ? i0 : i1) + (j & 3));
-        roots8(P, vv, pp, rr);
-        const uint4 r0 = make_uint4(rr[0], rr[1], rr[2], rr[3]), r1 = make_uint4(rr[4], rr[5], rr[6], rr[7]);
-        const uint32_t c0 = nchanged4(r0, a), c1 = nchanged4(r1, c);
-        writes += c0 + c1;
-        if (c0) reinterpret_cast<uint4*>(P)[i0 >> 2] = r0;
-        if (c1) reinterpret_cast<uint4*>(P)[i1 >> 2] = r1;
-        if (out) {
-            reinterpret_cast<uint4*>(out)[i0 >> 2] = r0;
-            reinterpret_cast<uint4*>(out)[i1 >> 2] = r1;
-        }
-    } else {
-        for (uint64_t v64 = base + threadIdx.x; v64 < n; v64 += kBlock) {      // ragged tail
-            const uint32_t v = (uint32_t)v64;
-            const uint32_t p = P[v];
-            const uint32_t r = p == v ? v : root_plain(P, p);
-            if (r != p) { P[v] = r; ++writes; }
-            if (out) out[v] = r;
+            for (int j = 0; j < 8; ++j) vv[j] = (uint32_t)((j < 4 ? i0 : i1) + (j & 3));
+            roots8(P, vv, pp, rr);
+            const uint4 r0 = make_uint4(rr[0], rr[1], rr[2], rr[3]), r1 = make_uint4(rr[4], rr[5], rr[6], rr[7]);
+            const uint32_t c0 = nchanged4(r0, a), c1 = nchanged4(r1, c);
+            writes += c0 + c1;
+            if (c0) reinterpret_cast<uint4*>(P)[i0 >> 2] = r0;
+            if (c1) reinterpret_cast<uint4*>(P)[i1 >> 2] = r1;
+            if (out) {
+                reinterpret_cast<uint4*>(out)[i0 >> 2] = r0;
+                reinterpret_cast<uint4*>(out)[i1 >> 2] = r1;
+            }
+        } else {
+            for (uint64_t v64 = base + threadIdx.x; v64 < n; v64 += kBlock) {      // ragged tail
+                const uint32_t v = (uint32_t)v64;
+                const uint32_t p = P[v];
+                const uint32_t r = p == v ? v : root_plain(P, p);
+                if (r != p) { P[v] = r; ++writes; }
+                if (out) out[v] = r;
+            }
         }
     }
     if (cnt) warp_count(&cnt->compress_writes, writes);
 }
 
 // scalar variant for buffers that are not 16-byte aligned
-__global__ void __launch_bounds__(kBlock) k_compress_scalar(uint32_t* P, uint32_t n, uint32_t* out, cc_counters* cnt)
+__global__ void __launch_bounds__(kBlock) k_compress_scalar(uint32_t* P, uint32_t n, uint32_t* out, cc_counters* cnt,
+                                                            const Ctl* gate)
 {
+    if (gate && gate->skip_mid) return;
     const uint64_t v64 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t writes = 0;
     if (v64 < n) {
@@ -285,14 +294,46 @@ __global__ void __launch_bounds__(kBlock) k_compress_scalar(uint32_t* P, uint32_
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
 static cc_status launch_compress(uint32_t* P, uint32_t n, uint32_t* out, cc_counters* cnt, cudaStream_t s,
-                                 const char* what)
+                                 const char* what, const Ctl* gate = nullptr)
 {
+    // a gated (maybe skipped) compress runs as a persistent grid so that a skip
+    // costs one short wave, not 65k empty blocks; otherwise one block per tile
+    const uint64_t ntiles = ((uint64_t)n + kCTile - 1) / kCTile;
     if (aligned16(P) && aligned16(out))
-        k_compress<<<(unsigned)(((uint64_t)n + kCTile - 1) / kCTile), kBlock, 0, s>>>(P, n, out, cnt);
+        k_compress<<<(unsigned)(gate ? std::min<uint64_t>(ntiles, (uint64_t)num_sms() * 8) : ntiles), kBlock, 0, s>>>(
+            P, n, out, cnt, gate);
     else
-        k_compress_scalar<<<(unsigned)(((uint64_t)n + kBlock - 1) / kBlock), kBlock, 0, s>>>(P, n, out, cnt);
+        k_compress_scalar<<<(unsigned)(((uint64_t)n + kBlock - 1) / kBlock), kBlock, 0, s>>>(P, n, out, cnt, gate);
     CC_LAUNCH_CHECK(what);
     return CC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// k_probe: is the mid compress worth a pass over P?  Walk up to kProbeDepth
+// steps from 1024 seeded vertices of the round-0 forest; if at least 1/8 of
+// them have not reached a root, the chains are long (ids with locality, e.g.
+// the road-like grid, whose first neighbours chain up whole columns) and the
+// compress runs; otherwise (random-permuted RMAT/ER) it is skipped and the CAS
+// links walk the short chains themselves.  The decision stays on the device.
+constexpr int kProbeDepth = 8;
+constexpr uint64_t PROBE_STREAM = 18;
+
+__global__ void __launch_bounds__(1024) k_probe(const uint32_t* P, uint32_t n, uint64_t seed, Ctl* ctl,
+                                                cc_counters* cnt)
+{
+    __shared__ uint32_t s_deep;
+    if (threadIdx.x == 0) s_deep = 0;
+    __syncthreads();
+    uint32_t x = uniform_below(mix(seed, PROBE_STREAM, threadIdx.x), n);
+    int steps = 0;
+    for (uint32_t p = P[x]; p != x && steps < kProbeDepth; p = P[x], ++steps) x = p;
+    const uint32_t deep = __reduce_add_sync(0xffffffffu, steps >= kProbeDepth ? 1u : 0u);
+    if ((threadIdx.x & 31) == 0 && deep) atomicAdd(&s_deep, deep);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        ctl->skip_mid = s_deep * 8 < blockDim.x ? 1u : 0u;
+        if (cnt) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt->probe_deep), (unsigned long long)s_deep);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -302,7 +343,10 @@ static cc_status launch_compress(uint32_t* P, uint32_t n, uint32_t* out, cc_coun
 // that first test (equal parents), the rest continue in link_rem_from.  The
 // __syncwarp re-converges the warp so the next group's loads are issued as
 // whole-warp transactions again.
-constexpr int kLB = 4;
+#ifndef CC_LINK_BATCH
+#define CC_LINK_BATCH 4
+#endif
+constexpr int kLB = CC_LINK_BATCH;
 
 template <int MODE, bool SF>
 __global__ void __launch_bounds__(kBlock) k_link_pending(
@@ -311,6 +355,7 @@ __global__ void __launch_bounds__(kBlock) k_link_pending(
     const unsigned long long total = ctl->pend_count;
     const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
     const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    Stat st;
     for (unsigned long long base = 0; base < total; base += nthreads * kLB) {
         uint2 pr[kLB];
         uint32_t pu[kLB], pv[kLB];
@@ -332,26 +377,33 @@ __global__ void __launch_bounds__(kBlock) k_link_pending(
                 if constexpr (SF) hooked += link_async(P, pr[q].x, pr[q].y, Forest{F});
                 else hooked += link_async(P, pr[q].x, pr[q].y, NoForest{});
             } else {
-                if constexpr (SF) hooked += link_rem_from<MODE == 1>(P, pr[q].x, pr[q].y, pu[q], pv[q], Forest{F});
-                else hooked += link_rem_from<MODE == 1>(P, pr[q].x, pr[q].y, pu[q], pv[q], NoForest{});
+                if constexpr (SF) hooked += link_rem_from<MODE == 1>(P, pr[q].x, pr[q].y, pu[q], pv[q], Forest{F}, cnt ? &st : nullptr);
+                else hooked += link_rem_from<MODE == 1>(P, pr[q].x, pr[q].y, pu[q], pv[q], NoForest{}, cnt ? &st : nullptr);
             }
         }
         __syncwarp();
         if (cnt) warp_count(&cnt->sample_hooks, hooked);
     }
+    if (cnt) {
+        warp_count(&cnt->link_steps, st.steps);
+        warp_count(&cnt->cas_failures, st.fails);
+    }
 }
 
 // ---------------------------------------------------------------------------
-// K4: IdentifyFrequent: mode of P[s_i], s_i = uniform_below(mix(seed,
-// IDENT, i), n), ties to the smaller label (reading R9).  One CTA of 1024
-// threads; a bitonic sort in shared memory, then a max-reduction of
-// (run length, -label).
+// K4: IdentifyFrequent: the mode of root(s_i) over S samples,
+// s_i = uniform_below(mix(seed, IDENT, i), n), ties to the smaller label
+// (reading R9).  One CTA: each thread finds the roots of its samples and
+// counts them in a shared-memory open-addressing table (CAS on the key,
+// atomicAdd on the count), then a max-reduction of (count, -label).
+constexpr int kIdTable = 4096;                       // 2 * max samples (2048)
+
 __global__ void __launch_bounds__(1024) k_identify(const uint32_t* P, uint32_t n, uint64_t seed,
                                                    uint32_t samples, const uint32_t* force, Ctl* ctl,
                                                    uint32_t* lmax_out)
 {
-    constexpr int S = 4096;
-    __shared__ uint32_t a[S];
+    __shared__ uint32_t keys[kIdTable];
+    __shared__ uint32_t cnts[kIdTable];
     __shared__ unsigned long long best[32];
     const int t = threadIdx.x;
     if (force) {
@@ -361,43 +413,33 @@ __global__ void __launch_bounds__(1024) k_identify(const uint32_t* P, uint32_t n
         }
         return;
     }
-    int size = 1;
-    while (size < (int)samples) size <<= 1;
-    for (int i = t; i < size; i += blockDim.x) {
-        uint32_t lab = kSentinel;
-        if (i < (int)samples) {
-            uint32_t s = uniform_below(mix(seed, IDENT_STREAM, (uint64_t)i), n);
-            uint32_t r = s, q = P[r];
-            while (q != r) { r = q; q = P[r]; }
-            lab = r;
-        }
-        a[i] = lab;
+    for (int i = t; i < kIdTable; i += blockDim.x) {
+        keys[i] = kSentinel;                         // labels are < n <= 0xFFFFFFFE
+        cnts[i] = 0;
     }
     __syncthreads();
-    for (int kk = 2; kk <= size; kk <<= 1) {
-        for (int j = kk >> 1; j > 0; j >>= 1) {
-            for (int i = t; i < size; i += blockDim.x) {
-                int ixj = i ^ j;
-                if (ixj > i) {
-                    uint32_t x = a[i], y = a[ixj];
-                    bool up = (i & kk) == 0;
-                    if ((x > y) == up) { a[i] = y; a[ixj] = x; }
-                }
-            }
-            __syncthreads();
-        }
-    }
-    unsigned long long key = 0;
     for (int i = t; i < (int)samples; i += blockDim.x) {
-        if (i == 0 || a[i] != a[i - 1]) {
-            int j = i + 1;
-            while (j < (int)samples && a[j] == a[i]) ++j;
-            unsigned long long kk2 = ((unsigned long long)(j - i) << 32) | (unsigned long long)(kSentinel - a[i]);
-            key = key > kk2 ? key : kk2;
+        const uint32_t sv = uniform_below(mix(seed, IDENT_STREAM, (uint64_t)i), n);
+        const uint32_t lab = root_plain(P, sv);      // no hook runs concurrently
+        uint32_t h = (lab * 0x9E3779B1u) >> 20;      // 12-bit multiplicative hash
+        while (true) {
+            const uint32_t old = atomicCAS(&keys[h], kSentinel, lab);
+            if (old == kSentinel || old == lab) {
+                atomicAdd(&cnts[h], 1u);
+                break;
+            }
+            h = (h + 1) & (kIdTable - 1);
         }
     }
+    __syncthreads();
+    unsigned long long key = 0;
+    for (int i = t; i < kIdTable; i += blockDim.x)
+        if (cnts[i]) {
+            const unsigned long long k2 = ((unsigned long long)cnts[i] << 32) | (unsigned long long)(kSentinel - keys[i]);
+            key = key > k2 ? key : k2;
+        }
     for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long y = __shfl_xor_sync(0xffffffffu, key, o);
+        const unsigned long long y = __shfl_xor_sync(0xffffffffu, key, o);
         key = key > y ? key : y;
     }
     if ((t & 31) == 0) best[t >> 5] = key;
@@ -405,11 +447,11 @@ __global__ void __launch_bounds__(1024) k_identify(const uint32_t* P, uint32_t n
     if (t < 32) {
         key = t < (int)(blockDim.x >> 5) ? best[t] : 0;
         for (int o = 16; o > 0; o >>= 1) {
-            unsigned long long y = __shfl_xor_sync(0xffffffffu, key, o);
+            const unsigned long long y = __shfl_xor_sync(0xffffffffu, key, o);
             key = key > y ? key : y;
         }
         if (t == 0) {
-            uint32_t lm = kSentinel - (uint32_t)(key & 0xFFFFFFFFull);
+            const uint32_t lm = kSentinel - (uint32_t)(key & 0xFFFFFFFFull);
             ctl->lmax = lm;
             if (lmax_out) *lmax_out = lm;
         }
@@ -507,9 +549,12 @@ __global__ void __launch_bounds__(kBlock) k_finish_proc(
     const unsigned lane = threadIdx.x & 31;
     const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
-    for (unsigned long long base = warp * 32; base < total; base += nwarps * 32) {
+    // candidates per warp: 32 when there is plenty of work, fewer when the queue
+    // is short so that every warp gets some (short queues are latency-bound)
+    const unsigned cpw = (unsigned)max(1ull, min(32ull, (total + nwarps - 1) / nwarps));
+    for (unsigned long long base = warp * cpw; base < total; base += nwarps * cpw) {
         const unsigned long long i = base + lane;
-        const bool cand = i < total;
+        const bool cand = lane < cpw && i < total;
         const uint32_t u = cand ? cq[i] : 0u;
         int64_t b = 0, e = 0;
         if (cand) {
@@ -783,9 +828,15 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
                                                           o.counters);
         CC_LAUNCH_CHECK("k_sample_init");
         CC_CUDA_TRY(mark(CC_MARK_INIT));
-        // shorten the first-round chains before the CAS links (grid-like inputs)
+        // shorten the first-round chains before the CAS links when they are long
+        // (grid-like inputs); k_probe decides on the device unless a flag forces it
         if (k > 0 && !(o.flags & CC_FLAG_NO_MIDCOMPRESS)) {
-            cc_status r = launch_compress(P, n, nullptr, nullptr, s, "k_compress(mid)");
+            const bool force = (o.flags & CC_FLAG_MIDCOMPRESS) != 0;
+            if (!force) {
+                k_probe<<<1, 1024, 0, s>>>(P, n, o.seed, ctl, o.counters);
+                CC_LAUNCH_CHECK("k_probe");
+            }
+            cc_status r = launch_compress(P, n, nullptr, nullptr, s, "k_compress(mid)", force ? nullptr : ctl);
             if (r) return r;
         }
         CC_CUDA_TRY(mark(CC_MARK_MIDCOMPRESS));

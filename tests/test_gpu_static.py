@@ -34,6 +34,8 @@ OPTION_GRID = [
     dict(k=2, variant="afforest", flags=cc.FLAG_NO_SKIP),
     dict(k=2, variant="afforest", flags=cc.FLAG_NO_DEGSKIP | cc.FLAG_NO_MIDCOMPRESS),
     dict(k=64, variant="afforest", flags=0),
+    dict(k=2, variant="afforest", flags=cc.FLAG_MIDCOMPRESS),
+    dict(k=3, variant="hybrid", flags=cc.FLAG_MIDCOMPRESS | cc.FLAG_HALVE, seed=5),
 ]
 
 
@@ -220,7 +222,8 @@ def test_repeat_stress_random_options():
     want = oracle.cc_bfs(off, adj)
     rng = np.random.default_rng(1)
     d_off, d_adj = to_dev(off, adj)
-    flags_pool = [0, cc.FLAG_HALVE, cc.FLAG_UF_ASYNC, cc.FLAG_NO_SKIP, cc.FLAG_NO_MIDCOMPRESS, cc.FLAG_NO_DEGSKIP]
+    flags_pool = [0, cc.FLAG_HALVE, cc.FLAG_UF_ASYNC, cc.FLAG_NO_SKIP, cc.FLAG_NO_MIDCOMPRESS, cc.FLAG_NO_DEGSKIP,
+                  cc.FLAG_MIDCOMPRESS]
     for it in range(200):
         k = int(rng.integers(0, 5))
         variant = ["afforest", "hybrid"][int(rng.integers(0, 2))]
@@ -234,7 +237,7 @@ def test_counters_and_timings():
     off, adj = gen.rmat(seed=15, scale=12)
     n = off.size - 1
     d_off, d_adj = to_dev(off, adj)
-    ctr = torch.zeros(8, dtype=torch.int64, device="cuda")
+    ctr = torch.zeros(len(cc.COUNTER_FIELDS), dtype=torch.int64, device="cuda")
     t = cc.Timings()
     lab = torch.empty(n, dtype=torch.int32, device="cuda")
     cc.cc_labels(d_off, d_adj, n, adj.size, lab, cc.make_opts(counters=ctr, timings=t))
@@ -269,3 +272,19 @@ def test_microbenchmarks():
     dst = torch.empty_like(dx)
     cc.copy(dx, dst, n - n % 4)
     assert torch.equal(dst[: n - n % 4], dx[: n - n % 4])
+
+
+@pytest.mark.parametrize("samples", [1, 7, 100, 1024, 2048])
+def test_identify_frequent_sample_counts(samples):
+    off, adj = gen.rmat(seed=17, scale=11)
+    n = off.size - 1
+    d_off, d_adj = to_dev(off, adj)
+    sampled = torch.empty(n, dtype=torch.int32, device="cuda")
+    lmax = torch.empty(1, dtype=torch.int32, device="cuda")
+    lab = torch.empty(n, dtype=torch.int32, device="cuda")
+    cc.cc_labels(d_off, d_adj, n, adj.size, lab, cc.make_opts(samples=samples, seed=3, sampled_out=sampled,
+                                                              lmax_out=lmax))
+    assert int(u32(lmax)[0]) == oracle.identify_frequent(u32(sampled), samples, 3)
+    assert np.array_equal(u32(lab), oracle.cc_bfs(off, adj))
+    with pytest.raises(cc.CCError):
+        cc.cc_labels(d_off, d_adj, n, adj.size, lab, cc.make_opts(samples=2049))
