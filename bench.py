@@ -223,6 +223,36 @@ def byte_model(off_h_deg_pos, n, m, k, ctr, sampled, final, mid_ran):
     return B, {"relabelled": relab, "sampled_nonroots": nonroot, "mid_nonroots_bound": npos}
 
 
+def floors(cc, d_off, d_adj, n, m, x, stream, cc_ms, reps=3):
+    """MapEdges / GatherEdges on the same CSR, a uniform random 4 B gather over an
+    n-sized array and a streaming copy: the empirical floors next to t_CC."""
+    import torch
+
+    def timed(fn):
+        ts = []
+        for _ in range(reps + 1):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return min(ts[1:])
+    out = torch.empty(n, dtype=torch.int32, device=d_off.device)
+    acc = torch.zeros(1, dtype=torch.int32, device=d_off.device)
+    t_map = timed(lambda: cc.map_edges(d_off, d_adj, n, out, stream))
+    t_gather = timed(lambda: cc.gather_edges(d_off, d_adj, n, x, out, stream))
+    cnt = 1 << 28
+    t_rand = timed(lambda: cc.random_gather(x, n, cnt, 7, acc, stream))
+    words = (n // 4) * 4
+    t_copy = timed(lambda: cc.copy(x, out, words, stream))
+    return {"map_edges_ms": round(t_map, 4), "gather_edges_ms": round(t_gather, 4),
+            "t_cc_over_t_gather": round(cc_ms / t_gather, 4), "t_cc_over_t_map": round(cc_ms / t_map, 4),
+            "random_gather": {"loads": cnt, "array_bytes": 4 * n, "ms": round(t_rand, 4),
+                              "Gloads_per_s": round(cnt / (t_rand * 1e-3) / 1e9, 2)},
+            "copy_GBps": round(2 * 4 * words / (t_copy * 1e-3) / 1e9, 1)}
+
+
 def run_ours(a, rank, ws):
     import numpy as np
     import torch
@@ -341,6 +371,9 @@ def run_ours(a, rank, ws):
             "roofline": roofline, "finish": finish, "sampling": sampling, "kernels": kernels,
             "counters": ctr, "byte_model_extra": extra, "gpu_launches": int(launches), "clocks": clocks}
 
+    # ---- measurement floors (K10, Table 8 analogue P:3732-3799), outside the timed region
+    line["floors"] = floors(cc, d_off, d_adj, n, m, labels, stream, mean_ms)
+
     # ---- e2e: the same metric through the C ABI with HOST (pinned) buffers
     if not a.no_e2e and a.e2e_steps > 0:
         h_off = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
@@ -362,8 +395,14 @@ def run_ours(a, rank, ws):
                 ts.append(e0.elapsed_time(e1))
         e2e_ms = reduce_max(statistics.mean(ts), ws)
         ok = bool(np.array_equal(h_lab.numpy().view(np.uint32), final))
+        # zero-copy: the kernels read the offsets, one 16 B window of list heads per
+        # non-isolated vertex and the finish candidates' lists straight from pinned
+        # host memory, and H6 writes the labels into it (cc.h §Memory)
+        h2d = 8 * (n + 1) + 16 * nonisolated + 16 * ctr["finish_vertices"] + 4 * ctr["finish_edges"]
         line["e2e"] = {"value": round(aggregate_value(m, e2e_ms * 1e-3, ws) / 1e9, 4), "unit": "GTEPS",
-                       "h2d_bytes_per_step": 8 * (n + 1) + 4 * m, "d2h_bytes_per_step": 4 * n,
+                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4 * n,
+                       "host_resident_csr_bytes": 8 * (n + 1) + 4 * m,
+                       "path": "cc_labels with pinned host offsets/adj/labels (zero-copy through UVA)",
                        "ms_per_step": round(e2e_ms, 3), "steps": a.e2e_steps, "labels_match_device_path": ok}
         del h_off, h_adj, h_lab
 

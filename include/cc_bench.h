@@ -21,7 +21,9 @@ extern "C" {
 #endif
 
 /* MapEdges: out[u] = sum over e in [off[u], off[u+1]) of 1,
- * computed by actually reading every adj entry (adj[e] < 0xFFFFFFFF counts 1). */
+ * computed by actually reading every adj entry (adj[e] < 0xFFFFFFFF counts 1).
+ * Both edge kernels read m = offsets[n] back to the host first (one sync) and
+ * zero `out`; the sweep itself is edge-balanced (4096 entries per warp). */
 cc_status cc_bench_map_edges(const int64_t* offsets, const uint32_t* adj, uint32_t n,
                              uint32_t* out, void* stream);
 

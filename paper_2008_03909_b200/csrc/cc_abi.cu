@@ -52,6 +52,24 @@ bool is_device_ptr(const void* p)
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+MemKind mem_kind(const void* p, void** dev_alias)
+{
+    if (dev_alias) *dev_alias = const_cast<void*>(p);
+    if (!p) return MEM_DEVICE;
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return MEM_PAGEABLE;
+    }
+    if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return MEM_DEVICE;
+    if (a.type == cudaMemoryTypeHost && a.devicePointer) {
+        if (dev_alias) *dev_alias = a.devicePointer;
+        return MEM_PINNED;
+    }
+    return MEM_PAGEABLE;
+}
+
 static void init_pool_once()
 {
     static std::once_flag flag[64];
@@ -162,6 +180,10 @@ size_t cc_workspace_bytes(uint32_t n, int64_t m, uint32_t kout_k, int op)
     return b;
 }
 
+// Array arguments: device memory is used in place; pinned host memory is used
+// in place too (zero-copy through UVA: the kernels read only the offsets, the
+// sampled list heads and the finish candidates' lists, and H6 writes the
+// labels straight into it); pageable host memory is staged through scratch.
 cc_status cc_labels(const int64_t* offsets, const uint32_t* adj, uint32_t n, int64_t m, uint32_t* labels,
                     const cc_opts* opts, void* stream)
 {
@@ -171,31 +193,29 @@ cc_status cc_labels(const int64_t* offsets, const uint32_t* adj, uint32_t n, int
     if (n == 0) return CC_OK;
     if (!labels) { set_error("labels is NULL"); return CC_EINVAL; }
     cudaStream_t s = (cudaStream_t)stream;
-    const bool dev = is_device_ptr(offsets) && is_device_ptr(adj) && is_device_ptr(labels);
-    if (dev) {
-        if (o.flags & CC_FLAG_VALIDATE) {
-            rc = validate_csr(offsets, adj, n, m, s);
-            if (rc) return rc;
-        }
-        return static_pipeline(offsets, adj, n, m, labels, nullptr, nullptr, false, o, s);
-    }
-    // host buffers: stage in, compute, stage out, synchronise
+    void *a_off, *a_adj, *a_lab;
+    const MemKind k_off = mem_kind(offsets, &a_off), k_adj = mem_kind(adj, &a_adj), k_lab = mem_kind(labels, &a_lab);
     Stage st{s, {}};
-    const int64_t* d_off = offsets;
-    const uint32_t* d_adj = adj;
-    uint32_t* d_lab = labels;
-    if (!is_device_ptr(offsets)) CC_CUDA_TRY(st.in(offsets, (size_t)n + 1, (int64_t**)&d_off));
-    if (!is_device_ptr(adj)) CC_CUDA_TRY(st.in(adj, (size_t)m, (uint32_t**)&d_adj));
-    if (!is_device_ptr(labels)) CC_CUDA_TRY(st.in((const uint32_t*)nullptr, (size_t)n, &d_lab));
+    const int64_t* d_off = (const int64_t*)a_off;
+    const uint32_t* d_adj = (const uint32_t*)a_adj;
+    if (k_off == MEM_PAGEABLE) CC_CUDA_TRY(st.in(offsets, (size_t)n + 1, (int64_t**)&d_off));
+    if (k_adj == MEM_PAGEABLE) CC_CUDA_TRY(st.in(adj, (size_t)m, (uint32_t**)&d_adj));
     if (o.flags & CC_FLAG_VALIDATE) {
         rc = validate_csr(d_off, d_adj, n, m, s);
         if (rc) return rc;
     }
-    rc = static_pipeline(d_off, d_adj, n, m, d_lab, nullptr, nullptr, false, o, s);
+    // the parent array must be device memory: the caller's labels if they are, else scratch
+    uint32_t* P = k_lab == MEM_DEVICE ? labels : nullptr;
+    uint32_t* out = k_lab == MEM_DEVICE ? labels : (k_lab == MEM_PINNED ? (uint32_t*)a_lab : nullptr);
+    uint32_t* staged = nullptr;
+    if (k_lab == MEM_PAGEABLE) {
+        CC_CUDA_TRY(st.in((const uint32_t*)nullptr, (size_t)n, &staged));
+        out = staged;
+    }
+    rc = static_pipeline(d_off, d_adj, n, m, P, out, nullptr, nullptr, false, o, s);
     if (rc) return rc;
-    if (d_lab != labels)
-        CC_CUDA_TRY(cudaMemcpyAsync(labels, d_lab, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, s));
-    CC_CUDA_TRY(cudaStreamSynchronize(s));
+    if (staged) CC_CUDA_TRY(cudaMemcpyAsync(labels, staged, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, s));
+    if (k_off != MEM_DEVICE || k_adj != MEM_DEVICE || k_lab != MEM_DEVICE) CC_CUDA_TRY(cudaStreamSynchronize(s));
     return CC_OK;
 }
 
@@ -207,48 +227,50 @@ cc_status cc_spanning_forest(const int64_t* offsets, const uint32_t* adj, uint32
     if (rc) return rc;
     if (!num_edges) { set_error("num_edges is NULL"); return CC_EINVAL; }
     cudaStream_t s = (cudaStream_t)stream;
+    void *a_off, *a_adj, *a_edges, *a_ne, *a_lab;
+    const MemKind k_ne = mem_kind(num_edges, &a_ne);
     if (n == 0) {
-        if (is_device_ptr(num_edges)) CC_CUDA_TRY(cudaMemsetAsync(num_edges, 0, sizeof(int64_t), s));
+        if (k_ne == MEM_DEVICE) CC_CUDA_TRY(cudaMemsetAsync(num_edges, 0, sizeof(int64_t), s));
         else *num_edges = 0;
         return CC_OK;
     }
     if (!edges) { set_error("edges is NULL"); return CC_EINVAL; }
-    const bool dev = is_device_ptr(offsets) && is_device_ptr(adj) && is_device_ptr(edges) &&
-                     is_device_ptr(num_edges) && is_device_ptr(labels);
-    if (dev) {
-        if (o.flags & CC_FLAG_VALIDATE) {
-            rc = validate_csr(offsets, adj, n, m, s);
-            if (rc) return rc;
-        }
-        return static_pipeline(offsets, adj, n, m, labels, edges, num_edges, true, o, s);
-    }
+    const MemKind k_off = mem_kind(offsets, &a_off), k_adj = mem_kind(adj, &a_adj);
+    const MemKind k_edges = mem_kind(edges, &a_edges), k_lab = mem_kind(labels, &a_lab);
     Stage st{s, {}};
-    const int64_t* d_off = offsets;
-    const uint32_t* d_adj = adj;
-    uint32_t* d_edges = edges;
-    int64_t* d_ne = num_edges;
-    uint32_t* d_lab = labels;
-    if (!is_device_ptr(offsets)) CC_CUDA_TRY(st.in(offsets, (size_t)n + 1, (int64_t**)&d_off));
-    if (!is_device_ptr(adj)) CC_CUDA_TRY(st.in(adj, (size_t)m, (uint32_t**)&d_adj));
-    if (!is_device_ptr(edges)) CC_CUDA_TRY(st.in((const uint32_t*)nullptr, 2 * (size_t)n, &d_edges));
-    if (!is_device_ptr(num_edges)) CC_CUDA_TRY(st.in((const int64_t*)nullptr, 1, &d_ne));
-    if (labels && !is_device_ptr(labels)) CC_CUDA_TRY(st.in((const uint32_t*)nullptr, (size_t)n, &d_lab));
+    const int64_t* d_off = (const int64_t*)a_off;
+    const uint32_t* d_adj = (const uint32_t*)a_adj;
+    uint32_t* d_edges = (uint32_t*)a_edges;
+    int64_t* d_ne = (int64_t*)a_ne;
+    if (k_off == MEM_PAGEABLE) CC_CUDA_TRY(st.in(offsets, (size_t)n + 1, (int64_t**)&d_off));
+    if (k_adj == MEM_PAGEABLE) CC_CUDA_TRY(st.in(adj, (size_t)m, (uint32_t**)&d_adj));
+    if (k_edges == MEM_PAGEABLE) CC_CUDA_TRY(st.in((const uint32_t*)nullptr, 2 * (size_t)n, &d_edges));
+    if (k_ne == MEM_PAGEABLE) CC_CUDA_TRY(st.in((const int64_t*)nullptr, 1, &d_ne));
     if (o.flags & CC_FLAG_VALIDATE) {
         rc = validate_csr(d_off, d_adj, n, m, s);
         if (rc) return rc;
     }
-    rc = static_pipeline(d_off, d_adj, n, m, d_lab, d_edges, d_ne, true, o, s);
+    uint32_t* P = (labels && k_lab == MEM_DEVICE) ? labels : nullptr;
+    uint32_t* out = labels ? (k_lab == MEM_PAGEABLE ? nullptr : (uint32_t*)a_lab) : nullptr;
+    uint32_t* staged = nullptr;
+    if (labels && k_lab == MEM_PAGEABLE) {
+        CC_CUDA_TRY(st.in((const uint32_t*)nullptr, (size_t)n, &staged));
+        out = staged;
+    }
+    rc = static_pipeline(d_off, d_adj, n, m, P, out, d_edges, d_ne, true, o, s);
     if (rc) return rc;
-    int64_t ne = 0;
-    CC_CUDA_TRY(cudaMemcpyAsync(&ne, d_ne, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    CC_CUDA_TRY(cudaStreamSynchronize(s));
-    if (d_ne != num_edges) *num_edges = ne;
-    else CC_CUDA_TRY(cudaMemcpyAsync(num_edges, d_ne, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
-    if (d_edges != edges)
-        CC_CUDA_TRY(cudaMemcpyAsync(edges, d_edges, sizeof(uint32_t) * 2 * (size_t)ne, cudaMemcpyDeviceToHost, s));
-    if (labels && d_lab != labels)
-        CC_CUDA_TRY(cudaMemcpyAsync(labels, d_lab, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, s));
-    CC_CUDA_TRY(cudaStreamSynchronize(s));
+    const bool host = k_off != MEM_DEVICE || k_adj != MEM_DEVICE || k_edges != MEM_DEVICE || k_ne != MEM_DEVICE ||
+                      (labels && k_lab != MEM_DEVICE);
+    if (k_edges == MEM_PAGEABLE || k_ne == MEM_PAGEABLE) {
+        int64_t ne = 0;
+        CC_CUDA_TRY(cudaMemcpyAsync(&ne, d_ne, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        CC_CUDA_TRY(cudaStreamSynchronize(s));
+        if (k_ne == MEM_PAGEABLE) *num_edges = ne;
+        if (k_edges == MEM_PAGEABLE)
+            CC_CUDA_TRY(cudaMemcpyAsync(edges, d_edges, sizeof(uint32_t) * 2 * (size_t)ne, cudaMemcpyDeviceToHost, s));
+    }
+    if (staged) CC_CUDA_TRY(cudaMemcpyAsync(labels, staged, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, s));
+    if (host) CC_CUDA_TRY(cudaStreamSynchronize(s));
     return CC_OK;
 }
 

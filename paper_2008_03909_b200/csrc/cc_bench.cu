@@ -10,41 +10,59 @@
 
 namespace ccb {
 
-// One warp per tile of 32 consecutive vertices: the warp sweeps the tile's
-// concatenated lists with coalesced loads; each entry's owner lane is found by
-// a binary search over the 33 tile offsets in shared memory and its value is
-// accumulated with a shared-memory atomic (segmented reduction).
+// Edge-balanced sweep: warp c owns adjacency entries [c*kChunk, (c+1)*kChunk)
+// whatever the degrees (hubs are split across warps), finds the owner of its
+// first entry by a binary search of the offsets, then reads 4 entries per lane
+// per iteration (coalesced, 4 loads in flight).  Each lane follows the owner of
+// its next entry with a monotone pointer and adds its running sum into out[]
+// with one atomic whenever the owner changes (out is zeroed first).
+constexpr int64_t kChunk = 4096;
+
 template <bool GATHER>
 __global__ void __launch_bounds__(kBlock) k_edges(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
-                                                  uint32_t n, const uint32_t* __restrict__ x,
+                                                  uint32_t n, int64_t m, const uint32_t* __restrict__ x,
                                                   uint32_t* __restrict__ out)
 {
-    __shared__ int64_t s_off[kBlock / 32][33];
-    __shared__ uint32_t s_acc[kBlock / 32][32];
-    const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t t = warp * 32; t < n; t += nwarps * 32) {
-        const uint64_t v = t + lane;
-        const int64_t m_end = off[n];
-        s_off[w][lane] = v < n ? off[v] : m_end;
-        if (lane == 0) s_off[w][32] = (t + 32 < n) ? off[t + 32] : m_end;
-        s_acc[w][lane] = 0;
-        __syncwarp();
-        const int64_t tb = s_off[w][0], te = s_off[w][32];
-        for (int64_t i = tb + lane; i < te; i += 32) {
-            const uint32_t a = ld_stream_u32(adj + i);
-            const uint32_t val = GATHER ? x[a] : (a != 0xFFFFFFFFu ? 1u : 0u);
-            int lo = 0, hi = 31;                     // owner: last lane with s_off <= i
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (s_off[w][mid] <= i) lo = mid; else hi = mid - 1;
+    const unsigned lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c0 = warp * kChunk; c0 < m; c0 += nwarps * kChunk) {
+        const int64_t c1 = min(c0 + kChunk, m);
+        uint32_t lo = 0, hi = n;                           // largest v with off[v] <= c0
+        if (lane == 0) {
+            while (hi - lo > 1) {
+                const uint32_t mid = lo + (hi - lo) / 2;
+                if (off[mid] <= c0) lo = mid; else hi = mid;
             }
-            atomicAdd(&s_acc[w][lo], val);
         }
-        __syncwarp();
-        if (v < n) out[v] = s_acc[w][lane];
-        __syncwarp();
+        uint32_t own = __shfl_sync(0xffffffffu, lo, 0);
+        int64_t own_end = off[own + 1];
+        uint32_t run = 0;
+        for (int64_t i0 = c0 + lane; i0 < c1; i0 += 128) {
+            uint32_t val[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int64_t i = i0 + 32 * j;
+                uint32_t a = 0xFFFFFFFFu;
+                if (i < c1) a = __ldcs(adj + i);
+                val[j] = (i < c1) ? (GATHER ? x[a] : (a != 0xFFFFFFFFu ? 1u : 0u)) : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int64_t i = i0 + 32 * j;
+                if (i >= c1) break;
+                if (i >= own_end) {                         // move to the owner of entry i
+                    if (run) atomicAdd(out + own, run);
+                    run = 0;
+                    do {
+                        ++own;
+                        own_end = off[own + 1];
+                    } while (own_end <= i);
+                }
+                run += val[j];
+            }
+        }
+        if (run) atomicAdd(out + own, run);
     }
 }
 
@@ -53,7 +71,17 @@ __global__ void __launch_bounds__(kBlock) k_random_gather(const uint32_t* __rest
 {
     uint32_t acc = 0;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < count; i += 4 * stride) {          // 4 independent loads in flight
+        uint32_t t[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint64_t r = splitmix64(seed + i + j * stride);
+            t[j] = __ldcg(x + (((r & 0xFFFFFFFFull) * len) >> 32));
+        }
+        acc += t[0] + t[1] + t[2] + t[3];
+    }
+    for (; i < count; i += stride) {
         const uint64_t r = splitmix64(seed + i);
         acc += __ldcg(x + (((r & 0xFFFFFFFFull) * len) >> 32));
     }
@@ -77,7 +105,12 @@ cc_status cc_bench_map_edges(const int64_t* offsets, const uint32_t* adj, uint32
 {
     if (n == 0) return CC_OK;
     if (!offsets || !adj || !out) return CC_EINVAL;
-    k_edges<false><<<num_sms() * 16, kBlock, 0, (cudaStream_t)stream>>>(offsets, adj, n, nullptr, out);
+    int64_t m = 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    CC_CUDA_TRY(cudaMemcpyAsync(&m, offsets + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CC_CUDA_TRY(cudaStreamSynchronize(s));
+    CC_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(uint32_t) * n, s));
+    k_edges<false><<<num_sms() * 16, kBlock, 0, s>>>(offsets, adj, n, m, nullptr, out);
     CC_LAUNCH_CHECK("k_edges<map>");
     return CC_OK;
 }
@@ -87,7 +120,12 @@ cc_status cc_bench_gather_edges(const int64_t* offsets, const uint32_t* adj, uin
 {
     if (n == 0) return CC_OK;
     if (!offsets || !adj || !out || !x) return CC_EINVAL;
-    k_edges<true><<<num_sms() * 16, kBlock, 0, (cudaStream_t)stream>>>(offsets, adj, n, x, out);
+    int64_t m = 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    CC_CUDA_TRY(cudaMemcpyAsync(&m, offsets + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CC_CUDA_TRY(cudaStreamSynchronize(s));
+    CC_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(uint32_t) * n, s));
+    k_edges<true><<<num_sms() * 16, kBlock, 0, s>>>(offsets, adj, n, m, x, out);
     CC_LAUNCH_CHECK("k_edges<gather>");
     return CC_OK;
 }

@@ -123,12 +123,13 @@ __device__ __forceinline__ bool link_rem_from(uint32_t* P, uint32_t u, uint32_t 
             t = pu; pu = pv; pv = t;
         }
         if (ru == pu) {                              // ru is a root: hook it (pv < ru)
-            if (cas(P + ru, ru, pv) == ru) {
+            const uint32_t old = cas(P + ru, ru, pv);
+            if (old == ru) {
                 rec.record(ru, u, v);
                 return true;
             }
             if (st) st->casfail();
-            pu = ld_relaxed(P + ru);                 // lost a race: re-read
+            pu = old;                                // lost a race: the CAS returned ru's new parent
             pv = ld_relaxed(P + rv);
             continue;
         }

@@ -178,14 +178,21 @@ cc_status cc_incr_batch(cc_incr* h, const uint32_t* inserts, int64_t n_ins, cons
         if (n_ins || n_q) { set_error("ids >= n = 0"); return CC_EINVAL; }
         return CC_OK;
     }
-    const bool dev = (!n_ins || is_device_ptr(inserts)) && (!n_q || (is_device_ptr(queries) && is_device_ptr(answers)));
-    if (dev) return insert_query(h, inserts, n_ins, queries, n_q, answers, s);
-    // host buffers: stage
+    // device and pinned host arrays are used in place (pinned: zero-copy through
+    // UVA); pageable host arrays are staged
+    void *a_ins, *a_q, *a_ans;
+    const MemKind k_ins = n_ins ? mem_kind(inserts, &a_ins) : MEM_DEVICE;
+    const MemKind k_q = n_q ? mem_kind(queries, &a_q) : MEM_DEVICE;
+    const MemKind k_ans = n_q ? mem_kind(answers, &a_ans) : MEM_DEVICE;
+    if (!n_ins) a_ins = (void*)inserts;
+    if (!n_q) a_q = (void*)queries, a_ans = (void*)answers;
+    if (k_ins == MEM_DEVICE && k_q == MEM_DEVICE && k_ans == MEM_DEVICE)
+        return insert_query(h, inserts, n_ins, queries, n_q, answers, s);
     std::vector<void*> bufs;
     auto release = [&]() { for (void* b : bufs) scratch_free(b, s); };
-    const uint32_t* d_ins = inserts;
-    const uint32_t* d_q = queries;
-    uint8_t* d_ans = answers;
+    const uint32_t* d_ins = (const uint32_t*)a_ins;
+    const uint32_t* d_q = (const uint32_t*)a_q;
+    uint8_t* d_ans = (uint8_t*)a_ans;
     auto stage_in = [&](const void* host, size_t bytes, void** dev_out) -> cudaError_t {
         cudaError_t e = scratch_alloc(dev_out, bytes, s);
         if (e != cudaSuccess) return e;
@@ -193,12 +200,12 @@ cc_status cc_incr_batch(cc_incr* h, const uint32_t* inserts, int64_t n_ins, cons
         return host ? cudaMemcpyAsync(*dev_out, host, bytes, cudaMemcpyHostToDevice, s) : cudaSuccess;
     };
     cudaError_t e = cudaSuccess;
-    if (n_ins && !is_device_ptr(inserts)) e = stage_in(inserts, 8 * (size_t)n_ins, (void**)&d_ins);
-    if (e == cudaSuccess && n_q && !is_device_ptr(queries)) e = stage_in(queries, 8 * (size_t)n_q, (void**)&d_q);
-    if (e == cudaSuccess && n_q && !is_device_ptr(answers)) e = stage_in(nullptr, (size_t)n_q, (void**)&d_ans);
+    if (k_ins == MEM_PAGEABLE) e = stage_in(inserts, 8 * (size_t)n_ins, (void**)&d_ins);
+    if (e == cudaSuccess && k_q == MEM_PAGEABLE) e = stage_in(queries, 8 * (size_t)n_q, (void**)&d_q);
+    if (e == cudaSuccess && k_ans == MEM_PAGEABLE) e = stage_in(nullptr, (size_t)n_q, (void**)&d_ans);
     if (e != cudaSuccess) { release(); return cuda_fail(e, "cc_incr_batch: staging"); }
     cc_status rc = insert_query(h, d_ins, n_ins, d_q, n_q, d_ans, s);
-    if (rc == CC_OK && n_q && d_ans != answers) {
+    if (rc == CC_OK && k_ans == MEM_PAGEABLE) {
         e = cudaMemcpyAsync(answers, d_ans, (size_t)n_q, cudaMemcpyDeviceToHost, s);
         if (e != cudaSuccess) rc = cuda_fail(e, "cc_incr_batch: answers");
     }
@@ -217,16 +224,17 @@ cc_status cc_incr_labels(cc_incr* h, uint32_t* labels, void* stream)
     if (!labels) { set_error("labels is NULL"); return CC_EINVAL; }
     cudaStream_t s = (cudaStream_t)stream;
     h->last = s;
-    uint32_t* d = labels;
-    const bool dev = is_device_ptr(labels);
-    if (!dev) CC_CUDA_TRY(scratch_alloc((void**)&d, sizeof(uint32_t) * h->n, s));
+    void* a_lab;
+    const MemKind kl = mem_kind(labels, &a_lab);
+    uint32_t* d = (uint32_t*)a_lab;
+    if (kl == MEM_PAGEABLE) CC_CUDA_TRY(scratch_alloc((void**)&d, sizeof(uint32_t) * h->n, s));
     k_labels<<<nblocks(h->n), kBlock, 0, s>>>(h->P, h->n, d);
     CC_LAUNCH_CHECK("k_labels");
-    if (!dev) {
+    if (kl == MEM_PAGEABLE) {
         CC_CUDA_TRY(cudaMemcpyAsync(labels, d, sizeof(uint32_t) * h->n, cudaMemcpyDeviceToHost, s));
-        CC_CUDA_TRY(cudaStreamSynchronize(s));
         scratch_free(d, s);
     }
+    if (kl != MEM_DEVICE) CC_CUDA_TRY(cudaStreamSynchronize(s));
     return CC_OK;
 }
 

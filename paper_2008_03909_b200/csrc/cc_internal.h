@@ -21,6 +21,12 @@ inline void count_launch(uint64_t k = 1) { g_launches.fetch_add(k, std::memory_o
 int num_sms();
 bool is_device_ptr(const void* p);
 
+// Where an array argument lives: device memory, pinned host memory (device-
+// accessible through UVA: used in place, zero-copy), or pageable host memory
+// (staged through device scratch).
+enum MemKind { MEM_DEVICE = 0, MEM_PINNED = 1, MEM_PAGEABLE = 2 };
+MemKind mem_kind(const void* p, void** dev_alias);
+
 // Stream-ordered scratch from the device's default memory pool (cached).
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s);
 void scratch_free(void* p, cudaStream_t s);
@@ -42,9 +48,9 @@ constexpr int kBlock = 256;
     } while (0)
 
 // Device pipeline entry points (device pointers only; validated args).
-cc_status static_pipeline(const int64_t* off, const uint32_t* adj, uint32_t n, int64_t m,
-                          uint32_t* labels, uint32_t* edges, int64_t* num_edges, bool sf,
-                          const cc_opts& o, cudaStream_t s);
+cc_status static_pipeline(const int64_t* off, const uint32_t* adj, uint32_t n, int64_t m, uint32_t* P,
+                          uint32_t* labels_out, uint32_t* edges, int64_t* num_edges, bool sf, const cc_opts& o,
+                          cudaStream_t s);
 cc_status validate_csr(const int64_t* off, const uint32_t* adj, uint32_t n, int64_t m, cudaStream_t s);
 
 }  // namespace ccb

@@ -80,9 +80,19 @@ constexpr int kV = 8;                        // vertices per lane
 constexpr int kWarpTile = 32 * kV;           // 256 vertices per warp
 constexpr int kBlockTile = kWarpTile * (kBlock / 32);
 
-template <bool HYBRID, bool SF>
+// Sampled neighbours j = 0 and j = 1 of a list starting at o: with WIN (adj
+// 16-byte aligned, in pinned host memory) both come from ONE aligned 16-byte
+// window load when they share it (3 of 4 list starts), halving the PCIe read
+// requests of the zero-copy path.
+template <bool WIN>
+__device__ __forceinline__ uint32_t pick4(uint4 w, uint32_t r)
+{
+    return r == 0 ? w.x : r == 1 ? w.y : r == 2 ? w.z : w.w;
+}
+
+template <bool HYBRID, bool SF, bool WIN>
 __global__ void __launch_bounds__(kBlock, 3) k_sample_init(
-    const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, uint32_t n, uint32_t k,
+    const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, uint32_t n, int64_t m, uint32_t k,
     uint64_t seed, uint32_t full_deg, uint32_t* __restrict__ P, uint2* __restrict__ F,
     uint2* __restrict__ pend, uint32_t* __restrict__ bm, Ctl* ctl, cc_counters* cnt)
 {
@@ -112,10 +122,22 @@ __global__ void __launch_bounds__(kBlock, 3) k_sample_init(
 #pragma unroll
     for (int j = 0; j < kV; ++j) {
         const uint64_t u = wbase + 32 * j + lane;
-        v0[j] = (d[j] > 0 && k > 0) ? __ldg(adj + o[j]) : kSentinel;
         uint32_t i1 = 1;
         if (HYBRID && d[j] > 0) i1 = uniform_below(mix(seed, KOUT_STREAM, u * 64 + 1), d[j]);
-        v1[j] = (k > 1 && (HYBRID ? d[j] > 0 : d[j] > 1)) ? __ldg(adj + o[j] + i1) : kSentinel;
+        const bool need0 = d[j] > 0 && k > 0;
+        const bool need1 = k > 1 && (HYBRID ? d[j] > 0 : d[j] > 1);
+        v0[j] = v1[j] = kSentinel;
+        const int64_t b4 = o[j] & ~(int64_t)3;
+        const uint32_t r = (uint32_t)(o[j] & 3);
+        if (WIN && need0 && b4 + 4 <= m) {
+            const uint4 wv = __ldg(reinterpret_cast<const uint4*>(adj + b4));
+            v0[j] = pick4<WIN>(wv, r);
+            if (need1 && r + i1 < 4) v1[j] = pick4<WIN>(wv, r + i1);
+            else if (need1) v1[j] = __ldg(adj + o[j] + i1);
+        } else {
+            if (need0) v0[j] = __ldg(adj + o[j]);
+            if (need1) v1[j] = __ldg(adj + o[j] + i1);
+        }
     }
     uint32_t c[kV];
     uint32_t bits = 0, nwl = 0;
@@ -824,8 +846,14 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
         CC_CUDA_TRY(mark(CC_MARK_START));
         // H1 + H2 (first round) + finish bitmap
         const uint32_t nblk0 = (uint32_t)(((uint64_t)n + kBlockTile - 1) / kBlockTile);
-        k_sample_init<HYBRID, SF><<<nblk0, kBlock, 0, s>>>(off, adj, n, k, o.seed, full_deg, P, F, pend, bm, ctl,
-                                                          o.counters);
+        // 16-byte list-head windows pay off when adj is read over PCIe (pinned host,
+        // zero-copy); from HBM two 4-byte loads of the same sector are cheaper
+        if (aligned16(adj) && mem_kind(adj, nullptr) == MEM_PINNED)
+            k_sample_init<HYBRID, SF, true><<<nblk0, kBlock, 0, s>>>(off, adj, n, m, k, o.seed, full_deg, P, F, pend,
+                                                                    bm, ctl, o.counters);
+        else
+            k_sample_init<HYBRID, SF, false><<<nblk0, kBlock, 0, s>>>(off, adj, n, m, k, o.seed, full_deg, P, F, pend,
+                                                                     bm, ctl, o.counters);
         CC_LAUNCH_CHECK("k_sample_init");
         CC_CUDA_TRY(mark(CC_MARK_INIT));
         // shorten the first-round chains before the CAS links when they are long
@@ -920,24 +948,29 @@ static cc_status dispatch_mode(const int64_t* off, const uint32_t* adj, uint32_t
     return run<0, SF, HYBRID>(off, adj, n, m, P, edges, num_edges, labels_out, o, s);
 }
 
-cc_status static_pipeline(const int64_t* off, const uint32_t* adj, uint32_t n, int64_t m, uint32_t* labels,
-                          uint32_t* edges, int64_t* num_edges, bool sf, const cc_opts& o, cudaStream_t s)
+cc_status static_pipeline(const int64_t* off, const uint32_t* adj, uint32_t n, int64_t m, uint32_t* P,
+                          uint32_t* labels_out, uint32_t* edges, int64_t* num_edges, bool sf, const cc_opts& o,
+                          cudaStream_t s)
 {
-    // cc_labels: labels is the parent array (in place).  cc_spanning_forest:
-    // a scratch parent array; labels (optional) receives the final compress.
-    uint32_t* P = labels;
-    uint32_t* out = nullptr;
-    if (sf && !labels) CC_CUDA_TRY(scratch_alloc((void**)&P, sizeof(uint32_t) * (size_t)n, s));
+    // P: the parent array (device memory; the caller's labels buffer for an
+    // in-place cc_labels).  NULL: library scratch.  labels_out: where H6 writes
+    // the labels when that is not P itself (NULL: nowhere).
+    uint32_t* scratch = nullptr;
+    if (!P) {
+        CC_CUDA_TRY(scratch_alloc((void**)&scratch, sizeof(uint32_t) * (size_t)n, s));
+        P = scratch;
+    }
+    uint32_t* out = labels_out == P ? nullptr : labels_out;
     const bool hybrid = o.kout_variant == CC_VARIANT_HYBRID;
     cc_status rc;
     if (sf) {
         rc = hybrid ? dispatch_mode<true, true>(off, adj, n, m, P, edges, num_edges, out, o, s)
                     : dispatch_mode<true, false>(off, adj, n, m, P, edges, num_edges, out, o, s);
-        if (!labels) scratch_free(P, s);
     } else {
         rc = hybrid ? dispatch_mode<false, true>(off, adj, n, m, P, edges, num_edges, out, o, s)
                     : dispatch_mode<false, false>(off, adj, n, m, P, edges, num_edges, out, o, s);
     }
+    scratch_free(scratch, s);
     return rc;
 }
 

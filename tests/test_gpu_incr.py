@@ -118,3 +118,22 @@ def test_host_buffers():
     h.close()
     assert np.array_equal(np.concatenate(outs), want)
     assert np.array_equal(lab, want_lab)
+
+
+def test_pinned_host_buffers_zero_copy():
+    n = 1 << 11
+    batches = [gen.incr_batch(seed=9, scale=11, b=b, n_ins=500, n_q=200) for b in range(4)]
+    want, want_lab = oracle.incr_run(n, batches, want_labels=True)
+    h = cc.Incr(n)
+    outs = []
+    for ins, qs in batches:
+        ti = torch.from_numpy(ins.view(np.int32)).pin_memory()
+        tq = torch.from_numpy(qs.view(np.int32)).pin_memory()
+        ta = torch.zeros(qs.shape[0], dtype=torch.uint8).pin_memory()
+        h.batch(ti, ins.shape[0], tq, qs.shape[0], ta)
+        outs.append(ta.numpy().copy())
+    lab = torch.empty(n, dtype=torch.int32).pin_memory()
+    h.labels(lab)
+    h.close()
+    assert np.array_equal(np.concatenate(outs), want)
+    assert np.array_equal(lab.numpy().view(np.uint32), want_lab)

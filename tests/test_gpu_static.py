@@ -288,3 +288,28 @@ def test_identify_frequent_sample_counts(samples):
     assert np.array_equal(u32(lab), oracle.cc_bfs(off, adj))
     with pytest.raises(cc.CCError):
         cc.cc_labels(d_off, d_adj, n, adj.size, lab, cc.make_opts(samples=2049))
+
+
+def test_pinned_host_buffers_zero_copy():
+    """Pinned host arrays are used in place (zero-copy): same bytes as the device path."""
+    off, adj = gen.rmat(seed=18, scale=13)
+    n = off.size - 1
+    h_off = torch.from_numpy(off).pin_memory()
+    h_adj = torch.from_numpy(adj.view(np.int32)).pin_memory()
+    h_lab = torch.empty(n, dtype=torch.int32).pin_memory()
+    for k in (0, 1, 2):
+        cc.cc_labels(h_off, h_adj, n, adj.size, h_lab, cc.make_opts(k=k))
+        assert np.array_equal(h_lab.numpy().view(np.uint32), oracle.cc_bfs(off, adj)), k
+    h_edges = torch.empty((n, 2), dtype=torch.int32).pin_memory()
+    h_ne = torch.zeros(1, dtype=torch.int64).pin_memory()
+    cc.cc_spanning_forest(h_off, h_adj, n, adj.size, h_edges, h_ne, h_lab, cc.make_opts())
+    want = oracle.cc_bfs(off, adj)
+    c = int(np.sum(want == np.arange(n)))
+    assert int(h_ne[0]) == n - c
+    assert oracle.forest_check(off, adj, c, h_edges[: int(h_ne[0])].numpy().view(np.uint32))[0] == 0
+    assert np.array_equal(h_lab.numpy().view(np.uint32), want)
+    # mixed: device offsets, pinned adjacency, device labels
+    d_off = torch.from_numpy(off).cuda()
+    d_lab = torch.empty(n, dtype=torch.int32, device="cuda")
+    cc.cc_labels(d_off, h_adj, n, adj.size, d_lab, cc.make_opts())
+    assert np.array_equal(u32(d_lab), want)
