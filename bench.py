@@ -211,12 +211,13 @@ def byte_model(off_h_deg_pos, n, m, k, ctr, sampled, final, mid_ran):
         # pending read + P[u], P[v] gathers + hook CAS
         "k_link_pending": 8 * pend + 8 * pend + 4 * ctr["sample_hooks"],
         "k_identify": 4 * 1024,
-        # fused H3 + H5 scan: P read + bitmap + compress writes + candidate queue writes
-        "k_finish": 4 * n + n // 8 + 4 * ctr["compress_writes"] + 4 * fin_v,
+        # fused H3 + H5 scan: P read + bitmap + first-level parent reads + compress writes
+        # + candidate queue writes
+        "k_finish": 4 * n + n // 8 + 4 * ctr["finish_gathers"] + 4 * ctr["compress_writes"] + 4 * fin_v,
         # H5 edge work: queue read + offsets pair + adj + P[v] gather per edge + hook CAS
         "k_finish_proc": 4 * fin_v + 16 * fin_v + 8 * fin_e + 4 * ctr["finish_hooks"],
-        # P read + changed-label writes
-        "k_compress_H6": 4 * n + 4 * relab,
+        # P read + first-level parent reads + changed-label writes
+        "k_compress_H6": 4 * n + 4 * ctr["h6_gathers"] + 4 * ctr["h6_writes"],
     }
     B["finish_phase"] = B["k_finish"] + B["k_finish_proc"] + B["k_compress_H6"]
     B["sampling_phase"] = B["k_sample_init"] + B["k_compress_mid"] + B["k_link_pending"]

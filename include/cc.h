@@ -106,6 +106,9 @@ typedef struct {
     uint64_t link_steps;       /* Rem-loop iterations of k_link_pending's walked links*/
     uint64_t cas_failures;     /* hook CAS that lost a race in k_link_pending        */
     uint64_t probe_deep;       /* probe samples whose round-0 chain exceeded 8 steps */
+    uint64_t finish_gathers;   /* first-level parent reads of k_finish (P[P[v]])      */
+    uint64_t h6_writes;        /* label slots rewritten by the final compress (H6)   */
+    uint64_t h6_gathers;       /* first-level parent reads of the final compress     */
 } cc_counters;
 
 typedef struct {

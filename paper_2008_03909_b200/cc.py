@@ -50,7 +50,7 @@ class Timings(ctypes.Structure):
 
 COUNTER_FIELDS = ["pending_links", "worklist", "finish_vertices", "finish_edges", "sample_hooks", "finish_hooks",
                   "big_vertices", "compress_writes",
-                  "link_steps", "cas_failures", "probe_deep"]
+                  "link_steps", "cas_failures", "probe_deep", "finish_gathers", "h6_writes", "h6_gathers"]
 
 
 class Opts(ctypes.Structure):

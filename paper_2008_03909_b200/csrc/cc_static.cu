@@ -224,6 +224,13 @@ __global__ void __launch_bounds__(kBlock, 3) k_sample_init(
 // most parents are already compressed when their children are visited.
 // Each thread owns 2 x uint4 = 8 slots (2 x 16 B loads in flight per thread)
 // and writes a uint4 back only if one of its slots changed.
+// resident blocks per SM the streaming passes are compiled for (register caps)
+#ifndef CC_COMPRESS_MINB
+#define CC_COMPRESS_MINB 8
+#endif
+#ifndef CC_FINISH_MINB
+#define CC_FINISH_MINB 8
+#endif
 constexpr int kCV = 8;                                   // slots per thread
 constexpr int kCTile = kBlock * kCV;                     // 2048 slots per block
 
@@ -242,14 +249,19 @@ __device__ __forceinline__ uint32_t root_plain(const uint32_t* P, uint32_t r)
 // rare after a compress, continue one slot at a time.  (A level-by-level
 // variant that batches every level measured slower on C4: more registers
 // and a serial live-mask loop for little extra parallelism.)
-__device__ __forceinline__ void roots8(const uint32_t* P, const uint32_t (&vv)[8], const uint32_t (&pp)[8],
-                                       uint32_t (&rr)[8])
+__device__ __forceinline__ uint32_t roots8(const uint32_t* P, const uint32_t (&vv)[8], const uint32_t (&pp)[8],
+                                           uint32_t (&rr)[8], uint32_t known_root = kSentinel)
 {
-    uint32_t q[8];
+    uint32_t q[8], gathers = 0;
 #pragma unroll
-    for (int s = 0; s < 8; ++s) q[s] = pp[s] == vv[s] ? pp[s] : P[pp[s]];
+    for (int s = 0; s < 8; ++s) {
+        const bool g = !(pp[s] == vv[s] || pp[s] == known_root);
+        q[s] = g ? P[pp[s]] : pp[s];
+        gathers += g;
+    }
 #pragma unroll
     for (int s = 0; s < 8; ++s) rr[s] = q[s] == pp[s] ? pp[s] : root_plain(P, q[s]);
+    return gathers;                                      // first-level parent reads issued
 }
 
 __device__ __forceinline__ uint32_t nchanged4(uint4 a, uint4 b)
@@ -257,11 +269,12 @@ __device__ __forceinline__ uint32_t nchanged4(uint4 a, uint4 b)
     return (a.x != b.x) + (a.y != b.y) + (a.z != b.z) + (a.w != b.w);
 }
 
-__global__ void __launch_bounds__(kBlock) k_compress(uint32_t* P, uint32_t n, uint32_t* out, cc_counters* cnt,
-                                                     const Ctl* gate)
+template <bool CNT>
+__global__ void __launch_bounds__(kBlock, CC_COMPRESS_MINB) k_compress(uint32_t* P, uint32_t n, uint32_t* out,
+                                                                       cc_counters* cnt, const Ctl* gate)
 {
     if (gate && gate->skip_mid) return;
-    uint32_t writes = 0;
+    uint32_t writes = 0, gathers = 0;
     const uint64_t ntiles = ((uint64_t)n + kCTile - 1) / kCTile;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {    // tiles in ascending waves
         const uint64_t base = tile * kCTile;
@@ -273,10 +286,11 @@ __global__ void __launch_bounds__(kBlock) k_compress(uint32_t* P, uint32_t n, ui
             uint32_t vv[8], rr[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) vv[j] = (uint32_t)((j < 4 ? i0 : i1) + (j & 3));
-            roots8(P, vv, pp, rr);
+            const uint32_t g = roots8(P, vv, pp, rr);
+            if (CNT) gathers += g;
             const uint4 r0 = make_uint4(rr[0], rr[1], rr[2], rr[3]), r1 = make_uint4(rr[4], rr[5], rr[6], rr[7]);
             const uint32_t c0 = nchanged4(r0, a), c1 = nchanged4(r1, c);
-            writes += c0 + c1;
+            if (CNT) writes += c0 + c1;
             if (c0) reinterpret_cast<uint4*>(P)[i0 >> 2] = r0;
             if (c1) reinterpret_cast<uint4*>(P)[i1 >> 2] = r1;
             if (out) {
@@ -288,12 +302,19 @@ __global__ void __launch_bounds__(kBlock) k_compress(uint32_t* P, uint32_t n, ui
                 const uint32_t v = (uint32_t)v64;
                 const uint32_t p = P[v];
                 const uint32_t r = p == v ? v : root_plain(P, p);
-                if (r != p) { P[v] = r; ++writes; }
+                if (CNT) gathers += p != v;
+                if (r != p) {
+                    P[v] = r;
+                    if (CNT) ++writes;
+                }
                 if (out) out[v] = r;
             }
         }
     }
-    if (cnt) warp_count(&cnt->compress_writes, writes);
+    if (CNT) {
+        warp_count(&cnt->h6_writes, writes);
+        warp_count(&cnt->h6_gathers, gathers);
+    }
 }
 
 // scalar variant for buffers that are not 16-byte aligned
@@ -310,7 +331,7 @@ __global__ void __launch_bounds__(kBlock) k_compress_scalar(uint32_t* P, uint32_
         if (r != p) { P[v] = r; writes = 1; }
         if (out) out[v] = r;
     }
-    if (cnt) warp_count(&cnt->compress_writes, writes);
+    if (cnt) warp_count(&cnt->h6_writes, writes);
 }
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
@@ -321,9 +342,9 @@ static cc_status launch_compress(uint32_t* P, uint32_t n, uint32_t* out, cc_coun
     // a gated (maybe skipped) compress runs as a persistent grid so that a skip
     // costs one short wave, not 65k empty blocks; otherwise one block per tile
     const uint64_t ntiles = ((uint64_t)n + kCTile - 1) / kCTile;
-    if (aligned16(P) && aligned16(out))
-        k_compress<<<(unsigned)(gate ? std::min<uint64_t>(ntiles, (uint64_t)num_sms() * 8) : ntiles), kBlock, 0, s>>>(
-            P, n, out, cnt, gate);
+    const unsigned grid = (unsigned)(gate ? std::min<uint64_t>(ntiles, (uint64_t)num_sms() * 8) : ntiles);
+    if (aligned16(P) && aligned16(out) && cnt) k_compress<true><<<grid, kBlock, 0, s>>>(P, n, out, cnt, gate);
+    else if (aligned16(P) && aligned16(out)) k_compress<false><<<grid, kBlock, 0, s>>>(P, n, out, nullptr, gate);
     else
         k_compress_scalar<<<(unsigned)(((uint64_t)n + kBlock - 1) / kBlock), kBlock, 0, s>>>(P, n, out, cnt, gate);
     CC_LAUNCH_CHECK(what);
@@ -486,14 +507,13 @@ __global__ void __launch_bounds__(1024) k_identify(const uint32_t* P, uint32_t n
 // One coalesced pass over P (2 x uint4 per thread, like k_compress): every
 // slot is compressed to its root r (H3, Def. 3.1's height-one labelling), and
 // a vertex whose bitmap bit is set (its list was not wholly sampled) and whose
-// root is not L_max has its remaining list unioned.  The skip test is the
-// dynamic one of reading R10: r was v's root at some point, so r == L_max
-// proves v connected to L_max; every edge (v, y) out of a skipped v is either
-// inside L_max's component or applied from y, which is then not skipped
-// (P:2090-2100).  Hooks of other warps run concurrently with this pass; the
-// compress store P[v] = r stays sound because r < v is a member of v's tree
-// at store time and trees only merge (no splice, reading R3), and v is not a
-// root (only non-root slots are rewritten; a non-root never becomes a root).
+// root is not L_max becomes a finish candidate (reading R10: r == L_max proves
+// v connected to L_max; every edge (v, y) out of a skipped v is either inside
+// L_max's component or applied from y, which is then not skipped,
+// P:2090-2100).  No hook runs in this kernel -- the candidates' edges are
+// unioned by k_finish_proc afterwards -- so the compress is race-free, L_max
+// (a root of the sampled forest) stays a root throughout, and a slot pointing
+// at L_max needs no gather at all (the giant's ~46 % of the vertices on C4).
 //
 // Candidates are appended (warp-aggregated) to a queue that k_finish_proc
 // degree-bins: lists (after the afforest-sampled prefix) of <= kSmallDeg
@@ -502,8 +522,8 @@ __global__ void __launch_bounds__(1024) k_identify(const uint32_t* P, uint32_t n
 // root is skipped without a link), longer lists are queued for k_finish_big
 // (one CTA per vertex).  Keeping the edge work out of the scan keeps the scan
 // a lean streaming kernel (no spills, full occupancy).
-template <bool VEC>
-__global__ void __launch_bounds__(kBlock) k_finish(uint32_t* P, const uint32_t* __restrict__ bm, uint32_t n,
+template <bool VEC, bool CNT>
+__global__ void __launch_bounds__(kBlock, CC_FINISH_MINB) k_finish(uint32_t* P, const uint32_t* __restrict__ bm, uint32_t n,
                                                    Ctl* ctl, bool no_skip, uint32_t* cq, cc_counters* cnt)
 {
     const uint32_t lmax = no_skip ? kSentinel : ctl->lmax;
@@ -525,7 +545,7 @@ __global__ void __launch_bounds__(kBlock) k_finish(uint32_t* P, const uint32_t* 
     const uint32_t w0 = i0 < n ? bm[i0 >> 5] : 0u;
     const uint32_t w1 = i1 < n ? bm[i1 >> 5] : 0u;
     uint32_t writes = 0;
-    roots8(P, vv, pp, rr);
+    const uint32_t gathers = roots8(P, vv, pp, rr, lmax);   // L_max stays a root: no hook runs here
 #pragma unroll
     for (int s = 0; s < kCV; ++s) writes += rr[s] != pp[s];
     if (full) {                                          // H3 compress writes
@@ -552,7 +572,10 @@ __global__ void __launch_bounds__(kBlock) k_finish(uint32_t* P, const uint32_t* 
         for (int s = 0; s < kCV; ++s)
             if (cm >> s & 1u) cq[pos + k2++] = vv[s];
     }
-    if (cnt) warp_count(&cnt->compress_writes, writes);
+    if (CNT) {
+        warp_count(&cnt->compress_writes, writes);
+        warp_count(&cnt->finish_gathers, gathers);
+    }
 }
 
 // k_finish_proc: the H5 edge work of the queued candidates.  A warp takes 32
@@ -586,7 +609,9 @@ __global__ void __launch_bounds__(kBlock) k_finish_proc(
         }
         const int64_t d = e - b;
         const bool isbig = d > kBigDeg;
-        const uint32_t ru = cand && !isbig && d > 0 ? find_naive(P, u) : 0u;
+        // u's parent: the root k_finish compressed u to (or a newer ancestor) --
+        // as good as a full FIND for the "v already under u's root" early exit
+        const uint32_t ru = cand && !isbig && d > 0 ? ld_relaxed(P + u) : 0u;
         if (cnt) {
             warp_count(&cnt->finish_vertices, cand ? 1u : 0u);
             warp_count(&cnt->finish_edges, cand ? (uint32_t)min(d, (int64_t)0xFFFFFFFF) : 0u);
@@ -619,9 +644,15 @@ __global__ void __launch_bounds__(kBlock) k_finish_proc(
             const uint32_t oex = __shfl_sync(0xffffffffu, excl, lo);
             if (t < tot) {
                 const uint32_t v = adj[ob + (t - oex)];
-                if (ld_relaxed(P + v) != orr) {
-                    if constexpr (SF) hooks += link<MODE>(P, ou, v, Forest{F});
-                    else hooks += link<MODE>(P, ou, v, NoForest{});
+                const uint32_t pv = ld_relaxed(P + v);
+                if (pv != orr) {                            // enter the Rem loop with both reads done
+                    if constexpr (MODE == 2) {
+                        if constexpr (SF) hooks += link_async(P, ou, v, Forest{F});
+                        else hooks += link_async(P, ou, v, NoForest{});
+                    } else {
+                        if constexpr (SF) hooks += link_rem_from<MODE == 1>(P, ou, v, orr, pv, Forest{F});
+                        else hooks += link_rem_from<MODE == 1>(P, ou, v, orr, pv, NoForest{});
+                    }
                 }
             }
             __syncwarp();
@@ -891,8 +922,9 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
         // H3 + H5
         {
             const unsigned nb = (unsigned)(((uint64_t)n + kCTile - 1) / kCTile);
-            if (aligned16(P)) k_finish<true><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters);
-            else k_finish<false><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters);
+            if (aligned16(P) && o.counters) k_finish<true, true><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters);
+            else if (aligned16(P)) k_finish<true, false><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, nullptr);
+            else k_finish<false, true><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters);
             CC_LAUNCH_CHECK("k_finish");
         }
         CC_CUDA_TRY(mark(CC_MARK_FINISH));
@@ -904,7 +936,7 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
         if (o.timings) CC_CUDA_TRY(cudaEventRecord(ev[3], s));
         // H6
         {
-            cc_status r = launch_compress(P, n, labels_out, nullptr, s, "k_compress(H6)");
+            cc_status r = launch_compress(P, n, labels_out, o.counters, s, "k_compress(H6)");
             if (r) return r;
         }
         CC_CUDA_TRY(mark(CC_MARK_COMPRESS));
