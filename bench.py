@@ -41,13 +41,14 @@ def parse():
     p.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--k", type=int, default=2)
-    p.add_argument("--variant", default="afforest", choices=["afforest", "hybrid"])
+    p.add_argument("--variant", default="afforest", choices=["afforest", "hybrid", "pure"])
     p.add_argument("--flags", type=int, default=0)
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-scale", type=int, default=CPU_SAMPLE_SCALE)
     p.add_argument("--l2-fetch", type=int, default=-1, help="cudaLimitMaxL2FetchGranularity (bytes) or -1")
+    p.add_argument("--study", action="store_true", help="NEXT-1 sampling variant x k sweep on C2-C4")
     return p.parse_args()
 
 
@@ -273,7 +274,7 @@ def run_ours(a, rank, ws):
     gen_s = time.time() - tg
     n, m = d_off.numel() - 1, d_adj.numel()
     labels = torch.empty(n, dtype=torch.int32, device=dev)
-    variant = cc.VARIANT_AFFOREST if a.variant == "afforest" else cc.VARIANT_HYBRID
+    variant = {"afforest": cc.VARIANT_AFFOREST, "hybrid": cc.VARIANT_HYBRID, "pure": cc.VARIANT_PURE}[a.variant]
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(2 * l2 // 4 + 1024, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
@@ -488,10 +489,70 @@ def run_ours_incr(a, rank, ws, cfg):
         print(json.dumps(line), flush=True)
 
 
+def run_study(a):
+    """NEXT-1: k-out variant x k sweep on C2-C4 -- per-phase device
+    times, sampling coverage (share of vertices in L_max's sampled component),
+    inter-component edges left by the sample (IC),
+    edges the finish traversed, and whether labels stayed bit-identical."""
+    import numpy as np
+    import torch
+
+    import inputs
+    from inputs import gpu as ggen
+    from paper_2008_03909_b200 import cc
+    grid = [("afforest", k) for k in (0, 1, 2, 3, 4)] + [("hybrid", 2), ("hybrid", 3), ("pure", 2), ("pure", 3)]
+    stream = torch.cuda.current_stream()
+    rows = []
+    for cfg in (inputs.C2, inputs.C3, inputs.C4):
+        d_off, d_adj = ggen.config_graph(cfg)
+        n, m = d_off.numel() - 1, d_adj.numel()
+        deg = torch.diff(d_off)
+        src = torch.repeat_interleave(torch.arange(n, device="cuda", dtype=torch.int32), deg) if m < 2**31 else None
+        ref = None
+        for variant, k in grid:
+            var = {"afforest": cc.VARIANT_AFFOREST, "hybrid": cc.VARIANT_HYBRID, "pure": cc.VARIANT_PURE}[variant]
+            labels = torch.empty(n, dtype=torch.int32, device="cuda")
+            sampled = torch.empty(n, dtype=torch.int32, device="cuda")
+            lmax = torch.empty(1, dtype=torch.int32, device="cuda")
+            ctr = torch.zeros(len(cc.COUNTER_FIELDS), dtype=torch.int64, device="cuda")
+            cc.cc_labels(d_off, d_adj, n, m, labels, cc.make_opts(k=k, variant=var, seed=cfg.seed, counters=ctr,
+                                                                  sampled_out=sampled, lmax_out=lmax), stream)
+            ms = []
+            for _ in range(a.warmup + a.steps):
+                marks = [torch.cuda.Event(enable_timing=True) for _ in range(cc.NUM_MARKS)]
+                for e in marks:
+                    e.record(stream)
+                torch.cuda.synchronize()
+                cc.cc_labels(d_off, d_adj, n, m, labels, cc.make_opts(k=k, variant=var, seed=cfg.seed,
+                                                                      marks=[e.cuda_event for e in marks]), stream)
+                torch.cuda.synchronize()
+                ms.append([marks[j - 1].elapsed_time(marks[j]) for j in range(1, cc.NUM_MARKS)])
+            ms = np.array(ms[a.warmup:]).mean(0)
+            c = dict(zip(cc.COUNTER_FIELDS, ctr.cpu().tolist()))
+            lm = int(lmax.item())
+            coverage = float((sampled == lm).float().mean().item())
+            ic = int((sampled[src.long()] != sampled[d_adj.long()]).sum().item()) // 2 if src is not None else None
+            lab = labels.cpu()
+            if ref is None:
+                ref = lab
+            rows.append({"workload": cfg.name, "variant": variant, "k": k,
+                         "ms_total": round(float(ms.sum()), 4),
+                         "ms": {cc.MARK_NAMES[j]: round(float(ms[j - 1]), 4) for j in range(1, cc.NUM_MARKS)},
+                         "coverage": round(coverage, 4), "ic_edges_after_sampling": ic,
+                         "pending_links": c["pending_links"], "finish_vertices": c["finish_vertices"],
+                         "finish_edges": c["finish_edges"], "labels_identical": bool(torch.equal(lab, ref))})
+            print(json.dumps(rows[-1]), file=sys.stderr, flush=True)
+        del d_off, d_adj, deg, src
+        torch.cuda.empty_cache()
+    print(json.dumps({"study": "NEXT-1 k-out variant x k sweep", "rows": rows}), flush=True)
+
+
 def main():
     a = parse()
     rank, ws = dist_setup()
-    if a.impl == "reference":
+    if a.study:
+        run_study(a)
+    elif a.impl == "reference":
         run_reference(a, rank, ws)
     else:
         run_ours(a, rank, ws)

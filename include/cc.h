@@ -66,11 +66,13 @@ typedef int cc_status;
 /* k-out edge choice (Alg. 4; variants P:3589-3599).
  * AFFOREST: adjacency positions 0..k-1 ("first k neighbours", the north_star).
  * HYBRID:   position 0 plus k-1 positions uniform with replacement (the
- *           paper's default); draw j of vertex u is
- *           ((lo32(mix(seed,16,u*64+j)) * deg(u)) >> 32) with
- *           mix(s,t,i) = splitmix64(s*0x9E3779B97F4A7C15 + t*2^40 + i).      */
+ *           paper's default);
+ * PURE:     k positions uniform with replacement (Holm et al.).
+ * Random draw j of vertex u is position ((lo32(mix(seed,16,u*64+j)) * deg(u)) >> 32)
+ * with mix(s,t,i) = splitmix64(s*0x9E3779B97F4A7C15 + t*2^40 + i).          */
 #define CC_VARIANT_AFFOREST 0u
 #define CC_VARIANT_HYBRID   1u
+#define CC_VARIANT_PURE     2u
 
 #define CC_FLAG_NO_SKIP     (1u << 0)  /* finish every vertex (no L_max skip)          */
 #define CC_FLAG_VALIDATE    (1u << 1)  /* check the CSR first (synchronises)                     */

@@ -179,6 +179,7 @@ def kout_sample_edges(off, adj, k: int, variant: str = "afforest", seed: int = 0
     afforest: adjacency positions 0..min(k,deg)-1 ("first k").
     hybrid:   position 0, then k-1 positions drawn uniformly with replacement
               (P:616-619), i = uniform_below(mix(seed, KOUT, u*64+j), deg).
+    pure:     k positions drawn that way, j = 0..k-1 (Holm et al.).
     Returns an (E, 2) uint32 array of (u, v) pairs."""
     off = np.asarray(off, dtype=np.int64)
     adj = np.asarray(adj, dtype=np.uint32)
@@ -190,9 +191,9 @@ def kout_sample_edges(off, adj, k: int, variant: str = "afforest", seed: int = 0
         u = np.nonzero(has)[0].astype(np.uint64)
         if u.size == 0:
             continue
-        if variant == "afforest" or j == 0:
+        if variant == "afforest" or (variant == "hybrid" and j == 0):
             pos = off[u.astype(np.int64)] + j
-        elif variant == "hybrid":
+        elif variant in ("hybrid", "pure"):
             r = mix(seed, KOUT_STREAM, u * np.uint64(64) + np.uint64(j))
             pos = off[u.astype(np.int64)] + uniform_below(r, deg[u.astype(np.int64)].astype(np.uint64)).astype(np.int64)
         else:

@@ -15,7 +15,7 @@ from __future__ import annotations
 from . import cc
 from .cc import CCError  # noqa: F401
 
-_VARIANTS = {"afforest": cc.VARIANT_AFFOREST, "hybrid": cc.VARIANT_HYBRID}
+_VARIANTS = {"afforest": cc.VARIANT_AFFOREST, "hybrid": cc.VARIANT_HYBRID, "pure": cc.VARIANT_PURE}
 
 
 def _opts(k, variant, seed, flags, **kw):

@@ -20,7 +20,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CC_LIBCC_PATH") or os.path.join(_HERE, "libcc.so")
 
 CC_OK, CC_EINVAL, CC_ERANGE, CC_ENOMEM, CC_ECUDA = 0, -1, -2, -3, -4
-VARIANT_AFFOREST, VARIANT_HYBRID = 0, 1
+VARIANT_AFFOREST, VARIANT_HYBRID, VARIANT_PURE = 0, 1, 2
 FLAG_NO_SKIP = 1 << 0
 FLAG_VALIDATE = 1 << 1
 FLAG_UF_ASYNC = 1 << 2

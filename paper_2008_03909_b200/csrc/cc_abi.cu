@@ -131,7 +131,7 @@ static cc_status check_graph_args(const int64_t* off, const uint32_t* adj, uint3
     if (n > 0xFFFFFFFEu) { set_error("n > 0xFFFFFFFE"); return CC_ERANGE; }
     if (m < 0) { set_error("m < 0"); return CC_EINVAL; }
     if (o.kout_k > 64) { set_error("kout_k > 64"); return CC_ERANGE; }
-    if (o.kout_variant > CC_VARIANT_HYBRID) { set_error("unknown kout_variant"); return CC_EINVAL; }
+    if (o.kout_variant > CC_VARIANT_PURE) { set_error("unknown kout_variant"); return CC_EINVAL; }
     if (o.samples > 2048) { set_error("samples > 2048"); return CC_ERANGE; }
     if (n > 0 && !off) { set_error("offsets is NULL"); return CC_EINVAL; }
     if (m > 0 && !adj) { set_error("adj is NULL"); return CC_EINVAL; }

@@ -90,7 +90,9 @@ __device__ __forceinline__ uint32_t pick4(uint4 w, uint32_t r)
     return r == 0 ? w.x : r == 1 ? w.y : r == 2 ? w.z : w.w;
 }
 
-template <bool HYBRID, bool SF, bool WIN>
+// VAR: 0 = afforest (positions 0..k-1), 1 = hybrid (0, then k-1 uniform picks),
+// 2 = pure (k uniform picks) -- cc.h CC_VARIANT_*.
+template <int VAR, bool SF, bool WIN>
 __global__ void __launch_bounds__(kBlock, 3) k_sample_init(
     const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, uint32_t n, int64_t m, uint32_t k,
     uint64_t seed, uint32_t full_deg, uint32_t* __restrict__ P, uint2* __restrict__ F,
@@ -122,20 +124,21 @@ __global__ void __launch_bounds__(kBlock, 3) k_sample_init(
 #pragma unroll
     for (int j = 0; j < kV; ++j) {
         const uint64_t u = wbase + 32 * j + lane;
-        uint32_t i1 = 1;
-        if (HYBRID && d[j] > 0) i1 = uniform_below(mix(seed, KOUT_STREAM, u * 64 + 1), d[j]);
+        uint32_t i0 = 0, i1 = 1;
+        if (VAR == 2 && d[j] > 0) i0 = uniform_below(mix(seed, KOUT_STREAM, u * 64 + 0), d[j]);
+        if (VAR >= 1 && d[j] > 0) i1 = uniform_below(mix(seed, KOUT_STREAM, u * 64 + 1), d[j]);
         const bool need0 = d[j] > 0 && k > 0;
-        const bool need1 = k > 1 && (HYBRID ? d[j] > 0 : d[j] > 1);
+        const bool need1 = k > 1 && (VAR >= 1 ? d[j] > 0 : d[j] > 1);
         v0[j] = v1[j] = kSentinel;
         const int64_t b4 = o[j] & ~(int64_t)3;
         const uint32_t r = (uint32_t)(o[j] & 3);
-        if (WIN && need0 && b4 + 4 <= m) {
+        if (WIN && VAR != 2 && need0 && b4 + 4 <= m) {
             const uint4 wv = __ldg(reinterpret_cast<const uint4*>(adj + b4));
             v0[j] = pick4<WIN>(wv, r);
             if (need1 && r + i1 < 4) v1[j] = pick4<WIN>(wv, r + i1);
             else if (need1) v1[j] = __ldg(adj + o[j] + i1);
         } else {
-            if (need0) v0[j] = __ldg(adj + o[j]);
+            if (need0) v0[j] = __ldg(adj + o[j] + i0);
             if (need1) v1[j] = __ldg(adj + o[j] + i1);
         }
     }
@@ -146,7 +149,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_sample_init(
         const uint64_t u = wbase + 32 * j + lane;
         uint32_t np = 0;
         if (v0[j] != kSentinel)
-            np = (v0[j] > (uint32_t)u ? 1u : 0u) + (HYBRID ? k : min(k, d[j])) - 1u;
+            np = (v0[j] > (uint32_t)u ? 1u : 0u) + (VAR >= 1 ? k : min(k, d[j])) - 1u;
         c[j] = np;
         const bool mark = u < n && d[j] > full_deg;
         nwl += mark;
@@ -202,10 +205,10 @@ __global__ void __launch_bounds__(kBlock, 3) k_sample_init(
         if (np) {
             unsigned long long pos = pbase + ex[j];
             if (v0[j] > (uint32_t)u) pend[pos++] = make_uint2((uint32_t)u, v0[j]);
-            const uint32_t kk = HYBRID ? k : min(k, d[j]);
+            const uint32_t kk = VAR >= 1 ? k : min(k, d[j]);
             if (kk > 1) pend[pos++] = make_uint2((uint32_t)u, v1[j]);
             for (uint32_t jj = 2; jj < kk; ++jj) {        // k > 2: the rest, loaded here
-                const uint32_t i = HYBRID ? uniform_below(mix(seed, KOUT_STREAM, u * 64 + jj), d[j]) : jj;
+                const uint32_t i = VAR >= 1 ? uniform_below(mix(seed, KOUT_STREAM, u * 64 + jj), d[j]) : jj;
                 pend[pos++] = make_uint2((uint32_t)u, __ldg(adj + o[j] + i));
             }
         }
@@ -813,23 +816,23 @@ cc_status validate_csr(const int64_t* off, const uint32_t* adj, uint32_t n, int6
 }
 
 // ---------------------------------------------------------------------------
-template <int MODE, bool SF, bool HYBRID>
+template <int MODE, bool SF, int VAR>
 static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_t m, uint32_t* P,
                      uint32_t* edges, int64_t* num_edges, uint32_t* labels_out, const cc_opts& o,
                      cudaStream_t s)
 {
     const uint32_t k = o.kout_k;
-    const bool afforest = !HYBRID;
     const bool degskip = !(o.flags & CC_FLAG_NO_DEGSKIP);
-    // a list of length <= full_deg was wholly unioned by the sampling
-    const uint32_t full_deg = !degskip ? 0u : (afforest ? k : std::min<uint32_t>(k, 1u));
-    const uint32_t skip_prefix = afforest ? k : std::min<uint32_t>(k, 1u);
+    // the list prefix known to be unioned by the sampling: afforest its first k
+    // entries, hybrid its first, pure none; a list no longer than it needs no finish
+    const uint32_t skip_prefix = VAR == 0 ? k : VAR == 1 ? std::min<uint32_t>(k, 1u) : 0u;
+    const uint32_t full_deg = degskip ? skip_prefix : 0u;
     const bool no_skip = (o.flags & CC_FLAG_NO_SKIP) != 0;
     const int sms = num_sms();
 
-    // afforest: at most sum_u min(k, deg u) <= m pending edges; hybrid: k per non-isolated vertex
+    // afforest: at most sum_u min(k, deg u) <= m pending edges; hybrid/pure: k per non-isolated vertex
     const uint64_t pend_cap = std::max<uint64_t>(
-        1, HYBRID ? (uint64_t)k * std::min<uint64_t>(n, (uint64_t)m) : std::min<uint64_t>((uint64_t)n * k, (uint64_t)m));
+        1, VAR >= 1 ? (uint64_t)k * std::min<uint64_t>(n, (uint64_t)m) : std::min<uint64_t>((uint64_t)n * k, (uint64_t)m));
     const uint64_t big_cap = std::max<uint64_t>(1, std::min<uint64_t>(n, (uint64_t)m / kBigDeg + 1));
     const uint64_t bm_words = ((uint64_t)n + 31) / 32;
     const uint32_t nfb = (uint32_t)(((uint64_t)n + kFTile - 1) / kFTile);
@@ -880,10 +883,10 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
         // 16-byte list-head windows pay off when adj is read over PCIe (pinned host,
         // zero-copy); from HBM two 4-byte loads of the same sector are cheaper
         if (aligned16(adj) && mem_kind(adj, nullptr) == MEM_PINNED)
-            k_sample_init<HYBRID, SF, true><<<nblk0, kBlock, 0, s>>>(off, adj, n, m, k, o.seed, full_deg, P, F, pend,
+            k_sample_init<VAR, SF, true><<<nblk0, kBlock, 0, s>>>(off, adj, n, m, k, o.seed, full_deg, P, F, pend,
                                                                     bm, ctl, o.counters);
         else
-            k_sample_init<HYBRID, SF, false><<<nblk0, kBlock, 0, s>>>(off, adj, n, m, k, o.seed, full_deg, P, F, pend,
+            k_sample_init<VAR, SF, false><<<nblk0, kBlock, 0, s>>>(off, adj, n, m, k, o.seed, full_deg, P, F, pend,
                                                                      bm, ctl, o.counters);
         CC_LAUNCH_CHECK("k_sample_init");
         CC_CUDA_TRY(mark(CC_MARK_INIT));
@@ -970,14 +973,26 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
     return rc;
 }
 
-template <bool SF, bool HYBRID>
+template <bool SF, int VAR>
 static cc_status dispatch_mode(const int64_t* off, const uint32_t* adj, uint32_t n, int64_t m, uint32_t* P,
                                uint32_t* edges, int64_t* num_edges, uint32_t* labels_out, const cc_opts& o,
                                cudaStream_t s)
 {
-    if (o.flags & CC_FLAG_UF_ASYNC) return run<2, SF, HYBRID>(off, adj, n, m, P, edges, num_edges, labels_out, o, s);
-    if (o.flags & CC_FLAG_HALVE) return run<1, SF, HYBRID>(off, adj, n, m, P, edges, num_edges, labels_out, o, s);
-    return run<0, SF, HYBRID>(off, adj, n, m, P, edges, num_edges, labels_out, o, s);
+    if (o.flags & CC_FLAG_UF_ASYNC) return run<2, SF, VAR>(off, adj, n, m, P, edges, num_edges, labels_out, o, s);
+    if (o.flags & CC_FLAG_HALVE) return run<1, SF, VAR>(off, adj, n, m, P, edges, num_edges, labels_out, o, s);
+    return run<0, SF, VAR>(off, adj, n, m, P, edges, num_edges, labels_out, o, s);
+}
+
+template <bool SF>
+static cc_status dispatch_variant(const int64_t* off, const uint32_t* adj, uint32_t n, int64_t m, uint32_t* P,
+                                  uint32_t* edges, int64_t* num_edges, uint32_t* labels_out, const cc_opts& o,
+                                  cudaStream_t s)
+{
+    if (o.kout_variant == CC_VARIANT_HYBRID)
+        return dispatch_mode<SF, 1>(off, adj, n, m, P, edges, num_edges, labels_out, o, s);
+    if (o.kout_variant == CC_VARIANT_PURE)
+        return dispatch_mode<SF, 2>(off, adj, n, m, P, edges, num_edges, labels_out, o, s);
+    return dispatch_mode<SF, 0>(off, adj, n, m, P, edges, num_edges, labels_out, o, s);
 }
 
 cc_status static_pipeline(const int64_t* off, const uint32_t* adj, uint32_t n, int64_t m, uint32_t* P,
@@ -993,15 +1008,8 @@ cc_status static_pipeline(const int64_t* off, const uint32_t* adj, uint32_t n, i
         P = scratch;
     }
     uint32_t* out = labels_out == P ? nullptr : labels_out;
-    const bool hybrid = o.kout_variant == CC_VARIANT_HYBRID;
-    cc_status rc;
-    if (sf) {
-        rc = hybrid ? dispatch_mode<true, true>(off, adj, n, m, P, edges, num_edges, out, o, s)
-                    : dispatch_mode<true, false>(off, adj, n, m, P, edges, num_edges, out, o, s);
-    } else {
-        rc = hybrid ? dispatch_mode<false, true>(off, adj, n, m, P, edges, num_edges, out, o, s)
-                    : dispatch_mode<false, false>(off, adj, n, m, P, edges, num_edges, out, o, s);
-    }
+    const cc_status rc = sf ? dispatch_variant<true>(off, adj, n, m, P, edges, num_edges, out, o, s)
+                            : dispatch_variant<false>(off, adj, n, m, P, edges, num_edges, out, o, s);
     scratch_free(scratch, s);
     return rc;
 }

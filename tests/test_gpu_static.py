@@ -36,6 +36,8 @@ OPTION_GRID = [
     dict(k=64, variant="afforest", flags=0),
     dict(k=2, variant="afforest", flags=cc.FLAG_MIDCOMPRESS),
     dict(k=3, variant="hybrid", flags=cc.FLAG_MIDCOMPRESS | cc.FLAG_HALVE, seed=5),
+    dict(k=2, variant="pure", flags=0, seed=13),
+    dict(k=1, variant="pure", flags=cc.FLAG_UF_ASYNC, seed=2),
 ]
 
 
@@ -89,7 +91,7 @@ def test_sampled_labels_are_cc_of_the_sampled_edges():
     for off, adj in graphs:
         n = off.size - 1
         for k, variant, seed in [(1, "afforest", 0), (2, "afforest", 0), (3, "afforest", 0), (2, "hybrid", 5),
-                                 (4, "hybrid", 99)]:
+                                 (4, "hybrid", 99), (1, "pure", 4), (3, "pure", 8)]:
             d_off, d_adj = to_dev(off, adj)
             sampled = torch.empty(n, dtype=torch.int32, device="cuda")
             lmax = torch.empty(1, dtype=torch.int32, device="cuda")
@@ -226,7 +228,7 @@ def test_repeat_stress_random_options():
                   cc.FLAG_MIDCOMPRESS]
     for it in range(200):
         k = int(rng.integers(0, 5))
-        variant = ["afforest", "hybrid"][int(rng.integers(0, 2))]
+        variant = ["afforest", "hybrid", "pure"][int(rng.integers(0, 3))]
         fl = int(rng.choice(flags_pool)) | int(rng.choice(flags_pool))
         lab = pkg.connected_components(d_off, d_adj, k=k, variant=variant, seed=int(rng.integers(0, 1 << 30)),
                                        flags=fl)

@@ -294,6 +294,19 @@ def test_kout_sample_edges_closed_forms():
     assert E.shape[0] == 2 * int((deg > 0).sum())
     for u, v in E[:2000]:
         assert v in set(adj[off[u]:off[u + 1]].tolist())
+    # hybrid's first pick is the first neighbour; pure draws every pick
+    first = set(zip(np.nonzero(deg > 0)[0].tolist(), adj[off[:-1][deg > 0]].tolist()))
+    assert first <= set(map(tuple, E.tolist()))
+    Ep = oracle.kout_sample_edges(off, adj, 3, "pure", seed=5)
+    assert Ep.shape[0] == 3 * int((deg > 0).sum())
+    for u, v in Ep[::97]:
+        assert v in set(adj[off[u]:off[u + 1]].tolist())
+    # a vertex of degree 1 samples its only edge under every variant
+    d1 = np.nonzero(deg == 1)[0][:50]
+    for var in ("afforest", "hybrid", "pure"):
+        Ev = oracle.kout_sample_edges(off, adj, 2, var, seed=1)
+        got = set(map(tuple, Ev.tolist()))
+        assert all((int(u), int(adj[off[u]])) in got for u in d1)
 
 
 def test_identify_frequent_and_canon():
