@@ -49,6 +49,7 @@ def parse():
     p.add_argument("--cpu-scale", type=int, default=CPU_SAMPLE_SCALE)
     p.add_argument("--l2-fetch", type=int, default=-1, help="cudaLimitMaxL2FetchGranularity (bytes) or -1")
     p.add_argument("--study", action="store_true", help="NEXT-1 sampling variant x k sweep on C2-C4")
+    p.add_argument("--incr-sweep", action="store_true", help="NEXT-2 incremental variants sweep")
     return p.parse_args()
 
 
@@ -174,9 +175,13 @@ def run_reference(a, rank, ws):
     use_gpu = torch.cuda.is_available()
     import inputs
     cfg = inputs.BY_INDEX[a.config]
-    times, m = [], 0
+    import oracle
+    m, dt0, off_s, adj_s, _ = cpu_oracle_sample(a.cpu_scale, use_gpu)     # sample generated once
+    times = []
     for i in range(a.warmup + a.steps):
-        m, dt, *_ = cpu_oracle_sample(a.cpu_scale, use_gpu)
+        t0 = time.perf_counter()
+        oracle.cc_bfs(off_s, adj_s)
+        dt = time.perf_counter() - t0
         if i >= a.warmup:
             times.append(dt)
     t = sum(times) / len(times)
@@ -547,11 +552,102 @@ def run_study(a):
     print(json.dumps({"study": "NEXT-1 k-out variant x k sweep", "rows": rows}), flush=True)
 
 
+def run_incr_sweep(a):
+    """NEXT-2: incremental variants.
+    A: throughput vs batch size, inserts only, empty start on 2^20 vertices (the
+       shape of the paper's Table 5), RMAT-20 stream.
+    B: the C5 shape (2^26 vertices, 256 batches of 2^20 ops): phase-concurrent
+       (type 3) vs wait-free (type 1); batch order as drawn vs sorted
+       by source; query share 10/50/90 % with naive vs splitting
+       finds (P:3315-3366)."""
+    import torch
+
+    from inputs import gpu as ggen
+    from paper_2008_03909_b200 import cc
+    stream = torch.cuda.current_stream()
+
+    def time_stream(n, ins_b, qs_b, flags):
+        ans = [torch.empty(q.shape[0], dtype=torch.uint8, device="cuda") for q in qs_b]
+        best = None
+        for rep in range(2):
+            h = cc.Incr(n, flags=flags)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for b in range(len(ins_b)):
+                h.batch(ins_b[b], ins_b[b].shape[0], qs_b[b], qs_b[b].shape[0], ans[b])
+            e1.record(stream)
+            e1.synchronize()
+            h.close()
+            t = e0.elapsed_time(e1)
+            best = t if best is None else min(best, t)
+        return best
+
+    out = {"A_batch_size": [], "B_c5_variants": []}
+    # ---- A
+    n = 1 << 20
+    total = 1 << 22
+    all_ins, _ = ggen.incr_batch(7, 20, 0, total, 1)
+    empty_q = torch.empty((0, 2), dtype=torch.int32, device="cuda")
+    import numpy as np
+    no_ans = torch.empty(1, dtype=torch.uint8, device="cuda")
+    for bs in (10, 100, 1000, 10_000, 100_000, 1_000_000, 2_000_000):
+        nb = min(total // bs, 2000)
+        ins_b = [all_ins[i * bs:(i + 1) * bs] for i in range(nb)]
+        t = time_stream(n, ins_b, [empty_q] * nb, 0)
+        # the same batches through one cc_incr_batches call (one launch for small batches)
+        best = None
+        for rep in range(2):
+            h = cc.Incr(n)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            h.batches(np.full(nb, bs), all_ins[:nb * bs], np.zeros(nb), empty_q, no_ans)
+            e1.record(stream)
+            e1.synchronize()
+            h.close()
+            tb = e0.elapsed_time(e1)
+            best = tb if best is None else min(best, tb)
+        out["A_batch_size"].append({"batch": bs, "batches": nb, "ms_per_call_api": round(t, 3),
+                                    "inserts_per_s": round(nb * bs / (t * 1e-3), 1),
+                                    "ms_multi_batch_api": round(best, 3),
+                                    "inserts_per_s_multi_batch_api": round(nb * bs / (best * 1e-3), 1)})
+        print(json.dumps(out["A_batch_size"][-1]), file=sys.stderr, flush=True)
+    # ---- B
+    n = 1 << 26
+    nb, per = 256, 1 << 20
+    for qfrac in (0.1, 0.5, 0.9):
+        n_q = int(per * qfrac) if qfrac != 0.1 else 104_858
+        n_ins = per - n_q
+        ins_b, qs_b = [], []
+        for b in range(nb):
+            i, q = ggen.incr_batch(5, 26, b, n_ins, n_q)
+            ins_b.append(i)
+            qs_b.append(q)
+        variants = [("phase_concurrent", 0, False), ("phase_concurrent_find_split", cc.FLAG_FIND_SPLIT, False),
+                    ("wait_free", cc.FLAG_WAIT_FREE, False)]
+        if qfrac == 0.1:
+            variants.append(("phase_concurrent_sorted_batches", 0, True))
+        for name, flags, sort in variants:
+            ib = ins_b
+            if sort:
+                ib = [x[torch.argsort(x[:, 0].long() * (1 << 32) + x[:, 1].long())].contiguous() for x in ins_b]
+            t = time_stream(n, ib, qs_b, flags)
+            out["B_c5_variants"].append({"query_share": qfrac, "variant": name, "ms": round(t, 3),
+                                         "ops_per_s": round(nb * per / (t * 1e-3), 1),
+                                         "inserts_per_s": round(nb * n_ins / (t * 1e-3), 1)})
+            print(json.dumps(out["B_c5_variants"][-1]), file=sys.stderr, flush=True)
+        del ins_b, qs_b
+    print(json.dumps({"study": "NEXT-2 incremental variants", **out}), flush=True)
+
+
 def main():
     a = parse()
     rank, ws = dist_setup()
     if a.study:
         run_study(a)
+    elif a.incr_sweep:
+        run_incr_sweep(a)
     elif a.impl == "reference":
         run_reference(a, rank, ws)
     else:

@@ -83,6 +83,12 @@ typedef int cc_status;
 #define CC_FLAG_NO_MIDCOMPRESS (1u << 6) /* never run the compress between k-out rounds        */
 #define CC_FLAG_MIDCOMPRESS (1u << 7)  /* always run it (default: a 1024-sample probe of the
                                           round-0 chain depth decides, on the device)        */
+#define CC_FLAG_WAIT_FREE   (1u << 8)  /* cc_incr: the wait-free type (1) setting (P:973-977,
+                                          P:2663-2682): a batch's inserts and queries run
+                                          concurrently in ONE kernel.  Answers are then
+                                          linearizable, not bit-exact: 1 implies connected
+                                          after this batch's inserts, 0 implies not
+                                          connected before them               */
 
 /* Per-phase device times, filled when cc_opts.timings != NULL (the call then
  * synchronises `stream` before returning).  Bench/diagnostics only.          */
@@ -174,7 +180,7 @@ typedef struct cc_incr cc_incr;
 
 /* Create a handle over n vertices with no edges (P[v] = v).  opts may be NULL;
  * only opts->flags (CC_FLAG_HALVE, CC_FLAG_UF_ASYNC, CC_FLAG_FIND_SPLIT,
- * CC_FLAG_VALIDATE) is used.  *out receives the handle (host pointer). */
+ * CC_FLAG_VALIDATE, CC_FLAG_WAIT_FREE) is used.  *out receives the handle (host pointer). */
 cc_status cc_incr_create(uint32_t n, const cc_opts* opts, void* stream, cc_incr** out);
 
 /* inserts: 2*n_ins uint32, (u, v) interleaved; queries: 2*n_q uint32;
@@ -184,6 +190,18 @@ cc_status cc_incr_create(uint32_t n, const cc_opts* opts, void* stream, cc_incr*
  * out-of-range ids return CC_EINVAL before any insert is applied. */
 cc_status cc_incr_batch(cc_incr* h, const uint32_t* inserts, int64_t n_ins,
                         const uint32_t* queries, int64_t n_q, uint8_t* answers, void* stream);
+
+/* Process nb batches in order in ONE call -- exactly what nb cc_incr_batch calls
+ * would compute (batch b's queries see the inserts of batches 0..b).  The
+ * batches' pairs are concatenated in `inserts` / `queries` and their answers in
+ * `answers`; ins_counts / q_counts are HOST int64 arrays of nb counts.  When
+ * every batch has at most 8192 operations the whole sequence runs in one
+ * single-CTA kernel with a block barrier between each insert and query phase
+ * (the paper's small-batch regime, Table 5); otherwise one launch
+ * pair per batch.  Arrays may be device or pinned host memory.  Errors as
+ * cc_incr_batch (with CC_FLAG_VALIDATE, all ids are checked first). */
+cc_status cc_incr_batches(cc_incr* h, int64_t nb, const int64_t* ins_counts, const uint32_t* inserts,
+                          const int64_t* q_counts, const uint32_t* queries, uint8_t* answers, void* stream);
 
 /* labels (out, n): canonical labels (min id per component) of the current state. */
 cc_status cc_incr_labels(cc_incr* h, uint32_t* labels, void* stream);

@@ -29,11 +29,12 @@ FLAG_FIND_SPLIT = 1 << 4
 FLAG_NO_DEGSKIP = 1 << 5
 FLAG_NO_MIDCOMPRESS = 1 << 6
 FLAG_MIDCOMPRESS = 1 << 7
+FLAG_WAIT_FREE = 1 << 8
 
 # every symbol include/cc.h and include/cc_bench.h declare
 EXPORTS = [
     "cc_opts_default", "cc_labels", "cc_spanning_forest", "cc_incr_create", "cc_incr_batch",
-    "cc_incr_labels", "cc_incr_destroy", "cc_incr_num_vertices", "cc_status_str", "cc_last_error",
+    "cc_incr_batches", "cc_incr_labels", "cc_incr_destroy", "cc_incr_num_vertices", "cc_status_str", "cc_last_error",
     "cc_workspace_bytes", "cc_version",
     "cc_bench_map_edges", "cc_bench_gather_edges", "cc_bench_random_gather", "cc_bench_copy",
     "cc_bench_launch_count", "cc_bench_set_l2_fetch",
@@ -89,6 +90,7 @@ def load() -> ctypes.CDLL:
         "cc_spanning_forest": (ctypes.c_int, [P, P, U32, I64, P, P, P, OP, P]),
         "cc_incr_create": (ctypes.c_int, [U32, OP, P, ctypes.POINTER(ctypes.c_void_p)]),
         "cc_incr_batch": (ctypes.c_int, [P, P, I64, P, I64, P, P]),
+        "cc_incr_batches": (ctypes.c_int, [P, I64, P, P, P, P, P, P]),
         "cc_incr_labels": (ctypes.c_int, [P, P, P]),
         "cc_incr_destroy": (None, [P]),
         "cc_incr_num_vertices": (U32, [P]),
@@ -177,6 +179,14 @@ class Incr:
     def batch(self, inserts, n_ins, queries, n_q, answers, stream=None):
         _check(self._lib.cc_incr_batch(self.h, _ptr(inserts), n_ins, _ptr(queries), n_q, _ptr(answers),
                                        _stream(stream)), "cc_incr_batch")
+
+    def batches(self, ins_counts, inserts, q_counts, queries, answers, stream=None):
+        """nb batches in one call; counts are int64 numpy arrays (host)."""
+        import numpy as np
+        ic = np.ascontiguousarray(ins_counts, dtype=np.int64)
+        qc = np.ascontiguousarray(q_counts, dtype=np.int64)
+        _check(self._lib.cc_incr_batches(self.h, ic.size, ic.ctypes.data, _ptr(inserts), qc.ctypes.data,
+                                         _ptr(queries), _ptr(answers), _stream(stream)), "cc_incr_batches")
 
     def labels(self, out, stream=None):
         _check(self._lib.cc_incr_labels(self.h, _ptr(out), _stream(stream)), "cc_incr_labels")

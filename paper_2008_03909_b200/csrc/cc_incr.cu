@@ -63,6 +63,91 @@ __global__ void __launch_bounds__(kBlock) k_query(uint32_t* P, const uint2* __re
     ans[i] = ra == rb ? 1 : 0;
 }
 
+// Wait-free type (1) batch (Theorem P:2663-2682): inserts and
+// queries of the batch in ONE kernel, interleaved over the threads so that
+// they really overlap.  A query is linearizable against the concurrent
+// unions: it finds ra, then rb; if they differ and ra is STILL a root after
+// rb was found, a and b were in different trees at the moment rb was read
+// (ra was a root throughout), so "0" is correct at that point; otherwise it
+// retries.  All parent reads are device-scope relaxed loads (reading R5).
+template <int MODE>
+__global__ void __launch_bounds__(kBlock) k_mixed(uint32_t* P, const uint2* __restrict__ ins, int64_t n_ins,
+                                                  const uint2* __restrict__ q, int64_t n_q, uint8_t* __restrict__ ans)
+{
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t both = 2 * min(n_ins, n_q);
+    bool is_ins;
+    int64_t i;
+    if (t < both) {                      // alternate insert / query while both remain
+        is_ins = (t & 1) == 0;
+        i = t >> 1;
+    } else {
+        i = both / 2 + (t - both);
+        is_ins = n_ins > n_q;
+        if (i >= (is_ins ? n_ins : n_q)) return;
+    }
+    if (is_ins) {
+        const uint2 e = ins[i];
+        link<MODE>(P, e.x, e.y, NoForest{});
+        return;
+    }
+    const uint2 e = q[i];
+    while (true) {
+        const uint32_t ra = find_naive(P, e.x);
+        const uint32_t rb = find_naive(P, e.y);
+        if (ra == rb) { ans[i] = 1; return; }
+        if (ld_relaxed(P + ra) == ra) { ans[i] = 0; return; }
+    }
+}
+
+// Small batches (the latency regime of the paper's Table 5, batch 10..1000):
+// ONE CTA applies all inserts, passes a block barrier -- the type (3)
+// insert/query barrier, P:986-993 -- and answers all queries: one launch
+// instead of two.  The hooks are device-scope CAS and the query reads are
+// relaxed device-scope loads, so the barrier also orders their visibility.
+constexpr int64_t kSmallBatch = 8192;
+
+template <int MODE, bool SPLIT>
+__global__ void __launch_bounds__(1024) k_small_batch(uint32_t* P, const uint2* __restrict__ ins, int64_t n_ins,
+                                                      const uint2* __restrict__ q, int64_t n_q,
+                                                      uint8_t* __restrict__ ans)
+{
+    for (int64_t i = threadIdx.x; i < n_ins; i += blockDim.x) {
+        const uint2 e = ins[i];
+        link<MODE>(P, e.x, e.y, NoForest{});
+    }
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < n_q; i += blockDim.x) {
+        const uint2 e = q[i];
+        const uint32_t ra = SPLIT ? find_split(P, e.x) : find_naive(P, e.x);
+        const uint32_t rb = SPLIT ? find_split(P, e.y) : find_naive(P, e.y);
+        ans[i] = ra == rb ? 1 : 0;
+    }
+}
+
+// The multi-batch form of k_small_batch: one CTA walks the whole batch sequence.
+template <int MODE, bool SPLIT>
+__global__ void __launch_bounds__(1024) k_small_batches(uint32_t* P, const uint2* __restrict__ ins,
+                                                        const uint2* __restrict__ q, uint8_t* __restrict__ ans,
+                                                        const int64_t* __restrict__ oi, const int64_t* __restrict__ oq,
+                                                        int64_t nb)
+{
+    for (int64_t b = 0; b < nb; ++b) {
+        for (int64_t i = oi[b] + threadIdx.x; i < oi[b + 1]; i += blockDim.x) {
+            const uint2 e = ins[i];
+            link<MODE>(P, e.x, e.y, NoForest{});
+        }
+        __syncthreads();                         // the batch's insert/query barrier
+        for (int64_t i = oq[b] + threadIdx.x; i < oq[b + 1]; i += blockDim.x) {
+            const uint2 e = q[i];
+            const uint32_t ra = SPLIT ? find_split(P, e.x) : find_naive(P, e.x);
+            const uint32_t rb = SPLIT ? find_split(P, e.y) : find_naive(P, e.y);
+            ans[i] = ra == rb ? 1 : 0;
+        }
+        __syncthreads();                         // batch b+1 starts after batch b's queries
+    }
+}
+
 __global__ void k_check_ids(const uint32_t* ids, int64_t count, uint32_t n, unsigned int* err)
 {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -111,6 +196,33 @@ static cc_status insert_query(cc_incr* h, const uint32_t* ins, int64_t n_ins, co
             set_error("cc_incr_batch: vertex id >= n");
             return CC_EINVAL;
         }
+    }
+    if (n_ins + n_q <= kSmallBatch && !(h->flags & CC_FLAG_WAIT_FREE)) {
+        const uint2* e = reinterpret_cast<const uint2*>(ins);
+        const uint2* q = reinterpret_cast<const uint2*>(qs);
+        const bool split = (h->flags & CC_FLAG_FIND_SPLIT) != 0;
+        if (h->flags & CC_FLAG_UF_ASYNC) {
+            if (split) k_small_batch<2, true><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
+            else k_small_batch<2, false><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
+        } else if (h->flags & CC_FLAG_HALVE) {
+            if (split) k_small_batch<1, true><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
+            else k_small_batch<1, false><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
+        } else {
+            if (split) k_small_batch<0, true><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
+            else k_small_batch<0, false><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
+        }
+        CC_LAUNCH_CHECK("k_small_batch");
+        return CC_OK;
+    }
+    if ((h->flags & CC_FLAG_WAIT_FREE) && n_ins > 0 && n_q > 0) {
+        const uint2* e = reinterpret_cast<const uint2*>(ins);
+        const uint2* q = reinterpret_cast<const uint2*>(qs);
+        const unsigned nb = nblocks(n_ins + n_q);
+        if (h->flags & CC_FLAG_UF_ASYNC) k_mixed<2><<<nb, kBlock, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
+        else if (h->flags & CC_FLAG_HALVE) k_mixed<1><<<nb, kBlock, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
+        else k_mixed<0><<<nb, kBlock, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
+        CC_LAUNCH_CHECK("k_mixed");
+        return CC_OK;
     }
     if (n_ins > 0) {
         const uint2* e = reinterpret_cast<const uint2*>(ins);
@@ -214,6 +326,93 @@ cc_status cc_incr_batch(cc_incr* h, const uint32_t* inserts, int64_t n_ins, cons
         if (e != cudaSuccess) rc = cuda_fail(e, "cc_incr_batch: sync");
     }
     release();
+    return rc;
+}
+
+cc_status cc_incr_batches(cc_incr* h, int64_t nb, const int64_t* ins_counts, const uint32_t* inserts,
+                          const int64_t* q_counts, const uint32_t* queries, uint8_t* answers, void* stream)
+{
+    if (!h) { set_error("handle is NULL"); return CC_EINVAL; }
+    if (nb < 0 || (nb > 0 && (!ins_counts || !q_counts))) { set_error("bad batch counts"); return CC_EINVAL; }
+    cudaStream_t s = (cudaStream_t)stream;
+    h->last = s;
+    std::vector<int64_t> oi(nb + 1, 0), oq(nb + 1, 0);
+    int64_t maxops = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        if (ins_counts[b] < 0 || q_counts[b] < 0) { set_error("negative count"); return CC_EINVAL; }
+        oi[b + 1] = oi[b] + ins_counts[b];
+        oq[b + 1] = oq[b] + q_counts[b];
+        maxops = std::max(maxops, ins_counts[b] + q_counts[b]);
+    }
+    const int64_t tot_i = oi[nb], tot_q = oq[nb];
+    if ((tot_i && !inserts) || (tot_q && (!queries || !answers))) { set_error("NULL array"); return CC_EINVAL; }
+    if (h->n == 0) {
+        if (tot_i || tot_q) { set_error("ids >= n = 0"); return CC_EINVAL; }
+        return CC_OK;
+    }
+    void *a_ins = (void*)inserts, *a_q = (void*)queries, *a_ans = (void*)answers;
+    const MemKind k_ins = tot_i ? mem_kind(inserts, &a_ins) : MEM_DEVICE;
+    const MemKind k_q = tot_q ? mem_kind(queries, &a_q) : MEM_DEVICE;
+    const MemKind k_ans = tot_q ? mem_kind(answers, &a_ans) : MEM_DEVICE;
+    if (k_ins == MEM_PAGEABLE || k_q == MEM_PAGEABLE || k_ans == MEM_PAGEABLE) {
+        // pageable host arrays: fall back to one staged cc_incr_batch per batch
+        for (int64_t b = 0; b < nb; ++b) {
+            const cc_status rc = cc_incr_batch(h, inserts + 2 * oi[b], ins_counts[b], queries + 2 * oq[b], q_counts[b],
+                                               answers + oq[b], stream);
+            if (rc) return rc;
+        }
+        return CC_OK;
+    }
+    const uint32_t* d_ins = (const uint32_t*)a_ins;
+    const uint32_t* d_q = (const uint32_t*)a_q;
+    uint8_t* d_ans = (uint8_t*)a_ans;
+    if (h->flags & CC_FLAG_VALIDATE) {
+        unsigned int* err = nullptr;
+        CC_CUDA_TRY(scratch_alloc((void**)&err, sizeof(unsigned int), s));
+        CC_CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(unsigned int), s));
+        if (tot_i) { k_check_ids<<<num_sms() * 4, kBlock, 0, s>>>(d_ins, 2 * tot_i, h->n, err); CC_LAUNCH_CHECK("k_check_ids"); }
+        if (tot_q) { k_check_ids<<<num_sms() * 4, kBlock, 0, s>>>(d_q, 2 * tot_q, h->n, err); CC_LAUNCH_CHECK("k_check_ids"); }
+        unsigned int e = 0;
+        CC_CUDA_TRY(cudaMemcpyAsync(&e, err, sizeof(e), cudaMemcpyDeviceToHost, s));
+        CC_CUDA_TRY(cudaStreamSynchronize(s));
+        scratch_free(err, s);
+        if (e) { set_error("cc_incr_batches: vertex id >= n"); return CC_EINVAL; }
+    }
+    const bool host = k_ins != MEM_DEVICE || k_q != MEM_DEVICE || k_ans != MEM_DEVICE;
+    if (maxops <= kSmallBatch && !(h->flags & CC_FLAG_WAIT_FREE)) {
+        int64_t* d_off = nullptr;
+        CC_CUDA_TRY(scratch_alloc((void**)&d_off, sizeof(int64_t) * 2 * (size_t)(nb + 1), s));
+        std::vector<int64_t> both(oi);
+        both.insert(both.end(), oq.begin(), oq.end());
+        CC_CUDA_TRY(cudaMemcpyAsync(d_off, both.data(), sizeof(int64_t) * both.size(), cudaMemcpyHostToDevice, s));
+        const uint2* e = reinterpret_cast<const uint2*>(d_ins);
+        const uint2* q = reinterpret_cast<const uint2*>(d_q);
+        const bool split = (h->flags & CC_FLAG_FIND_SPLIT) != 0;
+        const int64_t* po = d_off;
+        const int64_t* pq = d_off + nb + 1;
+        if (h->flags & CC_FLAG_UF_ASYNC) {
+            if (split) k_small_batches<2, true><<<1, 1024, 0, s>>>(h->P, e, q, d_ans, po, pq, nb);
+            else k_small_batches<2, false><<<1, 1024, 0, s>>>(h->P, e, q, d_ans, po, pq, nb);
+        } else if (h->flags & CC_FLAG_HALVE) {
+            if (split) k_small_batches<1, true><<<1, 1024, 0, s>>>(h->P, e, q, d_ans, po, pq, nb);
+            else k_small_batches<1, false><<<1, 1024, 0, s>>>(h->P, e, q, d_ans, po, pq, nb);
+        } else {
+            if (split) k_small_batches<0, true><<<1, 1024, 0, s>>>(h->P, e, q, d_ans, po, pq, nb);
+            else k_small_batches<0, false><<<1, 1024, 0, s>>>(h->P, e, q, d_ans, po, pq, nb);
+        }
+        CC_LAUNCH_CHECK("k_small_batches");
+        // the host vector `both` must outlive the async copy: synchronise before returning
+        CC_CUDA_TRY(cudaStreamSynchronize(s));
+        scratch_free(d_off, s);
+        return CC_OK;
+    }
+    const uint32_t saved = h->flags;
+    h->flags &= ~CC_FLAG_VALIDATE;                       // ids already checked above
+    cc_status rc = CC_OK;
+    for (int64_t b = 0; b < nb && rc == CC_OK; ++b)
+        rc = insert_query(h, d_ins + 2 * oi[b], ins_counts[b], d_q + 2 * oq[b], q_counts[b], d_ans + oq[b], s);
+    h->flags = saved;
+    if (rc == CC_OK && host) CC_CUDA_TRY(cudaStreamSynchronize(s));
     return rc;
 }
 

@@ -137,3 +137,47 @@ def test_pinned_host_buffers_zero_copy():
     h.close()
     assert np.array_equal(np.concatenate(outs), want)
     assert np.array_equal(lab.numpy().view(np.uint32), want_lab)
+
+
+@pytest.mark.parametrize("flags", [cc.FLAG_WAIT_FREE, cc.FLAG_WAIT_FREE | cc.FLAG_HALVE,
+                                   cc.FLAG_WAIT_FREE | cc.FLAG_UF_ASYNC])
+def test_wait_free_prefix_soundness(flags):
+    """Type (1): inserts and queries of a batch run concurrently.  Answers
+    are linearizable: 1 => connected after batches 0..i, 0 => not connected after
+    batches 0..i-1; final labels are still exact."""
+    scale = 12
+    n = 1 << scale
+    batches = [gen.incr_batch(seed=12, scale=scale, b=b, n_ins=3000, n_q=3000) for b in range(12)]
+    after, want_lab = oracle.incr_run(n, batches, want_labels=True)
+    empty = np.zeros((0, 2), np.uint32)
+    before_batches = [(batches[i - 1][0] if i else empty, batches[i][1]) for i in range(len(batches))]
+    before, _ = oracle.incr_run(n, before_batches)
+    got, lab = run_stream(n, batches, flags)
+    assert np.all(got[got == 1] <= after[got == 1])      # 1 => connected after the batch
+    assert np.all(before[got == 0] == 0)                 # 0 => not connected before it
+    assert np.array_equal(lab, want_lab)
+    # the contract has room: answers that changed inside a batch are either value
+    undecided = (after == 1) & (before == 0)
+    assert np.array_equal(got[~undecided], after[~undecided])
+
+
+@pytest.mark.parametrize("batch", [1, 10, 1000, 9000])
+@pytest.mark.parametrize("flags", [0, cc.FLAG_FIND_SPLIT | cc.FLAG_HALVE, cc.FLAG_VALIDATE])
+def test_multi_batch_call_bit_exact(batch, flags):
+    """cc_incr_batches == a sequence of cc_incr_batch calls == the oracle."""
+    n = 1 << 12
+    nb = max(1, 20000 // batch)
+    n_ins = max(1, int(batch * 0.9))
+    n_q = max(1, batch - n_ins)
+    batches = [gen.incr_batch(seed=14, scale=12, b=b, n_ins=n_ins, n_q=n_q) for b in range(nb)]
+    want, want_lab = oracle.incr_run(n, batches, want_labels=True)
+    ins = dev(np.concatenate([b[0] for b in batches]))
+    qs = dev(np.concatenate([b[1] for b in batches]))
+    ans = torch.empty(qs.shape[0], dtype=torch.uint8, device="cuda")
+    h = cc.Incr(n, flags)
+    h.batches(np.full(nb, n_ins), ins, np.full(nb, n_q), qs, ans)
+    lab = torch.empty(n, dtype=torch.int32, device="cuda")
+    h.labels(lab)
+    h.close()
+    assert np.array_equal(ans.cpu().numpy(), want)
+    assert np.array_equal(u32(lab), want_lab)
