@@ -83,6 +83,9 @@ typedef int cc_status;
 #define CC_FLAG_NO_MIDCOMPRESS (1u << 6) /* never run the compress between k-out rounds        */
 #define CC_FLAG_MIDCOMPRESS (1u << 7)  /* always run it (default: a 1024-sample probe of the
                                           round-0 chain depth decides, on the device)        */
+#define CC_FLAG_FINISH_SV   (1u << 9)  /* finish with Shiloach-Vishkin rounds (writeMin root
+                                          hooking + full shortcut) instead of
+                                          UF-Rem-CAS; one host sync per round (NEXT-3)      */
 #define CC_FLAG_WAIT_FREE   (1u << 8)  /* cc_incr: the wait-free type (1) setting (P:973-977,
                                           P:2663-2682): a batch's inserts and queries run
                                           concurrently in ONE kernel.  Answers are then
@@ -117,6 +120,7 @@ typedef struct {
     uint64_t finish_gathers;   /* first-level parent reads of k_finish (P[P[v]])      */
     uint64_t h6_writes;        /* label slots rewritten by the final compress (H6)   */
     uint64_t h6_gathers;       /* first-level parent reads of the final compress     */
+    uint64_t sv_rounds;        /* rounds of the Shiloach-Vishkin finish (FINISH_SV)  */
 } cc_counters;
 
 typedef struct {

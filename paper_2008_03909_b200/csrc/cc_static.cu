@@ -41,6 +41,8 @@ struct Ctl {
 
 constexpr uint32_t kSentinel = 0xFFFFFFFFu;
 constexpr int kBigDeg = 4096;     // >  : one CTA per vertex (second kernel)
+constexpr int kFItems = 16;                  // forest/SV scans: slots per thread
+constexpr int kFTile = kBlock * kFItems;     // forest/SV scans: slots per block
 
 // Exclusive warp prefix of c and one atomicAdd per warp; every lane must call.
 __device__ __forceinline__ unsigned long long warp_append(unsigned long long* counter, uint32_t c)
@@ -693,9 +695,211 @@ __global__ void __launch_bounds__(512) k_finish_big(const int64_t* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------
+// NEXT-3: Shiloach-Vishkin as the finish method (Alg. shiloach_vishkin,
+// P:4282-4308; SV hooks only roots, so it composes with sampling
+// and the L_max skip).  The finish candidates' edges (after the
+// sampled prefix) are materialised once; then each round hooks, for every edge
+// whose endpoints' labels differ, the larger label h -- if h was a root at the
+// start of the round (prev_labels[h] == h, kept as a bitmap) -- under the
+// smaller one with writeMin (atomicMin), then fully shortcuts.
+// Rounds repeat until no edge hooks.  The host reads a flag after each round
+// (one synchronisation per round), so this finish is an option, not the
+// default.  In SF mode a second pass per round records, for every hooked
+// root h, an edge whose writeMin value won (P[h] == l after the round).
+__global__ void __launch_bounds__(kBlock) k_sv_degree(const int64_t* __restrict__ off, const uint32_t* __restrict__ cq,
+                                                      const Ctl* ctl, uint32_t skip_prefix, uint32_t* deg)
+{
+    const unsigned long long total = ctl->cand_count;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const uint32_t u = cq[i];
+        const int64_t d = off[u + 1] - off[u] - (int64_t)skip_prefix;
+        deg[i] = d > 0 ? (uint32_t)min(d, (int64_t)0xFFFFFFFF) : 0u;
+    }
+}
+
+// per-block sums of deg[] (kFTile entries per block, 64-bit)
+__global__ void __launch_bounds__(kBlock) k_sv_blocksum(const uint32_t* deg, unsigned long long total,
+                                                        unsigned long long* bsum)
+{
+    const uint64_t base = (uint64_t)blockIdx.x * kFTile + (uint64_t)threadIdx.x * kFItems;
+    unsigned long long c = 0;
+#pragma unroll
+    for (int j = 0; j < kFItems; ++j)
+        if (base + j < total) c += deg[base + j];
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    __shared__ unsigned long long ws[kBlock / 32];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int i = 0; i < kBlock / 32; ++i) t += ws[i];
+        bsum[blockIdx.x] = t;
+    }
+}
+
+// single thread: exclusive scan of the block sums (few thousand entries)
+__global__ void k_sv_scan(unsigned long long* bsum, unsigned long long nb, unsigned long long* total_edges)
+{
+    unsigned long long acc = 0;
+    for (unsigned long long i = 0; i < nb; ++i) {
+        const unsigned long long t = bsum[i];
+        bsum[i] = acc;
+        acc += t;
+    }
+    *total_edges = acc;
+}
+
+// one warp per 32 candidates: each candidate's list is copied cooperatively to
+// its slot range of the flat edge list
+__global__ void __launch_bounds__(kBlock) k_sv_fill(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                                                    const uint32_t* __restrict__ cq, const uint32_t* __restrict__ deg,
+                                                    const unsigned long long* __restrict__ bsum,
+                                                    unsigned long long total, uint32_t skip_prefix, uint2* edges)
+{
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t i = (uint64_t)blockIdx.x * kFTile + (uint64_t)threadIdx.x * kFItems;
+    // exclusive position of each of this thread's kFItems candidates
+    unsigned long long c = 0, pos[kFItems];
+#pragma unroll
+    for (int j = 0; j < kFItems; ++j) {
+        pos[j] = c;
+        c += (i + j < total) ? deg[i + j] : 0u;
+    }
+    // block-level exclusive scan of c (64-bit) via warp shuffles + shared memory
+    unsigned long long incl = c;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (unsigned)o) incl += t;
+    }
+    __shared__ unsigned long long ws[kBlock / 32];
+    if (lane == 31) ws[threadIdx.x >> 5] = incl;
+    __syncthreads();
+    unsigned long long wbase = 0;
+    for (unsigned w = 0; w < (threadIdx.x >> 5); ++w) wbase += ws[w];
+    const unsigned long long tbase = bsum[blockIdx.x] + wbase + incl - c;
+#pragma unroll 1
+    for (int j = 0; j < kFItems; ++j) {
+        if (i + j >= total) break;
+        const uint32_t u = cq[i + j];
+        const int64_t b = off[u] + skip_prefix;
+        const uint32_t d = deg[i + j];
+        for (uint32_t x = 0; x < d; ++x) edges[tbase + pos[j] + x] = make_uint2(u, adj[b + x]);
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) k_sv_rootbits(const uint32_t* P, uint32_t n, uint32_t* bits)
+{
+    const uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool root = v < n && P[v] == (uint32_t)v;
+    const uint32_t w = __ballot_sync(0xffffffffu, root);
+    if ((threadIdx.x & 31) == 0 && v < n) bits[v >> 5] = w;
+}
+
+// the label of x at the start of the round: x itself if x was a root then,
+// else its parent (non-root slots are not written during a round)
+__device__ __forceinline__ uint32_t sv_label(const uint32_t* P, const uint32_t* bits, uint32_t x)
+{
+    return ((bits[x >> 5] >> (x & 31)) & 1u) ? x : P[x];
+}
+
+__global__ void __launch_bounds__(kBlock) k_sv_hook(uint32_t* P, const uint2* __restrict__ edges,
+                                                    unsigned long long ne, const uint32_t* __restrict__ bits,
+                                                    unsigned int* changed)
+{
+    unsigned int ch = 0;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < ne;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const uint2 e = edges[i];
+        const uint32_t a = sv_label(P, bits, e.x), b = sv_label(P, bits, e.y);
+        if (a == b) continue;
+        const uint32_t h = max(a, b), l = min(a, b);     // h is a root of the round's start (a label)
+        ch |= atomicMin(P + h, l) > l ? 1u : 0u;         // writeMin
+    }
+    if (__any_sync(0xffffffffu, ch != 0) && (threadIdx.x & 31) == 0) atomicOr(changed, 1u);
+}
+
+__global__ void __launch_bounds__(kBlock) k_sv_record(const uint32_t* P, const uint2* __restrict__ edges,
+                                                      unsigned long long ne, const uint32_t* __restrict__ bits, uint2* F)
+{
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < ne;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const uint2 e = edges[i];
+        const uint32_t a = sv_label(P, bits, e.x), b = sv_label(P, bits, e.y);
+        if (a == b) continue;
+        const uint32_t h = max(a, b), l = min(a, b);
+        if (P[h] == l) F[h] = e;                         // this edge's writeMin won at h
+    }
+}
+
+template <bool SF>
+static cc_status sv_finish(const int64_t* off, const uint32_t* adj, uint32_t* P, uint32_t n, const uint32_t* cq,
+                           Ctl* ctl, uint32_t skip_prefix, uint2* F, cc_counters* cnt, cudaStream_t s)
+{
+    unsigned long long cand = 0;
+    CC_CUDA_TRY(cudaMemcpyAsync(&cand, &ctl->cand_count, sizeof(cand), cudaMemcpyDeviceToHost, s));
+    CC_CUDA_TRY(cudaStreamSynchronize(s));
+    if (cand == 0) return CC_OK;
+    const int sms = num_sms();
+    const unsigned long long nbk = (cand + kFTile - 1) / kFTile;
+    uint32_t *deg = nullptr, *bits = nullptr;
+    unsigned long long *bsum = nullptr, *tot = nullptr;
+    uint2* edges = nullptr;
+    unsigned int* changed = nullptr;
+    cc_status rc = CC_OK;
+    auto body = [&]() -> cc_status {
+        CC_CUDA_TRY(scratch_alloc((void**)&deg, sizeof(uint32_t) * cand, s));
+        CC_CUDA_TRY(scratch_alloc((void**)&bsum, sizeof(unsigned long long) * nbk, s));
+        CC_CUDA_TRY(scratch_alloc((void**)&tot, sizeof(unsigned long long), s));
+        k_sv_degree<<<sms * 8, kBlock, 0, s>>>(off, cq, ctl, skip_prefix, deg);
+        CC_LAUNCH_CHECK("k_sv_degree");
+        k_sv_blocksum<<<(unsigned)nbk, kBlock, 0, s>>>(deg, cand, bsum);
+        CC_LAUNCH_CHECK("k_sv_blocksum");
+        k_sv_scan<<<1, 1, 0, s>>>(bsum, nbk, tot);
+        CC_LAUNCH_CHECK("k_sv_scan");
+        unsigned long long ne = 0;
+        CC_CUDA_TRY(cudaMemcpyAsync(&ne, tot, sizeof(ne), cudaMemcpyDeviceToHost, s));
+        CC_CUDA_TRY(cudaStreamSynchronize(s));
+        if (ne == 0) return CC_OK;
+        CC_CUDA_TRY(scratch_alloc((void**)&edges, sizeof(uint2) * ne, s));
+        CC_CUDA_TRY(scratch_alloc((void**)&bits, sizeof(uint32_t) * (((uint64_t)n + 31) / 32), s));
+        CC_CUDA_TRY(scratch_alloc((void**)&changed, sizeof(unsigned int), s));
+        k_sv_fill<<<(unsigned)nbk, kBlock, 0, s>>>(off, adj, cq, deg, bsum, cand, skip_prefix, edges);
+        CC_LAUNCH_CHECK("k_sv_fill");
+        const unsigned nbv = (unsigned)(((uint64_t)n + kBlock - 1) / kBlock);
+        for (uint64_t round = 1;; ++round) {
+            k_sv_rootbits<<<nbv, kBlock, 0, s>>>(P, n, bits);        // prev_labels[h] == h
+            CC_LAUNCH_CHECK("k_sv_rootbits");
+            CC_CUDA_TRY(cudaMemsetAsync(changed, 0, sizeof(unsigned int), s));
+            k_sv_hook<<<sms * 8, kBlock, 0, s>>>(P, edges, ne, bits, changed);
+            CC_LAUNCH_CHECK("k_sv_hook");
+            if (SF) {
+                k_sv_record<<<sms * 8, kBlock, 0, s>>>(P, edges, ne, bits, F);
+                CC_LAUNCH_CHECK("k_sv_record");
+            }
+            unsigned int h_changed = 0;
+            CC_CUDA_TRY(cudaMemcpyAsync(&h_changed, changed, sizeof(h_changed), cudaMemcpyDeviceToHost, s));
+            CC_CUDA_TRY(cudaStreamSynchronize(s));
+            if (cnt) CC_CUDA_TRY(cudaMemcpyAsync(&cnt->sv_rounds, &round, sizeof(round), cudaMemcpyHostToDevice, s));
+            if (!h_changed) break;
+            cc_status r = launch_compress(P, n, nullptr, nullptr, s, "k_compress(SV shortcut)");   // FullShortcut
+            if (r) return r;
+        }
+        CC_CUDA_TRY(cudaStreamSynchronize(s));
+        return CC_OK;
+    };
+    rc = body();
+    scratch_free(deg, s);
+    scratch_free(bsum, s);
+    scratch_free(tot, s);
+    scratch_free(edges, s);
+    scratch_free(bits, s);
+    scratch_free(changed, s);
+    return rc;
+}
+
+// ---------------------------------------------------------------------------
 // K7: Filter -- stable compaction of the non-sentinel forest slots.
-constexpr int kFItems = 16;                  // slots per thread
-constexpr int kFTile = kBlock * kFItems;     // slots per block
 
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* total)
 {
@@ -931,10 +1135,15 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
             CC_LAUNCH_CHECK("k_finish");
         }
         CC_CUDA_TRY(mark(CC_MARK_FINISH));
-        k_finish_proc<MODE, SF><<<sms * 8, kBlock, 0, s>>>(off, adj, P, cq, ctl, skip_prefix, big, F, o.counters);
-        CC_LAUNCH_CHECK("k_finish_proc");
-        k_finish_big<MODE, SF><<<sms * 2, 512, 0, s>>>(off, adj, P, big, ctl, skip_prefix, F, o.counters);
-        CC_LAUNCH_CHECK("k_finish_big");
+        if (o.flags & CC_FLAG_FINISH_SV) {
+            cc_status r = sv_finish<SF>(off, adj, P, n, cq, ctl, skip_prefix, F, o.counters, s);
+            if (r) return r;
+        } else {
+            k_finish_proc<MODE, SF><<<sms * 8, kBlock, 0, s>>>(off, adj, P, cq, ctl, skip_prefix, big, F, o.counters);
+            CC_LAUNCH_CHECK("k_finish_proc");
+            k_finish_big<MODE, SF><<<sms * 2, 512, 0, s>>>(off, adj, P, big, ctl, skip_prefix, F, o.counters);
+            CC_LAUNCH_CHECK("k_finish_big");
+        }
         CC_CUDA_TRY(mark(CC_MARK_FINISH_BIG));
         if (o.timings) CC_CUDA_TRY(cudaEventRecord(ev[3], s));
         // H6

@@ -37,6 +37,9 @@ OPTION_GRID = [
     dict(k=2, variant="afforest", flags=cc.FLAG_MIDCOMPRESS),
     dict(k=3, variant="hybrid", flags=cc.FLAG_MIDCOMPRESS | cc.FLAG_HALVE, seed=5),
     dict(k=2, variant="pure", flags=0, seed=13),
+    dict(k=2, variant="afforest", flags=cc.FLAG_FINISH_SV),
+    dict(k=0, variant="afforest", flags=cc.FLAG_FINISH_SV),
+    dict(k=1, variant="hybrid", flags=cc.FLAG_FINISH_SV | cc.FLAG_NO_SKIP, seed=3),
     dict(k=1, variant="pure", flags=cc.FLAG_UF_ASYNC, seed=2),
 ]
 
@@ -189,7 +192,9 @@ def test_empty_and_degenerate_abi():
 
 
 # ---------------------------------------------------------------------------
-@pytest.mark.parametrize("opt", [OPTION_GRID[0], OPTION_GRID[1], OPTION_GRID[4], OPTION_GRID[6], OPTION_GRID[7]],
+@pytest.mark.parametrize("opt", [OPTION_GRID[0], OPTION_GRID[1], OPTION_GRID[4], OPTION_GRID[6], OPTION_GRID[7],
+                                 dict(k=2, variant="afforest", flags=cc.FLAG_FINISH_SV),
+                                 dict(k=0, variant="afforest", flags=cc.FLAG_FINISH_SV)],
                          ids=lambda o: f"k{o['k']}-{o['variant']}-f{o['flags']}")
 def test_spanning_forest_valid(opt):
     for name, off, adj in small_graphs():
@@ -225,7 +230,7 @@ def test_repeat_stress_random_options():
     rng = np.random.default_rng(1)
     d_off, d_adj = to_dev(off, adj)
     flags_pool = [0, cc.FLAG_HALVE, cc.FLAG_UF_ASYNC, cc.FLAG_NO_SKIP, cc.FLAG_NO_MIDCOMPRESS, cc.FLAG_NO_DEGSKIP,
-                  cc.FLAG_MIDCOMPRESS]
+                  cc.FLAG_MIDCOMPRESS, cc.FLAG_FINISH_SV]
     for it in range(200):
         k = int(rng.integers(0, 5))
         variant = ["afforest", "hybrid", "pure"][int(rng.integers(0, 3))]
