@@ -380,6 +380,20 @@ def run_ours(a, rank, ws):
 
     # ---- measurement floors (K10, Table 8 analogue P:3732-3799), outside the timed region
     line["floors"] = floors(cc, d_off, d_adj, n, m, labels, stream, mean_ms)
+    # The link kernel is bound by dependent random 4-byte accesses into the 4n-byte
+    # parent array, not by streaming bandwidth: set its random-access count (one
+    # P[v] gather per pending link + one load or CAS per Rem-loop step + the hook
+    # CAS) against the uniform random-gather rate measured just above on an
+    # array of the same size.
+    rg = line["floors"]["random_gather"]["Gloads_per_s"]
+    lk = kernels.get("k_link_pending")
+    if lk:
+        acc = ctr["pending_links"] + ctr["link_steps"] + ctr["sample_hooks"]
+        ach = acc / (lk["ms"] * 1e-3) / 1e9
+        line["roofline"]["random_access_view"] = {
+            "kernel": "k_link_pending", "random_accesses_per_launch": int(acc),
+            "achieved_Gaccess_per_s": round(ach, 2), "uniform_random_gather_Gloads_per_s": rg,
+            "frac_of_random_gather_rate": round(ach / rg, 3)}
 
     # ---- e2e: the same metric through the C ABI with HOST (pinned) buffers
     if not a.no_e2e and a.e2e_steps > 0:
