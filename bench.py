@@ -106,20 +106,30 @@ class Clocks:
         try:
             self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.f,
+                                          "--format=csv,noheader,nounits", "-lms", "25"], stdout=self.f,
                                          stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
-        time.sleep(0.2)
+            return
+        # nvidia-smi takes ~1 s to start: wait for its first row so that a short
+        # timed region (20 steps of ~3 ms) is covered by samples
+        t0 = time.time()
+        while time.time() - t0 < 10:
+            self.f.flush()
+            if os.path.getsize(self.f.name) > 0:
+                break
+            time.sleep(0.05)
+        self.skip = open(self.f.name).read().count("\n")    # rows sampled before the timed region
 
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.1)
+        time.sleep(0.03)
         self.proc.terminate()
         self.proc.wait()
         self.f.flush()
-        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.count(",") >= 5]
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines()[getattr(self, "skip", 0):]
+                if r.count(",") >= 5]
         os.unlink(self.f.name)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
@@ -197,11 +207,12 @@ def run_reference(a, rank, ws):
 
 
 # ---------------------------------------------------------------------------
-def byte_model(off_h_deg_pos, n, m, k, ctr, sampled, final, mid_ran):
+def byte_model(off_h_deg_pos, n, m, k, ctr, sampled, final, mid_ran, f0=None):
     """Algorithmic bytes per launch of each kernel.
 
     Counts only what the implemented design must move (SURVEY §8(d) honesty
-    rules): 4 B per uint32 read/written, 8 B per int64 offset."""
+    rules): 4 B per uint32 read/written, 8 B per int64 offset.  f0 = (F0
+    non-roots, F0 vertices at depth >= 2) selects the contracted-link model."""
     import numpy as np
     npos, sum_mink = off_h_deg_pos
     pend = ctr["pending_links"]
@@ -225,6 +236,21 @@ def byte_model(off_h_deg_pos, n, m, k, ctr, sampled, final, mid_ran):
         # P read + first-level parent reads + changed-label writes
         "k_compress_H6": 4 * n + 4 * ctr["h6_gathers"] + 4 * ctr["h6_writes"],
     }
+    if f0 is not None:
+        # contracted link: + the F0-root bitmap words in k_sample_init;
+        # the "mid" span is the rank scan (bitmap read twice, prefix words written,
+        # rid + C initialised: 8 B per compact slot) and the F0 compress (P read, one
+        # parent read per F0 non-root, one write per vertex at depth >= 2); the link
+        # span reads the pending pairs and gathers P[u], P[v] (the C-space walk and
+        # CAS run on the L2-resident compact array and are not HBM bytes), then
+        # finalises C (read C, write rid); k_finish reads a rank word (8 B) and a
+        # rid entry (4 B) per non-isolated vertex instead of gathering in P
+        R = ctr["contract_roots"]
+        f0_nonroots, f0_deep = f0
+        B["k_sample_init"] += n // 8
+        B["k_compress_mid"] = 3 * (n // 8) + 8 * R + 4 * n + 4 * f0_nonroots + 4 * f0_deep
+        B["k_link_pending"] = 16 * pend + 8 * R
+        B["k_finish"] = 4 * n + n // 8 + 12 * ctr["finish_gathers"] + 4 * ctr["compress_writes"] + 4 * fin_v
     B["finish_phase"] = B["k_finish"] + B["k_finish_proc"] + B["k_compress_H6"]
     B["sampling_phase"] = B["k_sample_init"] + B["k_compress_mid"] + B["k_link_pending"]
     return B, {"relabelled": relab, "sampled_nonroots": nonroot, "mid_nonroots_bound": npos}
@@ -304,8 +330,27 @@ def run_ours(a, rank, ws):
     # the mid compress runs when forced, or when the device probe found long chains
     mid_ran = a.k > 0 and not (a.flags & cc.FLAG_NO_MIDCOMPRESS) and (
         bool(a.flags & cc.FLAG_MIDCOMPRESS) or ctr["probe_deep"] * 8 >= 1024)
-    B, extra = byte_model((nonisolated, sum_mink), n, m, a.k, ctr, sampled, final, mid_ran)
+    contract = a.k > 0 and bool(a.flags & cc.FLAG_CONTRACT) and not (a.flags & cc.FLAG_NO_SKIP)
+    f0 = None
+    if contract:
+        # the round-0 forest F0 (P[u] = first sampled neighbour if smaller), for the byte model
+        ids = torch.arange(n, device=dev, dtype=torch.int64)
+        if a.variant == "pure":                    # random first pick: bound by the non-isolated count
+            nr = nonisolated - ctr["contract_roots"]
+            f0 = (nr, nr)
+        else:
+            first = d_adj[d_off[:-1].clamp(max=max(m - 1, 0))].to(torch.int64) & 0xFFFFFFFF
+            p0 = torch.where((torch.diff(d_off) > 0) & (first < ids), first, ids)
+            del first
+            f0 = (int((p0 != ids).sum().item()), int((p0[p0] != p0).sum().item()))
+            del p0
+        del ids
+        mid_ran = True
+    B, extra = byte_model((nonisolated, sum_mink), n, m, a.k, ctr, sampled, final, mid_ran, f0)
     extra["mid_compress_ran"] = mid_ran
+    extra["contracted_link"] = contract
+    if f0 is not None:
+        extra["f0_nonroots"], extra["f0_depth_ge2"] = f0
     components = int(np.count_nonzero(final == np.arange(n, dtype=np.uint32)))
 
     # ---- warm-up
@@ -387,8 +432,22 @@ def run_ours(a, rank, ws):
     # array of the same size.
     rg = line["floors"]["random_gather"]["Gloads_per_s"]
     lk = kernels.get("k_link_pending")
-    if lk:
-        acc = ctr["pending_links"] + ctr["link_steps"] + ctr["sample_hooks"]
+    if lk and contract:
+        # contracted: the HBM random accesses are the P[v] gathers (one per pending
+        # link); the Rem walk and CAS run in the L2-resident compact array
+        acc = ctr["pending_links"]
+        ach = acc / (lk["ms"] * 1e-3) / 1e9
+        line["roofline"]["random_access_view"] = {
+            "kernel": "k_link_pending", "hbm_random_accesses_per_launch": int(acc),
+            "l2_link_accesses_per_launch": int(ctr["link_steps"] + ctr["sample_hooks"]),
+            "achieved_Gaccess_per_s": round(ach, 2), "uniform_random_gather_Gloads_per_s": rg,
+            "frac_of_random_gather_rate": round(ach / rg, 3)}
+    elif lk:
+        # lane-refill kernel (default): link_steps counts Rem iterations that issued a
+        # load or CAS, each lost CAS adds the re-read of P[rv]; round-1 kernel: every
+        # loop iteration plus the hook CAS
+        refill = not (a.flags & (cc.FLAG_NO_REFILL | cc.FLAG_HALVE | cc.FLAG_UF_ASYNC))
+        acc = ctr["pending_links"] + ctr["link_steps"] + (ctr["cas_failures"] if refill else ctr["sample_hooks"])
         ach = acc / (lk["ms"] * 1e-3) / 1e9
         line["roofline"]["random_access_view"] = {
             "kernel": "k_link_pending", "random_accesses_per_launch": int(acc),

@@ -86,6 +86,14 @@ typedef int cc_status;
 #define CC_FLAG_FINISH_SV   (1u << 9)  /* finish with Shiloach-Vishkin rounds (writeMin root
                                           hooking + full shortcut) instead of
                                           UF-Rem-CAS; one host sync per round (NEXT-3)      */
+#define CC_FLAG_CONTRACT    (1u << 10) /* run the k-out CAS links on the forest contracted by
+                                          the first k-out round: a compact parent array
+                                          with one slot per non-isolated F0 root (see
+                                          cc_labels); ignored with CC_FLAG_NO_SKIP.
+                                          Measured slower than the default in place link
+                                          on C3/C4                               */
+#define CC_FLAG_NO_REFILL   (1u << 11) /* k-out links: one warp step per slowest lane (the
+                                          round-1 kernel) instead of lane refill           */
 #define CC_FLAG_WAIT_FREE   (1u << 8)  /* cc_incr: the wait-free type (1) setting (P:973-977,
                                           P:2663-2682): a batch's inserts and queries run
                                           concurrently in ONE kernel.  Answers are then
@@ -121,6 +129,8 @@ typedef struct {
     uint64_t h6_writes;        /* label slots rewritten by the final compress (H6)   */
     uint64_t h6_gathers;       /* first-level parent reads of the final compress     */
     uint64_t sv_rounds;        /* rounds of the Shiloach-Vishkin finish (FINISH_SV)  */
+    uint64_t contract_roots;   /* slots of the contracted parent array (non-isolated
+                                  roots of the first k-out round's forest F0)        */
 } cc_counters;
 
 typedef struct {
@@ -161,7 +171,13 @@ void cc_opts_default(cc_opts* o);
 /* Connectivity, Alg. 1 with k-out sampling (Alg. 4), IdentifyFrequent
  * and the UF-Rem-CAS finish, then a full
  * compress.  labels (out, n) is also the parent array, used in place:
- * on return labels[v] = minimum vertex id of v's component (canonical). */
+ * on return labels[v] = minimum vertex id of v's component (canonical).
+ * The first k-out round hooks every vertex under its first sampled neighbour
+ * when that is smaller (a forest F0); the remaining sampled edges are then
+ * unioned in place on labels (default), or, with CC_FLAG_CONTRACT, with the
+ * same UF-Rem-CAS rule on a compact parent array with one slot per
+ * non-isolated F0 root, numbered in id order (so the min-id orientation is
+ * kept); the latter needs the symmetric-graph precondition above. */
 cc_status cc_labels(const int64_t* offsets, const uint32_t* adj, uint32_t n, int64_t m,
                     uint32_t* labels, const cc_opts* opts, void* stream);
 

@@ -31,6 +31,8 @@ FLAG_NO_MIDCOMPRESS = 1 << 6
 FLAG_MIDCOMPRESS = 1 << 7
 FLAG_WAIT_FREE = 1 << 8
 FLAG_FINISH_SV = 1 << 9
+FLAG_CONTRACT = 1 << 10
+FLAG_NO_REFILL = 1 << 11
 
 # every symbol include/cc.h and include/cc_bench.h declare
 EXPORTS = [
@@ -53,7 +55,7 @@ class Timings(ctypes.Structure):
 COUNTER_FIELDS = ["pending_links", "worklist", "finish_vertices", "finish_edges", "sample_hooks", "finish_hooks",
                   "big_vertices", "compress_writes",
                   "link_steps", "cas_failures", "probe_deep", "finish_gathers", "h6_writes", "h6_gathers",
-                  "sv_rounds"]
+                  "sv_rounds", "contract_roots"]
 
 
 class Opts(ctypes.Structure):

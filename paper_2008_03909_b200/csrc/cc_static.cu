@@ -68,6 +68,39 @@ __device__ __forceinline__ void warp_count(uint64_t* ctr, uint32_t c)
     if ((threadIdx.x & 31) == 0 && s) atomicAdd(reinterpret_cast<unsigned long long*>(ctr), (unsigned long long)s);
 }
 
+// Block-wide exclusive scan of one value per thread; *total = block sum.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* total)
+{
+    constexpr int NW = kBlock / 32;
+    __shared__ uint32_t ws[NW];
+    __shared__ uint32_t tot;
+    const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (unsigned)o) incl += t;
+    }
+    if (lane == 31) ws[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        const uint32_t sv = lane < (unsigned)NW ? ws[lane] : 0u;
+        uint32_t si = sv;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t t = __shfl_up_sync(0xffffffffu, si, o);
+            if (lane >= (unsigned)o) si += t;
+        }
+        if (lane < (unsigned)NW) ws[lane] = si - sv;
+        if (lane == (unsigned)NW - 1) tot = si;
+    }
+    __syncthreads();
+    const uint32_t r = ws[w] + incl - x;
+    *total = tot;
+    __syncthreads();
+    return r;
+}
+
 // ---------------------------------------------------------------------------
 // K0: H1 + first k-out round + pending list + finish bitmap.
 //
@@ -98,7 +131,7 @@ template <int VAR, bool SF, bool WIN>
 __global__ void __launch_bounds__(kBlock, 3) k_sample_init(
     const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, uint32_t n, int64_t m, uint32_t k,
     uint64_t seed, uint32_t full_deg, uint32_t* __restrict__ P, uint2* __restrict__ F,
-    uint2* __restrict__ pend, uint32_t* __restrict__ bm, Ctl* ctl, cc_counters* cnt)
+    uint2* __restrict__ pend, uint32_t* __restrict__ bm, uint2* __restrict__ rbw, Ctl* ctl, cc_counters* cnt)
 {
     __shared__ uint32_t s_wtot[kBlock / 32];
     __shared__ unsigned long long s_wbase[kBlock / 32];
@@ -145,7 +178,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_sample_init(
         }
     }
     uint32_t c[kV];
-    uint32_t bits = 0, nwl = 0;
+    uint32_t bits = 0, rbits = 0, nwl = 0;
 #pragma unroll
     for (int j = 0; j < kV; ++j) {
         const uint64_t u = wbase + 32 * j + lane;
@@ -157,8 +190,14 @@ __global__ void __launch_bounds__(kBlock, 3) k_sample_init(
         nwl += mark;
         const uint32_t word = __ballot_sync(0xffffffffu, mark);
         if (lane == (unsigned)j) bits = word;
+        // non-isolated root of the round-0 forest F0 (contracted link)
+        const uint32_t rword = __ballot_sync(0xffffffffu, u < n && d[j] > 0 && !(v0[j] < (uint32_t)u));
+        if (lane == (unsigned)j) rbits = rword;
     }
-    if (lane < (unsigned)kV && wbase + 32 * lane < n) bm[(wbase >> 5) + lane] = bits;
+    if (lane < (unsigned)kV && wbase + 32 * lane < n) {
+        bm[(wbase >> 5) + lane] = bits;
+        if (rbw) rbw[(wbase >> 5) + lane].x = rbits;
+    }
 #pragma unroll
     for (int j = 0; j < kV; ++j) {
         const uint64_t u = wbase + 32 * j + lane;
@@ -439,6 +478,276 @@ __global__ void __launch_bounds__(kBlock) k_link_pending(
 }
 
 // ---------------------------------------------------------------------------
+// K1': the same UF-Rem-CAS + SplitAtomicOne links with lane refill.
+//
+// The link kernel is latency-bound: every Rem-loop step is a dependent random
+// load, and in k_link_pending a warp keeps stepping until its slowest lane's
+// link is done, so on average half the lanes idle (ncu: 15 of 32 threads per
+// instruction).  Here each warp streams its pending links through a 32-entry
+// register buffer (one coalesced pend load + the P[u], P[v] gathers of all 32
+// entries, issued one buffer ahead so they are in flight while the current one
+// is consumed); a lane whose link finished takes the next buffered entry by a
+// shuffle, and entries whose first parents are already equal retire without
+// occupying a lane.  Every loop iteration then does one Rem step (one load, or
+// a CAS) on every lane that holds a link.  The step is exactly link_rem_from's
+// iteration (readings R1, R6), so the result is the same partition.
+#ifndef CC_REFILL_MINB
+#define CC_REFILL_MINB 6
+#endif
+template <bool SF>
+__global__ void __launch_bounds__(kBlock, CC_REFILL_MINB) k_link_refill(uint32_t* P, const uint2* __restrict__ pend, const Ctl* ctl,
+                                                        uint2* F, cc_counters* cnt)
+{
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const unsigned long long total = ctl->pend_count;
+    const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    unsigned long long chunk = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    // next buffer: entry chunk*32 + lane with its first two parent reads in flight
+    uint2 nb = make_uint2(0u, 0u);
+    uint32_t npu = 0, npv = 0, navail = 0;
+    auto fetch = [&]() {
+        const unsigned long long b0 = chunk * 32;
+        navail = b0 < total ? (uint32_t)min(32ull, total - b0) : 0u;
+        const bool ok = lane < navail;
+        nb = ok ? pend[b0 + lane] : make_uint2(0u, 0u);
+        npu = ok ? ld_relaxed(P + nb.x) : 0u;
+        npv = ok ? ld_relaxed(P + nb.y) : 0u;
+        chunk += nwarps;
+    };
+    fetch();
+    uint2 cb = nb;
+    uint32_t cpu = npu, cpv = npv, cavail = navail, cpos = 0;
+    if (cavail) fetch();
+    bool act = false;
+    uint32_t u = 0, v = 0, ru = 0, rv = 0, pu = 0, pv = 0;
+    uint32_t hooked = 0, steps = 0, fails = 0;
+    while (true) {
+        // refill idle lanes from the buffer (warp-uniform loop)
+        unsigned need = __ballot_sync(0xffffffffu, !act);
+        while (need && cavail) {
+            const uint32_t src = cpos + __popc(need & lt_mask);
+            const uint32_t sl = src & 31;
+            const uint32_t xu = __shfl_sync(0xffffffffu, cb.x, sl), xv = __shfl_sync(0xffffffffu, cb.y, sl);
+            const uint32_t xpu = __shfl_sync(0xffffffffu, cpu, sl), xpv = __shfl_sync(0xffffffffu, cpv, sl);
+            if (!act && src < cavail && xpu != xpv) {        // equal first parents: already one set
+                act = true;
+                u = ru = xu;
+                v = rv = xv;
+                pu = xpu;
+                pv = xpv;
+            }
+            cpos = min(cavail, cpos + (uint32_t)__popc(need));
+            if (cpos == cavail) {                            // buffer used up: rotate in the prefetched one
+                cb = nb;
+                cpu = npu;
+                cpv = npv;
+                cavail = navail;
+                cpos = 0;
+                if (cavail) fetch();
+            }
+            need = __ballot_sync(0xffffffffu, !act);
+        }
+        if (!__any_sync(0xffffffffu, act)) break;           // buffer empty and every link done
+        if (act) {                                           // one iteration of link_rem_from
+            ++steps;
+            if (pu < pv) {
+                uint32_t t = ru; ru = rv; rv = t;
+                t = pu; pu = pv; pv = t;
+            }
+            if (ru == pu) {                                  // ru is a root: hook it under pv
+                const uint32_t old = cas(P + ru, ru, pv);
+                if (old == ru) {
+                    if (SF) F[ru] = make_uint2(u, v);
+                    ++hooked;
+                    act = false;
+                } else {
+                    ++fails;
+                    pu = old;
+                    pv = ld_relaxed(P + rv);
+                }
+            } else {
+                const uint32_t w = ld_relaxed(P + pu);       // SplitAtomicOne on ru
+                if (w != pu) cas(P + ru, pu, w);
+                ru = pu;
+                pu = w;
+            }
+            if (act && pu == pv) act = false;
+        }
+    }
+    if (cnt) {
+        warp_count(&cnt->sample_hooks, hooked);
+        warp_count(&cnt->link_steps, steps);
+        warp_count(&cnt->cas_failures, fails);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Contracted k-out link (CC_FLAG_CONTRACT; measured slower than the in-place
+// link on C3/C4 -- DESIGN.md §6 -- and kept as an evaluated alternative).
+//
+// After round 0 the parent array is a forest F0: P[u] = v0(u) when the first
+// sampled neighbour is smaller, else u.  Its roots are the isolated vertices
+// and the non-isolated "local minima" (C4: 13.5M of 63M non-isolated).  Every
+// remaining sampled edge (u, v) is Union(u, v), and Union(u, v) is
+// Union(root_F0(u), root_F0(v)) -- same sets.  So, after one compress of F0
+// (P[u] = root_F0(u), a streaming pass whose parents mostly precede their
+// children), the CAS links run on a COMPACT parent array C with one slot per
+// non-isolated F0 root: the link reads P[u] (coalesced) and P[v] (the one
+// random HBM read of a link), maps both roots to compact ids, and the whole
+// UF-Rem-CAS walk then runs in C, which (with the 8-byte rank words below)
+// stays resident in the 126 MB L2 instead of walking the 512 MiB P.
+//
+// Compact ids are assigned in id order (the rank of r among the roots), so
+// "hook the larger root under the smaller" in C is the same orientation as in
+// P (reading R1) and the min-id-root invariant I1 carries over: the root of a
+// sampled component is its minimum vertex, which is an F0 root (its own first
+// neighbour, if smaller, would be in the component).
+//
+// rbw[w] (one uint2 per 32 vertices): x = bitmap of the word's non-isolated F0
+// roots (written by k_sample_init), y = number of such roots in earlier words.
+// cid(r) = rbw[r>>5].y + popc(rbw[r>>5].x & ((1 << (r&31)) - 1)); rid is the
+// inverse map (compact -> vertex id).  Neighbours of a vertex have degree > 0
+// only in a symmetric graph, hence the precondition (CC_FLAG_NO_SKIP falls back
+// to the in-place link).
+__device__ __forceinline__ uint32_t cid_of(uint2 w, uint32_t r)
+{
+    return w.y + __popc(w.x & ((1u << (r & 31)) - 1u));
+}
+
+// Forest record for C-space hooks: the hooked compact root c is the F0 root
+// rid[c] in vertex space, never hooked in round 0, so its F slot is free.
+struct ForestC {
+    uint2* F;
+    const uint32_t* rid;
+    uint32_t u, v;
+    __device__ __forceinline__ void record(uint32_t c, uint32_t, uint32_t) const { F[rid[c]] = make_uint2(u, v); }
+};
+
+template <int MODE, bool SF>
+__global__ void __launch_bounds__(kBlock) k_link_contract(
+    const uint32_t* __restrict__ P, const uint2* __restrict__ pend, const Ctl* ctl, const uint2* __restrict__ rbw,
+    uint32_t* C, const uint32_t* __restrict__ rid, uint2* F, cc_counters* cnt)
+{
+    const unsigned long long total = ctl->pend_count;
+    const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
+    const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    Stat st;
+    for (unsigned long long base = 0; base < total; base += nthreads * kLB) {
+        uint2 pr[kLB];
+        uint32_t ru[kLB], rv[kLB], cu[kLB], cv[kLB], pu[kLB], pv[kLB];
+#pragma unroll
+        for (int q = 0; q < kLB; ++q) {
+            const unsigned long long i = base + q * nthreads + tid;
+            pr[q] = i < total ? pend[i] : make_uint2(0u, 0u);
+        }
+        // P is read-only in this kernel (the hooks go to C): read-only loads
+#pragma unroll
+        for (int q = 0; q < kLB; ++q) {
+            ru[q] = __ldg(P + pr[q].x);
+            rv[q] = __ldg(P + pr[q].y);
+        }
+#pragma unroll
+        for (int q = 0; q < kLB; ++q) {
+            if (ru[q] != rv[q]) {
+                cu[q] = cid_of(__ldg(rbw + (ru[q] >> 5)), ru[q]);
+                cv[q] = cid_of(__ldg(rbw + (rv[q] >> 5)), rv[q]);
+            } else {
+                cu[q] = cv[q] = 0u;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kLB; ++q) {
+            pu[q] = ru[q] != rv[q] ? ld_relaxed(C + cu[q]) : 0u;
+            pv[q] = ru[q] != rv[q] ? ld_relaxed(C + cv[q]) : 0u;
+        }
+        uint32_t hooked = 0;
+#pragma unroll
+        for (int q = 0; q < kLB; ++q) {
+            if (pu[q] == pv[q]) continue;
+            if constexpr (MODE == 2) {
+                if constexpr (SF) hooked += link_async(C, cu[q], cv[q], ForestC{F, rid, pr[q].x, pr[q].y});
+                else hooked += link_async(C, cu[q], cv[q], NoForest{});
+            } else {
+                if constexpr (SF)
+                    hooked += link_rem_from<MODE == 1>(C, cu[q], cv[q], pu[q], pv[q], ForestC{F, rid, pr[q].x, pr[q].y},
+                                                       cnt ? &st : nullptr);
+                else hooked += link_rem_from<MODE == 1>(C, cu[q], cv[q], pu[q], pv[q], NoForest{}, cnt ? &st : nullptr);
+            }
+        }
+        __syncwarp();
+        if (cnt) warp_count(&cnt->sample_hooks, hooked);
+    }
+    if (cnt) {
+        warp_count(&cnt->link_steps, st.steps);
+        warp_count(&cnt->cas_failures, st.fails);
+    }
+}
+
+// After the links: rid[c] <- rid[root_C(c)], the vertex id of c's sampled
+// component root.  Safe in place: a C root's rid slot is never rewritten (its
+// root is itself) and only root slots are read through rid here.
+__global__ void __launch_bounds__(kBlock) k_contract_final(const uint32_t* C, uint32_t* rid, const int64_t* Rtot)
+{
+    const uint64_t R = (uint64_t)*Rtot;
+    for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < R; c += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t p = C[c];
+        if (p == (uint32_t)c) continue;
+        rid[c] = rid[root_plain(C, p)];
+    }
+}
+
+// The sampled label of a vertex whose F0 root (P[u] after the F0 compress) is r.
+__device__ __forceinline__ uint32_t expand_root(const uint2* rbw, const uint32_t* rid, uint32_t r)
+{
+    const uint2 w = rbw[r >> 5];
+    return (w.x >> (r & 31) & 1u) ? rid[cid_of(w, r)] : r;
+}
+
+// sampled_out debug path: P[u] <- expand(P[u]) for every u
+__global__ void __launch_bounds__(kBlock) k_expand(uint32_t* P, uint32_t n, const uint2* rbw, const uint32_t* rid)
+{
+    const uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) P[v] = expand_root(rbw, rid, P[v]);
+}
+
+// per-block root counts of the rank words (kFTile words per block)
+__global__ void __launch_bounds__(kBlock) k_rank_count(const uint2* __restrict__ rbw, uint32_t nw, uint32_t* bcnt)
+{
+    uint32_t tot;
+    const uint64_t base = (uint64_t)blockIdx.x * kFTile + (uint64_t)threadIdx.x * kFItems;
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < kFItems; ++j)
+        if (base + j < nw) c += __popc(rbw[base + j].x);
+    block_excl_scan(c, &tot);
+    if (threadIdx.x == 0) bcnt[blockIdx.x] = tot;
+}
+
+// per-word exclusive prefix, rid[] and C[c] = c.  The block's kFTile words are
+// taken kBlock at a time (one per thread, coalesced), so each round's rid / C
+// writes form one contiguous range.
+__global__ void __launch_bounds__(kBlock) k_rank_fill(uint2* rbw, uint32_t nw, const unsigned long long* boff,
+                                                      uint32_t* rid, uint32_t* C)
+{
+    uint32_t tot;
+    uint32_t run = (uint32_t)boff[blockIdx.x];
+    const uint64_t base = (uint64_t)blockIdx.x * kFTile;
+    for (int j = 0; j < kFItems; ++j) {
+        const uint64_t i = base + (uint64_t)j * kBlock + threadIdx.x;
+        const uint32_t bits = i < nw ? rbw[i].x : 0u;
+        uint32_t pref = run + block_excl_scan(__popc(bits), &tot);
+        if (i < nw) rbw[i].y = pref;
+        for (uint32_t b = bits; b; b &= b - 1) {
+            rid[pref] = (uint32_t)(i * 32 + (uint32_t)(__ffs(b) - 1));
+            C[pref] = pref;
+            ++pref;
+        }
+        run += tot;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K4: IdentifyFrequent: the mode of root(s_i) over S samples,
 // s_i = uniform_below(mix(seed, IDENT, i), n), ties to the smaller label
 // (reading R9).  One CTA: each thread finds the roots of its samples and
@@ -448,7 +757,7 @@ constexpr int kIdTable = 4096;                       // 2 * max samples (2048)
 
 __global__ void __launch_bounds__(1024) k_identify(const uint32_t* P, uint32_t n, uint64_t seed,
                                                    uint32_t samples, const uint32_t* force, Ctl* ctl,
-                                                   uint32_t* lmax_out)
+                                                   uint32_t* lmax_out, const uint2* rbw, const uint32_t* rid)
 {
     __shared__ uint32_t keys[kIdTable];
     __shared__ uint32_t cnts[kIdTable];
@@ -468,7 +777,8 @@ __global__ void __launch_bounds__(1024) k_identify(const uint32_t* P, uint32_t n
     __syncthreads();
     for (int i = t; i < (int)samples; i += blockDim.x) {
         const uint32_t sv = uniform_below(mix(seed, IDENT_STREAM, (uint64_t)i), n);
-        const uint32_t lab = root_plain(P, sv);      // no hook runs concurrently
+        // no hook runs concurrently; contracted: P[sv] is sv's F0 root
+        const uint32_t lab = rbw ? expand_root(rbw, rid, P[sv]) : root_plain(P, sv);
         uint32_t h = (lab * 0x9E3779B1u) >> 20;      // 12-bit multiplicative hash
         while (true) {
             const uint32_t old = atomicCAS(&keys[h], kSentinel, lab);
@@ -527,9 +837,10 @@ __global__ void __launch_bounds__(1024) k_identify(const uint32_t* P, uint32_t n
 // root is skipped without a link), longer lists are queued for k_finish_big
 // (one CTA per vertex).  Keeping the edge work out of the scan keeps the scan
 // a lean streaming kernel (no spills, full occupancy).
-template <bool VEC, bool CNT>
+template <bool VEC, bool CNT, bool CONTRACT>
 __global__ void __launch_bounds__(kBlock, CC_FINISH_MINB) k_finish(uint32_t* P, const uint32_t* __restrict__ bm, uint32_t n,
-                                                   Ctl* ctl, bool no_skip, uint32_t* cq, cc_counters* cnt)
+                                                   Ctl* ctl, bool no_skip, uint32_t* cq, cc_counters* cnt,
+                                                   const uint2* __restrict__ rbw, const uint32_t* __restrict__ rid)
 {
     const uint32_t lmax = no_skip ? kSentinel : ctl->lmax;
     const uint64_t base = (uint64_t)blockIdx.x * kCTile;
@@ -549,8 +860,22 @@ __global__ void __launch_bounds__(kBlock, CC_FINISH_MINB) k_finish(uint32_t* P, 
     }
     const uint32_t w0 = i0 < n ? bm[i0 >> 5] : 0u;
     const uint32_t w1 = i1 < n ? bm[i1 >> 5] : 0u;
-    uint32_t writes = 0;
-    const uint32_t gathers = roots8(P, vv, pp, rr, lmax);   // L_max stays a root: no hook runs here
+    uint32_t writes = 0, gathers = 0;
+    if constexpr (CONTRACT) {
+        // P[v] is v's F0 root: its sampled root is one rank-word + one rid
+        // lookup (L2-resident), no gather into P
+        uint2 w[kCV];
+#pragma unroll
+        for (int s = 0; s < kCV; ++s) w[s] = (uint64_t)((s < 4 ? i0 : i1) + (s & 3)) < n ? rbw[pp[s] >> 5] : make_uint2(0u, 0u);
+#pragma unroll
+        for (int s = 0; s < kCV; ++s) {
+            const bool cr = (w[s].x >> (pp[s] & 31)) & 1u;
+            rr[s] = cr ? rid[cid_of(w[s], pp[s])] : pp[s];
+            gathers += cr;
+        }
+    } else {
+        gathers = roots8(P, vv, pp, rr, lmax);               // L_max stays a root: no hook runs here
+    }
 #pragma unroll
     for (int s = 0; s < kCV; ++s) writes += rr[s] != pp[s];
     if (full) {                                          // H3 compress writes
@@ -901,38 +1226,6 @@ static cc_status sv_finish(const int64_t* off, const uint32_t* adj, uint32_t* P,
 // ---------------------------------------------------------------------------
 // K7: Filter -- stable compaction of the non-sentinel forest slots.
 
-__device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* total)
-{
-    constexpr int NW = kBlock / 32;
-    __shared__ uint32_t ws[NW];
-    __shared__ uint32_t tot;
-    const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    uint32_t incl = x;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= (unsigned)o) incl += t;
-    }
-    if (lane == 31) ws[w] = incl;
-    __syncthreads();
-    if (w == 0) {
-        const uint32_t sv = lane < (unsigned)NW ? ws[lane] : 0u;
-        uint32_t si = sv;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t t = __shfl_up_sync(0xffffffffu, si, o);
-            if (lane >= (unsigned)o) si += t;
-        }
-        if (lane < (unsigned)NW) ws[lane] = si - sv;
-        if (lane == (unsigned)NW - 1) tot = si;
-    }
-    __syncthreads();
-    const uint32_t r = ws[w] + incl - x;
-    *total = tot;
-    __syncthreads();
-    return r;
-}
-
 __global__ void __launch_bounds__(kBlock) k_forest_count(const uint2* F, uint32_t n, uint32_t* block_cnt)
 {
     uint32_t tot;
@@ -1032,7 +1325,11 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
     const uint32_t skip_prefix = VAR == 0 ? k : VAR == 1 ? std::min<uint32_t>(k, 1u) : 0u;
     const uint32_t full_deg = degskip ? skip_prefix : 0u;
     const bool no_skip = (o.flags & CC_FLAG_NO_SKIP) != 0;
+    // contracted k-out link (opt-in; needs the symmetric-graph precondition of the skip)
+    const bool contract = k > 0 && !no_skip && (o.flags & CC_FLAG_CONTRACT);
     const int sms = num_sms();
+    const uint32_t nw = (uint32_t)(((uint64_t)n + 31) / 32);
+    const uint32_t nrb = (uint32_t)(((uint64_t)nw + kFTile - 1) / kFTile);
 
     // afforest: at most sum_u min(k, deg u) <= m pending edges; hybrid/pure: k per non-isolated vertex
     const uint64_t pend_cap = std::max<uint64_t>(
@@ -1049,6 +1346,12 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
     uint2* F = nullptr;
     uint32_t* fcnt = nullptr;
     unsigned long long* foff = nullptr;
+    uint2* rbw = nullptr;                 // contracted link: rank words, compact parents, compact -> id
+    uint32_t* Cc = nullptr;
+    uint32_t* rid = nullptr;
+    uint32_t* rcnt = nullptr;
+    unsigned long long* roff = nullptr;
+    int64_t* Rtot = nullptr;
     cudaEvent_t ev[5] = {};
     cc_status rc = CC_OK;
 
@@ -1061,6 +1364,12 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
         scratch_free(F, s);
         scratch_free(fcnt, s);
         scratch_free(foff, s);
+        scratch_free(rbw, s);
+        scratch_free(Cc, s);
+        scratch_free(rid, s);
+        scratch_free(rcnt, s);
+        scratch_free(roff, s);
+        scratch_free(Rtot, s);
     };
     auto body = [&]() -> cc_status {
         CC_CUDA_TRY(scratch_alloc((void**)&ctl, sizeof(Ctl), s));
@@ -1073,6 +1382,16 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
             CC_CUDA_TRY(scratch_alloc((void**)&fcnt, sizeof(uint32_t) * nfb, s));
             CC_CUDA_TRY(scratch_alloc((void**)&foff, sizeof(unsigned long long) * nfb, s));
             CC_CUDA_TRY(cudaMemsetAsync(F, 0xFF, sizeof(uint2) * (size_t)n, s));
+        }
+        if (contract) {
+            // R <= number of non-isolated vertices <= min(n, m); sized for the worst case
+            const size_t rcap = std::max<size_t>(1, std::min<uint64_t>(n, (uint64_t)m));
+            CC_CUDA_TRY(scratch_alloc((void**)&rbw, sizeof(uint2) * nw, s));
+            CC_CUDA_TRY(scratch_alloc((void**)&Cc, sizeof(uint32_t) * rcap, s));
+            CC_CUDA_TRY(scratch_alloc((void**)&rid, sizeof(uint32_t) * rcap, s));
+            CC_CUDA_TRY(scratch_alloc((void**)&rcnt, sizeof(uint32_t) * nrb, s));
+            CC_CUDA_TRY(scratch_alloc((void**)&roff, sizeof(unsigned long long) * nrb, s));
+            CC_CUDA_TRY(scratch_alloc((void**)&Rtot, sizeof(int64_t), s));
         }
         CC_CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(Ctl), s));
         if (o.timings)
@@ -1088,15 +1407,27 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
         // zero-copy); from HBM two 4-byte loads of the same sector are cheaper
         if (aligned16(adj) && mem_kind(adj, nullptr) == MEM_PINNED)
             k_sample_init<VAR, SF, true><<<nblk0, kBlock, 0, s>>>(off, adj, n, m, k, o.seed, full_deg, P, F, pend,
-                                                                    bm, ctl, o.counters);
+                                                                    bm, rbw, ctl, o.counters);
         else
             k_sample_init<VAR, SF, false><<<nblk0, kBlock, 0, s>>>(off, adj, n, m, k, o.seed, full_deg, P, F, pend,
-                                                                     bm, ctl, o.counters);
+                                                                     bm, rbw, ctl, o.counters);
         CC_LAUNCH_CHECK("k_sample_init");
         CC_CUDA_TRY(mark(CC_MARK_INIT));
-        // shorten the first-round chains before the CAS links when they are long
-        // (grid-like inputs); k_probe decides on the device unless a flag forces it
-        if (k > 0 && !(o.flags & CC_FLAG_NO_MIDCOMPRESS)) {
+        if (contract) {
+            // rank words -> compact ids (rid, C[c] = c), then P[u] = root_F0(u)
+            k_rank_count<<<nrb, kBlock, 0, s>>>(rbw, nw, rcnt);
+            CC_LAUNCH_CHECK("k_rank_count");
+            k_forest_scan<<<1, kBlock, 0, s>>>(rcnt, nrb, roff, Rtot);
+            CC_LAUNCH_CHECK("k_forest_scan(rank)");
+            k_rank_fill<<<nrb, kBlock, 0, s>>>(rbw, nw, roff, rid, Cc);
+            CC_LAUNCH_CHECK("k_rank_fill");
+            if (o.counters)
+                CC_CUDA_TRY(cudaMemcpyAsync(&o.counters->contract_roots, Rtot, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+            cc_status r = launch_compress(P, n, nullptr, nullptr, s, "k_compress(F0)");
+            if (r) return r;
+        } else if (k > 0 && !(o.flags & CC_FLAG_NO_MIDCOMPRESS)) {
+            // shorten the first-round chains before the CAS links when they are long
+            // (grid-like inputs); k_probe decides on the device unless a flag forces it
             const bool force = (o.flags & CC_FLAG_MIDCOMPRESS) != 0;
             if (!force) {
                 k_probe<<<1, 1024, 0, s>>>(P, n, o.seed, ctl, o.counters);
@@ -1107,7 +1438,15 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
         }
         CC_CUDA_TRY(mark(CC_MARK_MIDCOMPRESS));
         // H2: the remaining sampled edges
-        if (k > 0) {
+        if (contract) {
+            k_link_contract<MODE, SF><<<sms * 8, kBlock, 0, s>>>(P, pend, ctl, rbw, Cc, rid, F, o.counters);
+            CC_LAUNCH_CHECK("k_link_contract");
+            k_contract_final<<<sms * 8, kBlock, 0, s>>>(Cc, rid, Rtot);
+            CC_LAUNCH_CHECK("k_contract_final");
+        } else if (k > 0 && MODE == 0 && !(o.flags & CC_FLAG_NO_REFILL)) {
+            k_link_refill<SF><<<sms * 8, kBlock, 0, s>>>(P, pend, ctl, F, o.counters);
+            CC_LAUNCH_CHECK("k_link_refill");
+        } else if (k > 0) {
             k_link_pending<MODE, SF><<<sms * 8, kBlock, 0, s>>>(P, pend, ctl, F, o.counters);
             CC_LAUNCH_CHECK("k_link_pending");
         }
@@ -1115,23 +1454,37 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
         // H3 as its own pass only when the caller asks for the sampled labels
         // (otherwise it is fused into k_finish)
         if (o.sampled_out) {
-            cc_status r = launch_compress(P, n, nullptr, nullptr, s, "k_compress(H3)");
-            if (r) return r;
+            if (contract) {
+                k_expand<<<(unsigned)(((uint64_t)n + kBlock - 1) / kBlock), kBlock, 0, s>>>(P, n, rbw, rid);
+                CC_LAUNCH_CHECK("k_expand");
+            } else {
+                cc_status r = launch_compress(P, n, nullptr, nullptr, s, "k_compress(H3)");
+                if (r) return r;
+            }
             CC_CUDA_TRY(cudaMemcpyAsync(o.sampled_out, P, sizeof(uint32_t) * (size_t)n, cudaMemcpyDeviceToDevice, s));
         }
         CC_CUDA_TRY(mark(CC_MARK_SAMPLED));
         if (o.timings) CC_CUDA_TRY(cudaEventRecord(ev[1], s));
         // H4 (roots of the sampled forest; identical before or after H3)
-        k_identify<<<1, 1024, 0, s>>>(P, n, o.seed, o.samples, o.lmax_force, ctl, o.lmax_out);
+        k_identify<<<1, 1024, 0, s>>>(P, n, o.seed, o.samples, o.lmax_force, ctl, o.lmax_out, rbw, rid);
         CC_LAUNCH_CHECK("k_identify");
         CC_CUDA_TRY(mark(CC_MARK_IDENTIFY));
         if (o.timings) CC_CUDA_TRY(cudaEventRecord(ev[2], s));
         // H3 + H5
         {
             const unsigned nb = (unsigned)(((uint64_t)n + kCTile - 1) / kCTile);
-            if (aligned16(P) && o.counters) k_finish<true, true><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters);
-            else if (aligned16(P)) k_finish<true, false><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, nullptr);
-            else k_finish<false, true><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters);
+            if (contract && aligned16(P) && o.counters)
+                k_finish<true, true, true><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters, rbw, rid);
+            else if (contract && aligned16(P))
+                k_finish<true, false, true><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, nullptr, rbw, rid);
+            else if (contract)
+                k_finish<false, true, true><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters, rbw, rid);
+            else if (aligned16(P) && o.counters)
+                k_finish<true, true, false><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters, nullptr, nullptr);
+            else if (aligned16(P))
+                k_finish<true, false, false><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, nullptr, nullptr, nullptr);
+            else
+                k_finish<false, true, false><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters, nullptr, nullptr);
             CC_LAUNCH_CHECK("k_finish");
         }
         CC_CUDA_TRY(mark(CC_MARK_FINISH));

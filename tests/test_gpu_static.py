@@ -41,6 +41,12 @@ OPTION_GRID = [
     dict(k=0, variant="afforest", flags=cc.FLAG_FINISH_SV),
     dict(k=1, variant="hybrid", flags=cc.FLAG_FINISH_SV | cc.FLAG_NO_SKIP, seed=3),
     dict(k=1, variant="pure", flags=cc.FLAG_UF_ASYNC, seed=2),
+    # the contracted k-out link and the round-1 (no lane refill) link kernel
+    dict(k=2, variant="afforest", flags=cc.FLAG_CONTRACT),
+    dict(k=3, variant="hybrid", flags=cc.FLAG_CONTRACT | cc.FLAG_HALVE, seed=5),
+    dict(k=2, variant="pure", flags=cc.FLAG_CONTRACT | cc.FLAG_UF_ASYNC, seed=9),
+    dict(k=2, variant="afforest", flags=cc.FLAG_NO_REFILL),
+    dict(k=3, variant="hybrid", flags=cc.FLAG_NO_REFILL, seed=3),
 ]
 
 
@@ -93,13 +99,14 @@ def test_sampled_labels_are_cc_of_the_sampled_edges():
     graphs += [(o, a) for _, o, a in fixtures()]
     for off, adj in graphs:
         n = off.size - 1
-        for k, variant, seed in [(1, "afforest", 0), (2, "afforest", 0), (3, "afforest", 0), (2, "hybrid", 5),
-                                 (4, "hybrid", 99), (1, "pure", 4), (3, "pure", 8)]:
+        for (k, variant, seed), fl in itertools.product(
+                [(1, "afforest", 0), (2, "afforest", 0), (3, "afforest", 0), (2, "hybrid", 5),
+                 (4, "hybrid", 99), (1, "pure", 4), (3, "pure", 8)], [0, cc.FLAG_CONTRACT, cc.FLAG_NO_REFILL]):
             d_off, d_adj = to_dev(off, adj)
             sampled = torch.empty(n, dtype=torch.int32, device="cuda")
             lmax = torch.empty(1, dtype=torch.int32, device="cuda")
             lab = pkg.connected_components(d_off, d_adj, k=k, variant=variant, seed=seed, sampled_out=sampled,
-                                           lmax_out=lmax)
+                                           lmax_out=lmax, flags=fl)
             E = oracle.kout_sample_edges(off, adj, k, variant, seed)
             o2, a2 = oracle.csr_from_pairs(n, E)
             want_s = oracle.cc_bfs(o2, a2)
@@ -194,7 +201,11 @@ def test_empty_and_degenerate_abi():
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("opt", [OPTION_GRID[0], OPTION_GRID[1], OPTION_GRID[4], OPTION_GRID[6], OPTION_GRID[7],
                                  dict(k=2, variant="afforest", flags=cc.FLAG_FINISH_SV),
-                                 dict(k=0, variant="afforest", flags=cc.FLAG_FINISH_SV)],
+                                 dict(k=0, variant="afforest", flags=cc.FLAG_FINISH_SV),
+                                 dict(k=2, variant="afforest", flags=cc.FLAG_CONTRACT),
+                                 dict(k=3, variant="pure", flags=cc.FLAG_CONTRACT | cc.FLAG_HALVE, seed=4),
+                                 dict(k=2, variant="afforest", flags=cc.FLAG_NO_REFILL),
+                                 dict(k=1, variant="hybrid", flags=0, seed=6)],
                          ids=lambda o: f"k{o['k']}-{o['variant']}-f{o['flags']}")
 def test_spanning_forest_valid(opt):
     for name, off, adj in small_graphs():
@@ -230,7 +241,7 @@ def test_repeat_stress_random_options():
     rng = np.random.default_rng(1)
     d_off, d_adj = to_dev(off, adj)
     flags_pool = [0, cc.FLAG_HALVE, cc.FLAG_UF_ASYNC, cc.FLAG_NO_SKIP, cc.FLAG_NO_MIDCOMPRESS, cc.FLAG_NO_DEGSKIP,
-                  cc.FLAG_MIDCOMPRESS, cc.FLAG_FINISH_SV]
+                  cc.FLAG_MIDCOMPRESS, cc.FLAG_FINISH_SV, cc.FLAG_CONTRACT, cc.FLAG_NO_REFILL]
     for it in range(200):
         k = int(rng.integers(0, 5))
         variant = ["afforest", "hybrid", "pure"][int(rng.integers(0, 3))]
@@ -253,6 +264,13 @@ def test_counters_and_timings():
     assert c["pending_links"] == int(np.minimum(deg, 2).sum()) - int(
         sum(1 for v in range(n) if deg[v] > 0 and adj[off[v]] < v))
     assert c["finish_vertices"] <= c["worklist"] == int((deg > 2).sum())
+    assert c["contract_roots"] == 0
+    # contracted link: one compact slot per non-isolated root of the round-0 forest
+    ctr.zero_()
+    cc.cc_labels(d_off, d_adj, n, adj.size, lab, cc.make_opts(counters=ctr, flags=cc.FLAG_CONTRACT))
+    c = dict(zip(cc.COUNTER_FIELDS, ctr.cpu().tolist()))
+    assert c["contract_roots"] == int(sum(1 for v in range(n) if deg[v] > 0 and adj[off[v]] >= v))
+    assert np.array_equal(u32(lab), oracle.cc_bfs(off, adj))
     assert t.total_ms > 0
     assert np.array_equal(u32(lab), oracle.cc_bfs(off, adj))
 
