@@ -24,7 +24,7 @@ import numpy as np
 M64 = (1 << 64) - 1
 GOLD = 0x9E3779B97F4A7C15
 
-ER_STREAM, GRID_STREAM, RMAT_STREAM, PERM_STREAM, QUERY_STREAM = 1, 2, 3, 4, 5
+ER_STREAM, GRID_STREAM, RMAT_STREAM, PERM_STREAM, QUERY_STREAM, WEIGHT_STREAM = 1, 2, 3, 4, 5, 6
 
 # fixed-point thresholds: floor(p * 2^32)
 P55 = 2362232012            # Bernoulli(0.55) for the grid
@@ -169,6 +169,56 @@ def incr_batch(seed: int, scale: int, b: int, n_ins: int, n_q: int):
     ins = np.stack([u, v], axis=1).astype(np.uint32)
     qs = np.stack([a, c], axis=1).astype(np.uint32)
     return ins, qs
+
+
+# ---------------------------------------------------------------------------
+# Edge weights for the AMSF workload (NEXT-4): the paper adds "random weights
+# drawn from an exponential distribution with a constant mean";
+# mean 1 here.  w(u,v) = -ln(U), U = (k + 1/2) 2^-52, k = mix(seed, WEIGHT,
+# min(u,v) 2^32 + max(u,v)) >> 12, so both directions of an edge carry the same
+# weight and 0 < U < 1 (w > 0).  ln is evaluated with IEEE +,-,*,/ only, in a
+# fixed order (no fused multiply-add), so that the CUDA twin (csrc/gen.cu)
+# produces bit-identical float32 weights.
+LN2 = 0.6931471805599453
+LN_TERMS = 10                     # atanh series: t^(2k) / (2k+1), k = 0..LN_TERMS
+
+
+def _atanh2(t):
+    """2 atanh(t) = 2t sum_k t^(2k)/(2k+1) for 0 <= t <= 1/3 (error < 1e-12)."""
+    t2 = t * t
+    p = np.full_like(t, 1.0 / (2 * LN_TERMS + 1))
+    for k in range(LN_TERMS - 1, -1, -1):
+        p = p * t2
+        p = p + 1.0 / (2 * k + 1)
+    return (2.0 * t) * p
+
+
+def neg_ln_fixed(x) -> np.ndarray:
+    """-ln(x) for float64 x in (0, 1).  x < 1/2: x = m 2^e, m in [1, 2),
+    -ln x = -(e ln2 + 2 atanh((m-1)/(m+1))); x >= 1/2: d = 1 - x (exact),
+    -ln x = 2 atanh(d / (2 - d)) -- no cancellation near x = 1, so the result
+    is > 0 for every x < 1."""
+    x = np.asarray(x, dtype=np.float64)
+    bits = x.view(np.uint64)
+    e = ((bits >> np.uint64(52)) & np.uint64(0x7FF)).astype(np.int64) - 1023
+    m = ((bits & np.uint64(0x000FFFFFFFFFFFFF)) | np.uint64(1023 << 52)).view(np.float64)
+    lo = -(e.astype(np.float64) * LN2 + _atanh2((m - 1.0) / (m + 1.0)))
+    d = 1.0 - x
+    hi = _atanh2(d / (2.0 - d))
+    return np.where(x < 0.5, lo, hi)
+
+
+def exp_weights(off, adj, seed: int) -> np.ndarray:
+    """float32 weight of every adjacency entry (symmetric: w(u,v) == w(v,u))."""
+    off = np.asarray(off, dtype=np.int64)
+    adj = np.asarray(adj, dtype=np.uint32)
+    n = off.size - 1
+    src = np.repeat(np.arange(n, dtype=np.uint64), np.diff(off))
+    dst = adj.astype(np.uint64)
+    key = (np.minimum(src, dst) << np.uint64(32)) | np.maximum(src, dst)
+    k = mix(seed, WEIGHT_STREAM, key) >> np.uint64(12)
+    u = (k.astype(np.float64) + 0.5) * (2.0 ** -52)
+    return neg_ln_fixed(u).astype(np.float32)
 
 
 def validate_csr(off, adj, n: int | None = None) -> None:

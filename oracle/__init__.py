@@ -23,6 +23,12 @@ Contents (each cites the PAPER.md passage it follows):
   the most frequent label among S seeded samples, ties to the smaller label
   (reading R9).
 * ``canon`` -- map every label class to its minimum member (reading R13).
+* ``kruskal`` -- exact minimum spanning forest W(F_OPT), from
+  ``oracle.c``.
+* ``amsf`` -- the folklore AMSF algorithm step by step: W_min,
+  (1+eps)-buckets (reading R25), per-bucket spanning forests over the
+  labeling, from ``oracle.c``; ``amsf_bounds`` / ``amsf_bucket`` restate the
+  bucket rule in numpy (same fp64 product chain) for checking a forest.
 
 Random draws the method makes (hybrid picks, IdentifyFrequent samples) use the
 counter-based generator of reading R7/R9, re-implemented here independently of
@@ -65,7 +71,11 @@ def _load():
         lib.oracle_forest_check.argtypes = [ctypes.c_uint32, P, P, ctypes.c_uint64, P, ctypes.c_int64,
                                             ctypes.POINTER(ctypes.c_int64)]
         lib.oracle_incr_run.argtypes = [ctypes.c_uint32, ctypes.c_int64, P, P, P, P, P, P]
-        for f in (lib.oracle_cc_bfs, lib.oracle_cc_dsu, lib.oracle_forest_check, lib.oracle_incr_run):
+        D, I64P = ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)
+        lib.oracle_kruskal.argtypes = [ctypes.c_uint32, P, P, P, D, P, P, I64P]
+        lib.oracle_amsf.argtypes = [ctypes.c_uint32, P, P, P, ctypes.c_double, D, P, P, P, I64P, I64P]
+        for f in (lib.oracle_cc_bfs, lib.oracle_cc_dsu, lib.oracle_forest_check, lib.oracle_incr_run,
+                  lib.oracle_kruskal, lib.oracle_amsf):
             f.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -241,3 +251,68 @@ def canon(labels) -> np.ndarray:
     mn = np.full(int(labels.max()) + 1, np.iinfo(np.int64).max, dtype=np.int64)
     np.minimum.at(mn, labels, np.arange(n, dtype=np.int64))
     return mn[labels].astype(np.uint32)
+
+
+# ---------------------------------------------------------------------------
+# Minimum spanning forests: exact (Kruskal) and the AMSF folklore algorithm.
+# ---------------------------------------------------------------------------
+def _weights(off, w):
+    w = np.ascontiguousarray(w, dtype=np.float32)
+    if w.size == 0:
+        w = np.zeros(1, dtype=np.float32)
+    return w
+
+
+def kruskal(off, adj, w):
+    """Exact MSF: (total weight fp64, pairs (k,2) uint32, weights (k,) f32)."""
+    off, adj = _csr(off, adj)
+    n = off.size - 1
+    w = _weights(off, w)
+    F = np.zeros(2 * max(n, 1), dtype=np.uint32)
+    Fw = np.zeros(max(n, 1), dtype=np.float32)
+    tot = ctypes.c_double()
+    nf = ctypes.c_int64()
+    rc = _load().oracle_kruskal(n, _ptr(off), _ptr(adj), _ptr(w), ctypes.byref(tot), _ptr(F), _ptr(Fw),
+                                ctypes.byref(nf))
+    if rc:
+        raise ValueError(f"oracle_kruskal failed: {rc}")
+    k = nf.value
+    return tot.value, F[:2 * k].reshape(-1, 2), Fw[:k]
+
+
+def amsf(off, adj, w, eps: float):
+    """AMSF folklore algorithm.  Returns a dict with the forest
+    pairs, their weights and bucket indices (in the order added), the fp64
+    total and the bucket count."""
+    off, adj = _csr(off, adj)
+    n = off.size - 1
+    w = _weights(off, w)
+    F = np.zeros(2 * max(n, 1), dtype=np.uint32)
+    Fw = np.zeros(max(n, 1), dtype=np.float32)
+    Fb = np.zeros(max(n, 1), dtype=np.int32)
+    tot = ctypes.c_double()
+    nf = ctypes.c_int64()
+    nb = ctypes.c_int64()
+    rc = _load().oracle_amsf(n, _ptr(off), _ptr(adj), _ptr(w), float(eps), ctypes.byref(tot), _ptr(F), _ptr(Fw),
+                             _ptr(Fb), ctypes.byref(nf), ctypes.byref(nb))
+    if rc:
+        raise ValueError(f"oracle_amsf failed: {rc}")
+    k = nf.value
+    return {"total": tot.value, "pairs": F[:2 * k].reshape(-1, 2), "weights": Fw[:k], "buckets": Fb[:k],
+            "nbuckets": nb.value}
+
+
+def amsf_bounds(wmin: float, wmax: float, eps: float) -> np.ndarray:
+    """Bucket boundaries b_0 = W_min, b_(i+1) = b_i (1+eps) in fp64 (reading R25),
+    up to the first one above W_max."""
+    g = 1.0 + float(eps)
+    b = [float(np.float32(wmin))]
+    while b[-1] * g <= float(np.float32(wmax)):
+        b.append(b[-1] * g)
+    b.append(b[-1] * g)
+    return np.array(b, dtype=np.float64)
+
+
+def amsf_bucket(w, bounds: np.ndarray) -> np.ndarray:
+    """Bucket index i with b_i <= w < b_(i+1) of float32 weights w."""
+    return (np.searchsorted(bounds, np.asarray(w, dtype=np.float32).astype(np.float64), side="right") - 1).astype(np.int64)

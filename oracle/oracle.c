@@ -34,6 +34,20 @@
  *                    phase-concurrent order; reading R15):
  *                    per batch, apply all inserts to a sequential union-find,
  *                    then answer every query as find(a) == find(b).
+ *   oracle_kruskal   exact minimum spanning forest (the reference point of the
+ *                    AMSF definition: W(F_OPT) of "any spanning
+ *                    forest of G of minimum weight"): Kruskal's algorithm --
+ *                    every undirected edge once, sorted by (w, u, v), added
+ *                    unless it closes a cycle (sequential union-find).
+ *   oracle_amsf      the folklore AMSF algorithm, step by step in the paper's
+ *                    order: W_min = min w(e); bucket i holds the
+ *                    edges with W_min(1+eps)^i <= w < W_min(1+eps)^(i+1)
+ *                    (boundaries b_0 = W_min, b_(i+1) = b_i * (1+eps) in fp64,
+ *                    DESIGN.md reading R25); buckets from light to heavy; in
+ *                    each bucket drop the edges whose endpoints are already
+ *                    connected ("self-loops" of the labeling C) and add the
+ *                    rest to a spanning forest F_i, updating C; F = U F_i.
+ *                    The edges of a bucket are taken in CSR order (u < v).
  *
  * Pins (tests/test_oracle.py): exhaustive brute-force reachability for every
  * labelled graph on n <= 5 vertices, Warshall closure on random graphs up to
@@ -206,5 +220,137 @@ int oracle_incr_run(uint32_t n, int64_t nb, const int64_t* ins_cnt, const uint32
     }
     free(parent);
     free(size);
+    return 0;
+}
+
+/* ---- exact minimum spanning forest: Kruskal ------------------ */
+typedef struct { float w; uint32_t u, v; } wedge;
+
+static int wedge_cmp(const void* a, const void* b)
+{
+    const wedge* x = (const wedge*)a;
+    const wedge* y = (const wedge*)b;
+    if (x->w != y->w) return x->w < y->w ? -1 : 1;
+    if (x->u != y->u) return x->u < y->u ? -1 : 1;
+    if (x->v != y->v) return x->v < y->v ? -1 : 1;
+    return 0;
+}
+
+/* Undirected edges of a symmetric CSR (u < v), with the weight stored at u's
+ * entry.  Returns the count, or -1 on a bad id / allocation failure. */
+static int64_t collect_edges(uint32_t n, const int64_t* off, const uint32_t* adj, const float* w, wedge** out)
+{
+    int64_t ne = 0;
+    for (uint32_t u = 0; u < n; ++u)
+        for (int64_t e = off[u]; e < off[u + 1]; ++e) {
+            if (adj[e] >= n) return -1;
+            if (adj[e] > u) ++ne;
+        }
+    wedge* E = (wedge*)malloc((size_t)(ne ? ne : 1) * sizeof(wedge));
+    if (!E) return -1;
+    int64_t k = 0;
+    for (uint32_t u = 0; u < n; ++u)
+        for (int64_t e = off[u]; e < off[u + 1]; ++e)
+            if (adj[e] > u) { E[k].w = w[e]; E[k].u = u; E[k].v = adj[e]; ++k; }
+    *out = E;
+    return ne;
+}
+
+/* F (out, 2*(n-1) uint32) receives the forest pairs in the order they were
+ * added, Fw (out, n-1) their weights; *nf the count, *total the weight sum
+ * accumulated in fp64 in that order. */
+int oracle_kruskal(uint32_t n, const int64_t* off, const uint32_t* adj, const float* w, double* total,
+                   uint32_t* F, float* Fw, int64_t* nf)
+{
+    *total = 0.0;
+    *nf = 0;
+    if (n == 0) return 0;
+    wedge* E = NULL;
+    int64_t ne = collect_edges(n, off, adj, w, &E);
+    if (ne < 0) return -1;
+    qsort(E, (size_t)ne, sizeof(wedge), wedge_cmp);
+    uint32_t* parent = (uint32_t*)malloc((size_t)n * sizeof(uint32_t));
+    uint32_t* size = (uint32_t*)malloc((size_t)n * sizeof(uint32_t));
+    if (!parent || !size) { free(parent); free(size); free(E); return -3; }
+    for (uint32_t v = 0; v < n; ++v) { parent[v] = v; size[v] = 1; }
+    for (int64_t i = 0; i < ne; ++i) {
+        if (dsu_find(parent, E[i].u) == dsu_find(parent, E[i].v)) continue;
+        dsu_union(parent, size, E[i].u, E[i].v);
+        F[2 * *nf] = E[i].u;
+        F[2 * *nf + 1] = E[i].v;
+        Fw[*nf] = E[i].w;
+        *total += (double)E[i].w;
+        ++*nf;
+    }
+    free(parent);
+    free(size);
+    free(E);
+    return 0;
+}
+
+/* ---- AMSF, the folklore algorithm of P:1797-1812 --------------------------- */
+/* F / Fw / *nf / *total as oracle_kruskal; Fb (out, n-1 int32) the bucket
+ * index of each forest edge; *nbuckets the number of buckets up to W_max.
+ * Returns -2 for a non-positive weight or eps. */
+int oracle_amsf(uint32_t n, const int64_t* off, const uint32_t* adj, const float* w, double eps, double* total,
+                uint32_t* F, float* Fw, int32_t* Fb, int64_t* nf, int64_t* nbuckets)
+{
+    *total = 0.0;
+    *nf = 0;
+    *nbuckets = 0;
+    if (!(eps > 0.0)) return -2;
+    if (n == 0) return 0;
+    wedge* E = NULL;
+    int64_t ne = collect_edges(n, off, adj, w, &E);
+    if (ne < 0) return -1;
+    if (ne == 0) { free(E); return 0; }
+    /* W_min and the boundaries b_i = W_min (1+eps)^i (reading R25) */
+    float wmin = E[0].w, wmax = E[0].w;
+    for (int64_t i = 0; i < ne; ++i) {
+        if (!(E[i].w > 0.0f)) { free(E); return -2; }
+        if (E[i].w < wmin) wmin = E[i].w;
+        if (E[i].w > wmax) wmax = E[i].w;
+    }
+    const double g = 1.0 + eps;
+    int64_t nb = 1;
+    double bi = (double)wmin;
+    while (bi * g <= (double)wmax) { bi = bi * g; ++nb; }      /* b_(nb-1) <= W_max < b_nb */
+    double* b = (double*)malloc((size_t)(nb + 1) * sizeof(double));
+    int32_t* bucket = (int32_t*)malloc((size_t)ne * sizeof(int32_t));
+    uint32_t* parent = (uint32_t*)malloc((size_t)n * sizeof(uint32_t));
+    uint32_t* size = (uint32_t*)malloc((size_t)n * sizeof(uint32_t));
+    if (!b || !bucket || !parent || !size) { free(b); free(bucket); free(parent); free(size); free(E); return -3; }
+    b[0] = (double)wmin;
+    for (int64_t i = 1; i <= nb; ++i) b[i] = b[i - 1] * g;
+    /* bucket of each edge: the i with b_i <= w < b_(i+1) (binary search) */
+    for (int64_t e = 0; e < ne; ++e) {
+        const double x = (double)E[e].w;
+        int64_t lo = 0, hi = nb;                                  /* b_lo <= x < b_hi */
+        while (hi - lo > 1) {
+            int64_t mid = lo + (hi - lo) / 2;
+            if (b[mid] <= x) lo = mid; else hi = mid;
+        }
+        bucket[e] = (int32_t)lo;
+    }
+    for (uint32_t v = 0; v < n; ++v) { parent[v] = v; size[v] = 1; }
+    /* buckets from light to heavy; within one, CSR order (u < v) */
+    for (int64_t i = 0; i < nb; ++i)
+        for (int64_t e = 0; e < ne; ++e) {
+            if (bucket[e] != i) continue;
+            if (dsu_find(parent, E[e].u) == dsu_find(parent, E[e].v)) continue;   /* a self-loop of C */
+            dsu_union(parent, size, E[e].u, E[e].v);
+            F[2 * *nf] = E[e].u;
+            F[2 * *nf + 1] = E[e].v;
+            Fw[*nf] = E[e].w;
+            Fb[*nf] = (int32_t)i;
+            *total += (double)E[e].w;
+            ++*nf;
+        }
+    *nbuckets = nb;
+    free(b);
+    free(bucket);
+    free(parent);
+    free(size);
+    free(E);
     return 0;
 }

@@ -127,7 +127,7 @@ __device__ __forceinline__ uint32_t pick4(uint4 w, uint32_t r)
 
 // VAR: 0 = afforest (positions 0..k-1), 1 = hybrid (0, then k-1 uniform picks),
 // 2 = pure (k uniform picks) -- cc.h CC_VARIANT_*.
-template <int VAR, bool SF, bool WIN>
+template <int VAR, bool SF, bool WIN, bool RB>
 __global__ void __launch_bounds__(kBlock, 3) k_sample_init(
     const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, uint32_t n, int64_t m, uint32_t k,
     uint64_t seed, uint32_t full_deg, uint32_t* __restrict__ P, uint2* __restrict__ F,
@@ -190,13 +190,14 @@ __global__ void __launch_bounds__(kBlock, 3) k_sample_init(
         nwl += mark;
         const uint32_t word = __ballot_sync(0xffffffffu, mark);
         if (lane == (unsigned)j) bits = word;
-        // non-isolated root of the round-0 forest F0 (contracted link)
-        const uint32_t rword = __ballot_sync(0xffffffffu, u < n && d[j] > 0 && !(v0[j] < (uint32_t)u));
-        if (lane == (unsigned)j) rbits = rword;
+        if constexpr (RB) {             // non-isolated root of the round-0 forest F0 (contracted link)
+            const uint32_t rword = __ballot_sync(0xffffffffu, u < n && d[j] > 0 && !(v0[j] < (uint32_t)u));
+            if (lane == (unsigned)j) rbits = rword;
+        }
     }
     if (lane < (unsigned)kV && wbase + 32 * lane < n) {
         bm[(wbase >> 5) + lane] = bits;
-        if (rbw) rbw[(wbase >> 5) + lane].x = rbits;
+        if constexpr (RB) rbw[(wbase >> 5) + lane].x = rbits;
     }
 #pragma unroll
     for (int j = 0; j < kV; ++j) {
@@ -1405,12 +1406,19 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
         const uint32_t nblk0 = (uint32_t)(((uint64_t)n + kBlockTile - 1) / kBlockTile);
         // 16-byte list-head windows pay off when adj is read over PCIe (pinned host,
         // zero-copy); from HBM two 4-byte loads of the same sector are cheaper
-        if (aligned16(adj) && mem_kind(adj, nullptr) == MEM_PINNED)
-            k_sample_init<VAR, SF, true><<<nblk0, kBlock, 0, s>>>(off, adj, n, m, k, o.seed, full_deg, P, F, pend,
-                                                                    bm, rbw, ctl, o.counters);
+        const bool win = aligned16(adj) && mem_kind(adj, nullptr) == MEM_PINNED;
+        if (contract && win)
+            k_sample_init<VAR, SF, true, true><<<nblk0, kBlock, 0, s>>>(off, adj, n, m, k, o.seed, full_deg, P, F,
+                                                                          pend, bm, rbw, ctl, o.counters);
+        else if (contract)
+            k_sample_init<VAR, SF, false, true><<<nblk0, kBlock, 0, s>>>(off, adj, n, m, k, o.seed, full_deg, P, F,
+                                                                           pend, bm, rbw, ctl, o.counters);
+        else if (win)
+            k_sample_init<VAR, SF, true, false><<<nblk0, kBlock, 0, s>>>(off, adj, n, m, k, o.seed, full_deg, P, F,
+                                                                           pend, bm, nullptr, ctl, o.counters);
         else
-            k_sample_init<VAR, SF, false><<<nblk0, kBlock, 0, s>>>(off, adj, n, m, k, o.seed, full_deg, P, F, pend,
-                                                                     bm, rbw, ctl, o.counters);
+            k_sample_init<VAR, SF, false, false><<<nblk0, kBlock, 0, s>>>(off, adj, n, m, k, o.seed, full_deg, P, F,
+                                                                            pend, bm, nullptr, ctl, o.counters);
         CC_LAUNCH_CHECK("k_sample_init");
         CC_CUDA_TRY(mark(CC_MARK_INIT));
         if (contract) {
