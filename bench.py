@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--l2-fetch", type=int, default=-1, help="cudaLimitMaxL2FetchGranularity (bytes) or -1")
     p.add_argument("--study", action="store_true", help="NEXT-1 sampling variant x k sweep on C2-C4")
     p.add_argument("--incr-sweep", action="store_true", help="NEXT-2 incremental variants sweep")
+    p.add_argument("--amsf", action="store_true", help="NEXT-4 AMSF-NF-S study on C3/C4 with Exp(1) weights")
+    p.add_argument("--eps", type=float, default=0.25)
     return p.parse_args()
 
 
@@ -714,11 +716,90 @@ def run_incr_sweep(a):
     print(json.dumps({"study": "NEXT-2 incremental variants", **out}), flush=True)
 
 
+def run_amsf(a):
+    """NEXT-4: AMSF-NF-S on C3 / C4 with the seeded
+    Exp(1) weights (the paper's weighted inputs are not here),
+    eps = 0.25.  Variants: NF-S with the per-vertex weight-range index
+    (default), NF-S as stated (AMSF_PLAIN), and both without the L_max skip (NF).
+    Per variant: device time of one cc_amsf call (CUDA events, mean of --steps
+    after --warmup), rounds, active-vertex visits, weights inspected, forest
+    weight; the oracle's AMSF and Kruskal timed on an RMAT-20 sample (1 thread)
+    with W_APX / W_OPT there."""
+    import numpy as np
+    import torch
+
+    import inputs
+    import oracle
+    from inputs import gen
+    from inputs import gpu as ggen
+    from paper_2008_03909_b200 import cc
+    stream = torch.cuda.current_stream()
+    variants = [("nf_s_range", 0), ("nf_s_plain", cc.FLAG_AMSF_PLAIN), ("nf_range", cc.FLAG_NO_SKIP),
+                ("nf_plain", cc.FLAG_AMSF_PLAIN | cc.FLAG_NO_SKIP)]
+    rows = []
+    for cfg in (inputs.C3, inputs.C4):
+        d_off, d_adj = ggen.config_graph(cfg)
+        d_w = ggen.exp_weights(d_off, d_adj, cfg.seed)
+        n, m = d_off.numel() - 1, d_adj.numel()
+        edges = torch.empty((n, 2), dtype=torch.int32, device="cuda")
+        ew = torch.empty(n, dtype=torch.float32, device="cuda")
+        num = torch.zeros(1, dtype=torch.int64, device="cuda")
+        tot = torch.zeros(1, dtype=torch.float64, device="cuda")
+        for name, flags in variants:
+            if cfg is inputs.C4 and flags & cc.FLAG_AMSF_PLAIN and flags & cc.FLAG_NO_SKIP:
+                continue                                   # ~100 full passes over 34 GB: skipped at C4
+            ctr = torch.zeros(len(cc.COUNTER_FIELDS), dtype=torch.int64, device="cuda")
+            cc.cc_amsf(d_off, d_adj, d_w, n, m, a.eps, edges, ew, num, tot, cc.make_opts(flags=flags, counters=ctr),
+                       stream)
+            torch.cuda.synchronize()
+            c = dict(zip(cc.COUNTER_FIELDS, ctr.cpu().tolist()))
+            ts = []
+            for i in range(a.warmup + a.steps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                cc.cc_amsf(d_off, d_adj, d_w, n, m, a.eps, edges, ew, num, tot, cc.make_opts(flags=flags), stream)
+                e1.record(stream)
+                e1.synchronize()
+                if i >= a.warmup:
+                    ts.append(e0.elapsed_time(e1))
+            ms = float(np.mean(ts))
+            # algorithmic bytes: one weight per inspected entry, the endpoint of every
+            # in-bucket entry (<= m), offsets + weight range per visit
+            byts = 4 * c["amsf_edges"] + 4 * m + 24 * c["amsf_visits"]
+            rows.append({"workload": cfg.name, "variant": name, "flags": flags, "eps": a.eps, "ms": round(ms, 3),
+                         "GTEPS": round(m / (ms * 1e-3) / 1e9, 2), "rounds": c["amsf_rounds"],
+                         "visits": c["amsf_visits"], "weights_inspected": c["amsf_edges"],
+                         "inspected_per_entry": round(c["amsf_edges"] / m, 3), "forest_edges": int(num.item()),
+                         "forest_weight": float(tot.item()), "rebuilds": c["amsf_rebuilds"],
+                         "algorithmic_GBps": round(byts / (ms * 1e-3) / 1e9, 1)})
+            print(json.dumps(rows[-1]), file=sys.stderr, flush=True)
+        del d_off, d_adj, d_w, edges, ew
+        torch.cuda.empty_cache()
+    # the oracle on a bounded sample: RMAT-20 (C4 recipe)
+    off, adj = gen.rmat(seed=4, scale=20)
+    w = gen.exp_weights(off, adj, 4)
+    t0 = time.time()
+    r = oracle.amsf(off, adj, w, a.eps)
+    t1 = time.time()
+    wopt = oracle.kruskal(off, adj, w)[0]
+    t2 = time.time()
+    d_off, d_adj = torch.from_numpy(off).cuda(), torch.from_numpy(adj.view(np.int32)).cuda()
+    d_w = torch.from_numpy(w).cuda()
+    E, W, tg = __import__("paper_2008_03909_b200").amsf(d_off, d_adj, d_w, a.eps)
+    sample = {"graph": "RMAT-20 (C4 recipe, seed 4)", "m": int(adj.size), "oracle_amsf_s": round(t1 - t0, 3),
+              "oracle_kruskal_s": round(t2 - t1, 3), "cores": 1, "W_opt": wopt, "W_oracle_amsf": r["total"],
+              "W_gpu_amsf": tg, "gpu_over_opt": round(tg / wopt, 6), "oracle_over_opt": round(r["total"] / wopt, 6),
+              "buckets": r["nbuckets"]}
+    print(json.dumps({"study": "NEXT-4 AMSF-NF-S", "rows": rows, "cpu_sample": sample}), flush=True)
+
+
 def main():
     a = parse()
     rank, ws = dist_setup()
     if a.study:
         run_study(a)
+    elif a.amsf:
+        run_amsf(a)
     elif a.incr_sweep:
         run_incr_sweep(a)
     elif a.impl == "reference":

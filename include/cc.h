@@ -94,6 +94,10 @@ typedef int cc_status;
                                           on C3/C4                               */
 #define CC_FLAG_NO_REFILL   (1u << 11) /* k-out links: one warp step per slowest lane (the
                                           round-1 kernel) instead of lane refill           */
+#define CC_FLAG_AMSF_PLAIN  (1u << 12) /* cc_amsf: inspect every edge of every non-skipped
+                                          vertex in every round, as AMSF-NF-S is stated
+                                          (P:1819-1822), instead of consulting the per-
+                                          vertex [min, max] weight index first          */
 #define CC_FLAG_WAIT_FREE   (1u << 8)  /* cc_incr: the wait-free type (1) setting (P:973-977,
                                           P:2663-2682): a batch's inserts and queries run
                                           concurrently in ONE kernel.  Answers are then
@@ -131,6 +135,11 @@ typedef struct {
     uint64_t sv_rounds;        /* rounds of the Shiloach-Vishkin finish (FINISH_SV)  */
     uint64_t contract_roots;   /* slots of the contracted parent array (non-isolated
                                   roots of the first k-out round's forest F0)        */
+    uint64_t amsf_rounds;      /* cc_amsf: weight buckets processed                    */
+    uint64_t amsf_visits;      /* cc_amsf: active-vertex visits over all rounds        */
+    uint64_t amsf_edges;       /* cc_amsf: adjacency weights inspected over all rounds */
+    uint64_t amsf_hooks;       /* cc_amsf: successful root hooks (= forest edges)      */
+    uint64_t amsf_rebuilds;    /* cc_amsf: rounds whose L_max left the skipped component*/
 } cc_counters;
 
 typedef struct {
@@ -190,6 +199,32 @@ cc_status cc_labels(const int64_t* offsets, const uint32_t* adj, uint32_t n, int
 cc_status cc_spanning_forest(const int64_t* offsets, const uint32_t* adj, uint32_t n, int64_t m,
                              uint32_t* edges, int64_t* num_edges, uint32_t* labels,
                              const cc_opts* opts, void* stream);
+
+/* Approximate minimum spanning forest, AMSF-NF-S (Sec. 5.1):
+ * W(F_OPT) <= W(F) <= (1+eps) W(F_OPT).  The folklore algorithm:
+ * W_min = min w(e); bucket i holds the edges with b_i <= w < b_(i+1), b_0 =
+ * W_min, b_(i+1) = b_i * (1+eps) in fp64 (reading R25); buckets are
+ * processed from light to heavy, each one's edges unioned with UF-Rem-CAS +
+ * SplitAtomicOne on one persistent parent array, recording the
+ * edge at the hooked root as in cc_spanning_forest.  NF: the CSR
+ * is never mutated.  S: each round samples L_max (IdentifyFrequent
+ * on the current labeling) and skips the vertices of its component; CC_FLAG_NO_SKIP
+ * turns that off.  Unless CC_FLAG_AMSF_PLAIN is set, a vertex is visited only in
+ * the rounds between the buckets of its lightest and heaviest edge.
+ *   w         float32[m], aligned with adj; strictly positive, finite, and
+ *             symmetric (w(u,v) == w(v,u)) -- the skip relies on it.
+ *   eps       > 0 (the paper uses 0.25).
+ *   edges     (out, capacity 2*n uint32): forest pairs (u, v), input edges.
+ *   edge_w    (out, capacity n float, may be NULL): their weights.
+ *   num_edges (out, one int64) = n - #components.
+ *   total     (out, one double, may be NULL): sum of the forest weights (fp64).
+ * All array arguments must be device memory (CC_EINVAL otherwise).  The call
+ * synchronises `stream` once, to read W_min / W_max and size the buckets.
+ * Errors: CC_EINVAL for eps <= 0 or a non-positive / non-finite weight
+ * (checked on the device; outputs untouched). */
+cc_status cc_amsf(const int64_t* offsets, const uint32_t* adj, const float* w, uint32_t n, int64_t m, double eps,
+                  uint32_t* edges, float* edge_w, int64_t* num_edges, double* total, const cc_opts* opts,
+                  void* stream);
 
 /* Batch-incremental connectivity, Alg. 3, UF-Rem-CAS +
  * SplitAtomicOne on a persistent parent array owned by the

@@ -21,7 +21,8 @@
 namespace {
 
 constexpr uint64_t GOLD = 0x9E3779B97F4A7C15ull;
-constexpr uint64_t ER_STREAM = 1, GRID_STREAM = 2, RMAT_STREAM = 3, PERM_STREAM = 4, QUERY_STREAM = 5;
+constexpr uint64_t ER_STREAM = 1, GRID_STREAM = 2, RMAT_STREAM = 3, PERM_STREAM = 4, QUERY_STREAM = 5,
+                   WEIGHT_STREAM = 6;
 constexpr uint32_t RMAT_T1 = 2448131358u, RMAT_T2 = 3264175144u, RMAT_T3 = 4080218931u;
 
 __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x)
@@ -207,6 +208,49 @@ struct State {
     int vb = 0;
 };
 
+constexpr int LN_TERMS = 10;
+constexpr double LN2 = 0.6931471805599453;
+
+__device__ __forceinline__ double atanh2(double t)
+{
+    const double t2 = __dmul_rn(t, t);
+    double p = __ddiv_rn(1.0, (double)(2 * LN_TERMS + 1));
+    for (int k = LN_TERMS - 1; k >= 0; --k) {
+        p = __dmul_rn(p, t2);
+        p = __dadd_rn(p, __ddiv_rn(1.0, (double)(2 * k + 1)));
+    }
+    return __dmul_rn(__dmul_rn(2.0, t), p);
+}
+
+__device__ __forceinline__ double neg_ln_fixed(double x)
+{
+    if (x < 0.5) {
+        const uint64_t bits = (uint64_t)__double_as_longlong(x);
+        const int64_t e = (int64_t)((bits >> 52) & 0x7FF) - 1023;
+        const double mm = __longlong_as_double((long long)((bits & 0x000FFFFFFFFFFFFFull) | (1023ull << 52)));
+        const double t = __ddiv_rn(__dsub_rn(mm, 1.0), __dadd_rn(mm, 1.0));
+        return -__dadd_rn(__dmul_rn((double)e, LN2), atanh2(t));
+    }
+    const double d = __dsub_rn(1.0, x);
+    return atanh2(__ddiv_rn(d, __dsub_rn(2.0, d)));
+}
+
+__global__ void k_weights(const int64_t* off, const uint32_t* adj, uint32_t n, uint64_t m, uint64_t seed, float* w)
+{
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t lo = 0, hi = n;                              // src: largest u with off[u] <= e
+        while (hi - lo > 1) {
+            const uint32_t mid = lo + (hi - lo) / 2;
+            if ((uint64_t)off[mid] <= e) lo = mid; else hi = mid;
+        }
+        const uint64_t a = lo, b = adj[e];
+        const uint64_t key = ((a < b ? a : b) << 32) | (a < b ? b : a);
+        const uint64_t k = mix(seed, WEIGHT_STREAM, key) >> 12;
+        const double u = __dmul_rn(__dadd_rn((double)k, 0.5), 0x1p-52);
+        w[e] = __double2float_rn(neg_ln_fixed(u));
+    }
+}
+
 int bits_for(uint64_t n)
 {
     int b = 1;
@@ -371,6 +415,19 @@ int gen_incr_batch(uint64_t seed, int s, uint64_t b, uint64_t n_ins, uint64_t n_
 {
     Perm perm = make_perm(seed, s);
     k_incr<<<grid_blocks(), 256, 0, (cudaStream_t)stream>>>(seed, s, perm, b * n_ins, n_ins, b * n_q, n_q, ins, qs);
+    TRY(cudaGetLastError());
+    return 0;
+}
+
+// Exp(1) edge weights (inputs/gen.py exp_weights): w(u,v) = -ln(U),
+// U = (k + 1/2) 2^-52, k = mix(seed, WEIGHT, min(u,v) 2^32 + max(u,v)) >> 12,
+// with gen.py's fixed-order log (explicit _rn intrinsics: no FMA contraction),
+// so the float32 bytes are identical.
+int gen_exp_weights(const int64_t* off, const uint32_t* adj, uint32_t n, int64_t m, uint64_t seed, float* w,
+                    void* stream)
+{
+    if (m <= 0) return 0;
+    k_weights<<<grid_blocks(), 256, 0, (cudaStream_t)stream>>>(off, adj, n, (uint64_t)m, seed, w);
     TRY(cudaGetLastError());
     return 0;
 }

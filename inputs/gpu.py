@@ -30,7 +30,8 @@ def _load():
         lib.gen_csr_finish.argtypes = [P, P, P]
         lib.gen_csr_abort.argtypes = [P]
         lib.gen_incr_batch.argtypes = [U64, ctypes.c_int, U64, U64, U64, P, P, P]
-        for f in (lib.gen_csr_begin, lib.gen_csr_finish, lib.gen_incr_batch):
+        lib.gen_exp_weights.argtypes = [P, P, ctypes.c_uint32, ctypes.c_int64, U64, P, P]
+        for f in (lib.gen_csr_begin, lib.gen_csr_finish, lib.gen_incr_batch, lib.gen_exp_weights):
             f.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -90,3 +91,14 @@ def incr_batch(seed: int, scale: int, b: int, n_ins: int, n_q: int, ins=None, qs
     if rc:
         raise RuntimeError(f"gen_incr_batch failed: {rc}")
     return ins, qs
+
+
+def exp_weights(d_off, d_adj, seed: int, stream=None):
+    """Device float32 weights aligned with d_adj (gen.exp_weights' bytes)."""
+    n, m = d_off.numel() - 1, d_adj.numel()
+    w = torch.empty(max(m, 1), dtype=torch.float32, device=d_adj.device)
+    s = torch.cuda.current_stream().cuda_stream if stream is None else stream
+    rc = _load().gen_exp_weights(d_off.data_ptr(), d_adj.data_ptr(), n, m, seed, w.data_ptr(), s)
+    if rc:
+        raise RuntimeError(f"gen_exp_weights failed: {rc}")
+    return w[:m]

@@ -332,11 +332,22 @@ int oracle_amsf(uint32_t n, const int64_t* off, const uint32_t* adj, const float
         }
         bucket[e] = (int32_t)lo;
     }
+    /* the edges of each bucket, in CSR order (u < v): a stable counting sort by bucket */
+    int64_t* first = (int64_t*)calloc((size_t)nb + 1, sizeof(int64_t));
+    int64_t* idx = (int64_t*)malloc((size_t)ne * sizeof(int64_t));
+    if (!first || !idx) {
+        free(first); free(idx); free(b); free(bucket); free(parent); free(size); free(E);
+        return -3;
+    }
+    for (int64_t e = 0; e < ne; ++e) ++first[bucket[e] + 1];
+    for (int64_t i = 0; i < nb; ++i) first[i + 1] += first[i];
+    for (int64_t e = 0; e < ne; ++e) idx[first[bucket[e]]++] = e;          /* first[i] -> end of bucket i */
     for (uint32_t v = 0; v < n; ++v) { parent[v] = v; size[v] = 1; }
-    /* buckets from light to heavy; within one, CSR order (u < v) */
+    /* buckets from light to heavy */
+    int64_t k = 0;
     for (int64_t i = 0; i < nb; ++i)
-        for (int64_t e = 0; e < ne; ++e) {
-            if (bucket[e] != i) continue;
+        for (; k < first[i]; ++k) {
+            const int64_t e = idx[k];
             if (dsu_find(parent, E[e].u) == dsu_find(parent, E[e].v)) continue;   /* a self-loop of C */
             dsu_union(parent, size, E[e].u, E[e].v);
             F[2 * *nf] = E[e].u;
@@ -347,6 +358,8 @@ int oracle_amsf(uint32_t n, const int64_t* off, const uint32_t* adj, const float
             ++*nf;
         }
     *nbuckets = nb;
+    free(first);
+    free(idx);
     free(b);
     free(bucket);
     free(parent);

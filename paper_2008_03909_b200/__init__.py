@@ -5,6 +5,8 @@ Public API (torch tensors in, torch tensors out; all compute in libcc.so):
 * ``connected_components(offsets, adj, k=2, variant="afforest", ...)`` ->
   int32 labels (canonical: min vertex id of each component).
 * ``spanning_forest(offsets, adj, ...)`` -> (edges (F,2) int32, labels).
+* ``amsf(offsets, adj, w, eps=0.25)`` -> (edges (F,2) int32, weights (F,) f32,
+  total weight): an approximate minimum spanning forest (AMSF-NF-S).
 * ``IncrementalCC(n)`` with ``.batch(inserts, queries)`` -> uint8 answers and
   ``.labels()``.
 
@@ -46,6 +48,23 @@ def spanning_forest(offsets, adj, k: int = 2, variant: str = "afforest", seed: i
                           stream)
     ne = int(num.item())
     return edges[:ne], labels
+
+
+def amsf(offsets, adj, w, eps: float = 0.25, flags: int = 0, seed: int = 0, samples: int = 1024, stream=None,
+         **hooks):
+    """AMSF-NF-S (Sec. 5.1): W(F_OPT) <= W(F) <= (1+eps) W(F_OPT) for symmetric
+    positive float32 weights w aligned with adj."""
+    import torch
+    n = offsets.numel() - 1
+    dev = offsets.device
+    edges = torch.empty((max(n, 1), 2), dtype=torch.int32, device=dev)
+    ew = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+    num = torch.zeros(1, dtype=torch.int64, device=dev)
+    tot = torch.zeros(1, dtype=torch.float64, device=dev)
+    cc.cc_amsf(offsets, adj, w, n, adj.numel(), eps, edges, ew, num, tot,
+               cc.make_opts(seed=seed, samples=samples, flags=flags, **hooks), stream)
+    ne = int(num.item())
+    return edges[:ne], ew[:ne], float(tot.item())
 
 
 class IncrementalCC:

@@ -33,11 +33,13 @@ FLAG_WAIT_FREE = 1 << 8
 FLAG_FINISH_SV = 1 << 9
 FLAG_CONTRACT = 1 << 10
 FLAG_NO_REFILL = 1 << 11
+FLAG_AMSF_PLAIN = 1 << 12
 
 # every symbol include/cc.h and include/cc_bench.h declare
 EXPORTS = [
     "cc_opts_default", "cc_labels", "cc_spanning_forest", "cc_incr_create", "cc_incr_batch",
     "cc_incr_batches", "cc_incr_labels", "cc_incr_destroy", "cc_incr_num_vertices", "cc_status_str", "cc_last_error",
+    "cc_amsf",
     "cc_workspace_bytes", "cc_version",
     "cc_bench_map_edges", "cc_bench_gather_edges", "cc_bench_random_gather", "cc_bench_copy",
     "cc_bench_launch_count", "cc_bench_set_l2_fetch",
@@ -55,7 +57,8 @@ class Timings(ctypes.Structure):
 COUNTER_FIELDS = ["pending_links", "worklist", "finish_vertices", "finish_edges", "sample_hooks", "finish_hooks",
                   "big_vertices", "compress_writes",
                   "link_steps", "cas_failures", "probe_deep", "finish_gathers", "h6_writes", "h6_gathers",
-                  "sv_rounds", "contract_roots"]
+                  "sv_rounds", "contract_roots", "amsf_rounds", "amsf_visits", "amsf_edges", "amsf_hooks",
+                  "amsf_rebuilds"]
 
 
 class Opts(ctypes.Structure):
@@ -92,6 +95,7 @@ def load() -> ctypes.CDLL:
         "cc_opts_default": (None, [OP]),
         "cc_labels": (ctypes.c_int, [P, P, U32, I64, P, OP, P]),
         "cc_spanning_forest": (ctypes.c_int, [P, P, U32, I64, P, P, P, OP, P]),
+        "cc_amsf": (ctypes.c_int, [P, P, P, U32, I64, ctypes.c_double, P, P, P, P, OP, P]),
         "cc_incr_create": (ctypes.c_int, [U32, OP, P, ctypes.POINTER(ctypes.c_void_p)]),
         "cc_incr_batch": (ctypes.c_int, [P, P, I64, P, I64, P, P]),
         "cc_incr_batches": (ctypes.c_int, [P, I64, P, P, P, P, P, P]),
@@ -167,6 +171,15 @@ def cc_spanning_forest(offsets, adj, n, m, edges, num_edges, labels=None, opts: 
     rc = load().cc_spanning_forest(_ptr(offsets), _ptr(adj), n, m, _ptr(edges), _ptr(num_edges), _ptr(labels),
                                    ctypes.byref(opts) if opts is not None else None, _stream(stream))
     _check(rc, "cc_spanning_forest")
+
+
+def cc_amsf(offsets, adj, w, n, m, eps, edges, edge_w, num_edges, total=None, opts: Opts | None = None,
+            stream=None):
+    """AMSF-NF-S (include/cc.h cc_amsf); every array is a device tensor."""
+    rc = load().cc_amsf(_ptr(offsets), _ptr(adj), _ptr(w), n, m, float(eps), _ptr(edges), _ptr(edge_w),
+                        _ptr(num_edges), _ptr(total), ctypes.byref(opts) if opts is not None else None,
+                        _stream(stream))
+    _check(rc, "cc_amsf")
 
 
 class Incr:

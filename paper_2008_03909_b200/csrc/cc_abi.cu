@@ -274,4 +274,35 @@ cc_status cc_spanning_forest(const int64_t* offsets, const uint32_t* adj, uint32
     return CC_OK;
 }
 
+// AMSF-NF-S (include/cc.h): device memory only.
+cc_status cc_amsf(const int64_t* offsets, const uint32_t* adj, const float* w, uint32_t n, int64_t m, double eps,
+                  uint32_t* edges, float* edge_w, int64_t* num_edges, double* total, const cc_opts* opts,
+                  void* stream)
+{
+    const cc_opts o = resolve(opts);
+    cc_status rc = check_graph_args(offsets, adj, n, m, o);
+    if (rc) return rc;
+    if (!(eps > 0.0) || !(eps < 1e300)) { set_error("cc_amsf: eps must be > 0 and finite"); return CC_EINVAL; }
+    if (!num_edges) { set_error("num_edges is NULL"); return CC_EINVAL; }
+    if (n > 0 && !edges) { set_error("edges is NULL"); return CC_EINVAL; }
+    if (m > 0 && !w) { set_error("w is NULL"); return CC_EINVAL; }
+    for (const void* p : {(const void*)offsets, (const void*)adj, (const void*)w, (const void*)edges,
+                          (const void*)edge_w, (const void*)num_edges, (const void*)total})
+        if (p && mem_kind(p, nullptr) != MEM_DEVICE) {
+            set_error("cc_amsf: every array argument must be device memory");
+            return CC_EINVAL;
+        }
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n == 0) {
+        CC_CUDA_TRY(cudaMemsetAsync(num_edges, 0, sizeof(int64_t), s));
+        if (total) CC_CUDA_TRY(cudaMemsetAsync(total, 0, sizeof(double), s));
+        return CC_OK;
+    }
+    if (o.flags & CC_FLAG_VALIDATE) {
+        rc = validate_csr(offsets, adj, n, m, s);
+        if (rc) return rc;
+    }
+    return amsf_pipeline(offsets, adj, w, n, m, eps, edges, edge_w, num_edges, total, o, s);
+}
+
 }  // extern "C"

@@ -1,0 +1,522 @@
+// cc_amsf.cu -- approximate minimum spanning forest, AMSF-NF-S (NEXT-4).
+//
+// Sec. 5.1 of the paper.  The folklore algorithm:
+// bucket the edges by weight, [W_min (1+eps)^i, W_min (1+eps)^(i+1)), process
+// the buckets from light to heavy, and in each one add to the forest the edges
+// that join two different components of the labeling built so far.  NF
+// (P:1819-1822): the CSR is never mutated, every round reads the lists again.
+// S: each round finds the largest component L_max of the current
+// labeling and skips its vertices -- an edge leaving it is seen from its other
+// endpoint (the weights are symmetric, so both directions share a bucket).
+// Every union is UF-Rem-CAS + SplitAtomicOne on ONE persistent
+// parent array; the edge whose CAS hooks a root is recorded at that root (the
+// rule of Alg. 2), so a root is recorded at most once over all
+// rounds and the slots form the forest U F_i.
+//
+// B200 layout of a round (one persistent-grid kernel, no host round trip):
+//   active list  -- the vertices that may still have work: those carried over
+//                   from the previous round plus those whose lightest edge
+//                   falls in this bucket (a counting sort by that bucket,
+//                   computed once).  A vertex leaves the list for good when
+//                   its heaviest edge is below the bucket, or when its root is
+//                   the skipped component's (if a later round's L_max is a
+//                   different component the list is rebuilt from scratch).
+//   edge sweep   -- a warp takes up to 32 active vertices and sweeps their
+//                   concatenated lists 32 entries at a time (prefix sums +
+//                   shuffle search, as in the static finish): each lane reads
+//                   one weight (coalesced) and only an in-bucket edge reads its
+//                   endpoint and runs a link.
+// CC_FLAG_AMSF_PLAIN drops the per-vertex [min, max] weight index: every
+// non-skipped vertex is active and fully inspected in every round, as the
+// paper states NF-S.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "cc_common.cuh"
+#include "cc_device.cuh"
+#include "cc_internal.h"
+
+namespace ccb {
+
+namespace {
+
+constexpr uint32_t kPosInfBits = 0x7F800000u;     // +inf as float bits
+constexpr uint64_t AMSF_IDENT_STREAM = 19;        // per-round L_max samples: index = round * 2^20 + i
+
+struct AmsfCtl {
+    unsigned long long cnt[2];   // carry-list lengths (ping-pong)
+    unsigned int wmin_bits;      // min / max weight (positive floats order like their bits)
+    unsigned int wmax_bits;
+    unsigned int bad;            // a weight <= 0 or not finite
+    unsigned int anchor;         // a vertex of the component whose vertices are being dropped
+    unsigned int skip_root;      // its root at the start of the current round
+    unsigned int rebuild;        // this round's input is order[0 .. start[i+1])
+};
+
+// Record for AMSF hooks: the edge and its weight at the hooked root.
+struct ForestW {
+    uint2* F;
+    float* Fw;
+    float w;
+    __device__ __forceinline__ void record(uint32_t r, uint32_t u, uint32_t v) const
+    {
+        F[r] = make_uint2(u, v);
+        Fw[r] = w;
+    }
+};
+
+__device__ __forceinline__ bool good_weight(float x) { return x > 0.0f && x < __int_as_float((int)kPosInfBits); }
+
+// Per-vertex lightest / heaviest edge weight and the global range.  Edge-balanced:
+// warp c owns entries [c*4096, (c+1)*4096) and follows their owners with a
+// monotone pointer, flushing one atomicMin / atomicMax per (lane, owner) run.
+constexpr int64_t kChunk = 4096;
+__global__ void __launch_bounds__(kBlock) k_amsf_wrange(const int64_t* __restrict__ off, const float* __restrict__ w,
+                                                        uint32_t n, int64_t m, uint32_t* wlo, uint32_t* whi,
+                                                        AmsfCtl* ac)
+{
+    const unsigned lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    uint32_t gmin = kPosInfBits, gmax = 0, bad = 0;
+    for (int64_t c0 = warp * kChunk; c0 < m; c0 += nwarps * kChunk) {
+        const int64_t c1 = min(c0 + kChunk, m);
+        uint32_t lo = 0, hi = n;                              // largest u with off[u] <= c0
+        if (lane == 0) {
+            while (hi - lo > 1) {
+                const uint32_t mid = lo + (hi - lo) / 2;
+                if (off[mid] <= c0) lo = mid; else hi = mid;
+            }
+        }
+        uint32_t own = __shfl_sync(0xffffffffu, lo, 0);
+        int64_t own_end = off[own + 1];
+        uint32_t rlo = kPosInfBits, rhi = 0;
+        for (int64_t i = c0 + lane; i < c1; i += 32) {
+            const float x = w[i];
+            if (!good_weight(x)) bad = 1;
+            const uint32_t b = __float_as_uint(x) & 0x7FFFFFFFu;
+            if (i >= own_end) {
+                if (rhi) {
+                    atomicMin(wlo + own, rlo);
+                    atomicMax(whi + own, rhi);
+                }
+                rlo = kPosInfBits;
+                rhi = 0;
+                do {
+                    ++own;
+                    own_end = off[own + 1];
+                } while (own_end <= i);
+            }
+            rlo = min(rlo, b);
+            rhi = max(rhi, b);
+            gmin = min(gmin, b);
+            gmax = max(gmax, b);
+        }
+        if (rhi) {
+            atomicMin(wlo + own, rlo);
+            atomicMax(whi + own, rhi);
+        }
+    }
+    gmin = __reduce_min_sync(0xffffffffu, gmin);
+    gmax = __reduce_max_sync(0xffffffffu, gmax);
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if (lane == 0) {
+        if (gmin != kPosInfBits) atomicMin(&ac->wmin_bits, gmin);
+        if (gmax) atomicMax(&ac->wmax_bits, gmax);
+        if (bad) atomicOr(&ac->bad, 1u);
+    }
+}
+
+__global__ void k_amsf_init(uint32_t* P, uint32_t* wlo, uint32_t* whi, uint2* F, uint32_t n)
+{
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+        P[v] = (uint32_t)v;
+        wlo[v] = kPosInfBits;
+        whi[v] = 0u;
+        F[v] = make_uint2(kSentinel, kSentinel);
+    }
+}
+
+// bucket of a weight: the i with b[i] <= x < b[i+1] (b[0] = W_min <= x)
+__device__ __forceinline__ uint32_t bucket_of(const double* b, uint32_t nb, float x)
+{
+    const double d = (double)x;
+    uint32_t lo = 0, hi = nb;
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (b[mid] <= d) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// activation bucket of every non-isolated vertex (its lightest edge's bucket;
+// 0 in PLAIN mode) and the histogram of those buckets
+__global__ void __launch_bounds__(kBlock) k_amsf_first(const uint32_t* wlo, const uint32_t* whi, uint32_t n,
+                                                       const double* b, uint32_t nb, bool plain, uint32_t* fb,
+                                                       unsigned long long* hist)
+{
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+        if (!whi[v]) continue;                                // isolated
+        const uint32_t f = plain ? 0u : bucket_of(b, nb, __uint_as_float(wlo[v]));
+        fb[v] = f;
+        atomicAdd(hist + f, 1ull);
+    }
+}
+
+// exclusive scan of the histogram (nb + 1 entries, one block)
+__global__ void __launch_bounds__(kBlock) k_amsf_scan(unsigned long long* hist, uint32_t nb)
+{
+    __shared__ unsigned long long carry;
+    __shared__ unsigned long long ws[kBlock / 32];
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const unsigned lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    for (uint32_t base = 0; base <= nb; base += kBlock) {
+        const uint32_t i = base + threadIdx.x;
+        const unsigned long long x = i <= nb ? hist[i] : 0ull;
+        unsigned long long incl = x;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (unsigned)o) incl += t;
+        }
+        if (lane == 31) ws[wi] = incl;
+        __syncthreads();
+        unsigned long long wb = 0;
+        for (unsigned j = 0; j < wi; ++j) wb += ws[j];
+        const unsigned long long c = carry;
+        if (i <= nb) hist[i] = c + wb + incl - x;
+        __syncthreads();
+        if (threadIdx.x == kBlock - 1) carry = c + wb + incl;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) k_amsf_scatter(const uint32_t* whi, const uint32_t* fb, uint32_t n,
+                                                         unsigned long long* cursor, uint32_t* order)
+{
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+        if (!whi[v]) continue;
+        order[atomicAdd(cursor + fb[v], 1ull)] = (uint32_t)v;
+    }
+}
+
+// S: L_max of the current labeling (IdentifyFrequent: the mode of the
+// roots of S seeded samples, ties to the smaller label), kept as the "anchor"
+// of the skipped component.  The dropped vertices all lie in the anchor's
+// component (components only merge, so it only grows); if L_max is now a
+// different component -- seen by more samples than the anchor's -- the anchor
+// moves there and this round rebuilds its input from every activated vertex.
+constexpr int kIdTable = 4096;
+__global__ void __launch_bounds__(1024) k_amsf_lmax(const uint32_t* P, uint32_t n, uint64_t seed, uint32_t round,
+                                                    uint32_t samples, AmsfCtl* ac)
+{
+    __shared__ uint32_t keys[kIdTable];
+    __shared__ uint32_t cnts[kIdTable];
+    __shared__ unsigned long long best[32];
+    __shared__ uint32_t s_ra, s_cnt_ra;
+    const int t = threadIdx.x;
+    for (int i = t; i < kIdTable; i += blockDim.x) {
+        keys[i] = kSentinel;
+        cnts[i] = 0;
+    }
+    if (t == 0) {
+        s_ra = ac->anchor == kSentinel ? kSentinel : find_naive(P, ac->anchor);   // no hook runs now
+        s_cnt_ra = 0;
+    }
+    __syncthreads();
+    for (int i = t; i < (int)samples; i += blockDim.x) {
+        const uint32_t sv = uniform_below(mix(seed, AMSF_IDENT_STREAM, ((uint64_t)round << 20) + (uint64_t)i), n);
+        const uint32_t lab = find_naive(P, sv);
+        if (lab == s_ra) atomicAdd(&s_cnt_ra, 1u);
+        uint32_t h = (lab * 0x9E3779B1u) >> 20;
+        while (true) {
+            const uint32_t old = atomicCAS(&keys[h], kSentinel, lab);
+            if (old == kSentinel || old == lab) {
+                atomicAdd(&cnts[h], 1u);
+                break;
+            }
+            h = (h + 1) & (kIdTable - 1);
+        }
+    }
+    __syncthreads();
+    unsigned long long key = 0;
+    for (int i = t; i < kIdTable; i += blockDim.x)
+        if (cnts[i]) {
+            const unsigned long long k2 = ((unsigned long long)cnts[i] << 32) | (unsigned long long)(kSentinel - keys[i]);
+            key = key > k2 ? key : k2;
+        }
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(0xffffffffu, key, o);
+        key = key > y ? key : y;
+    }
+    if ((t & 31) == 0) best[t >> 5] = key;
+    __syncthreads();
+    if (t < 32) {
+        key = t < (int)(blockDim.x >> 5) ? best[t] : 0;
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long y = __shfl_xor_sync(0xffffffffu, key, o);
+            key = key > y ? key : y;
+        }
+        if (t == 0) {
+            const uint32_t lm = kSentinel - (uint32_t)(key & 0xFFFFFFFFull);
+            const uint32_t cnt_lm = (uint32_t)(key >> 32);
+            // a component seen by under 1/64 of the samples is not worth skipping (while the
+            // labeling is all singletons every sample is its own mode): start, or move, the
+            // anchor only for a component at least that large
+            const bool big = (uint64_t)cnt_lm * 64 >= samples;
+            ac->rebuild = 0;
+            if (s_ra == kSentinel) {
+                if (big) ac->anchor = lm;                 // nothing dropped yet: no rebuild needed
+            } else if (big && lm != s_ra && cnt_lm > s_cnt_ra) {
+                ac->anchor = lm;                          // a different, larger component
+                ac->rebuild = 1;
+            }
+            ac->skip_root = ac->anchor == kSentinel ? kSentinel : (ac->anchor == lm ? lm : s_ra);
+        }
+    }
+}
+
+// One round (bucket i = [blo, bhi)): the active list is the carry list plus the
+// vertices activated in this bucket (order[start[i] .. start[i+1])), or, after
+// an anchor move, order[0 .. start[i+1]).  Survivors are appended to the next
+// carry list.
+template <int MODE>
+__global__ void __launch_bounds__(kBlock) k_amsf_round(
+    const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, const float* __restrict__ w, uint32_t* P,
+    const uint32_t* __restrict__ wlo, const uint32_t* __restrict__ whi, const uint32_t* __restrict__ order,
+    const unsigned long long* __restrict__ start, uint32_t round, double blo, double bhi,
+    const uint32_t* __restrict__ carry_in, AmsfCtl* ac, int in_slot, uint32_t* carry_out, bool skip, bool plain,
+    uint2* F, float* Fw, cc_counters* cnt)
+{
+    const unsigned lane = threadIdx.x & 31;
+    const bool rebuild = ac->rebuild != 0;
+    const unsigned long long s0 = rebuild ? 0ull : start[round], s1 = start[round + 1];
+    const unsigned long long n1 = rebuild ? 0ull : ac->cnt[in_slot];
+    const unsigned long long total = n1 + (s1 - s0);
+    const uint32_t skip_root = skip ? ac->skip_root : kSentinel;
+    unsigned long long* out_cnt = &ac->cnt[in_slot ^ 1];
+    const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    const unsigned cpw = (unsigned)max(1ull, min(32ull, (total + nwarps - 1) / nwarps));
+    uint32_t visits = 0, hooks = 0;
+    unsigned long long scanned = 0;
+    for (unsigned long long base = warp * cpw; base < total; base += nwarps * cpw) {
+        const unsigned long long i = base + lane;
+        const bool cand = lane < cpw && i < total;
+        const uint32_t u = cand ? (i < n1 ? carry_in[i] : order[s0 + (i - n1)]) : 0u;
+        bool keep = false, work = false;
+        if (cand) {
+            ++visits;
+            const double hi_w = plain ? INFINITY : (double)__uint_as_float(whi[u]);
+            const double lo_w = plain ? 0.0 : (double)__uint_as_float(wlo[u]);
+            if (hi_w >= blo && !(skip_root != kSentinel && find_naive(P, u) == skip_root)) {
+                keep = hi_w >= bhi;                            // edges left for later buckets
+                work = lo_w < bhi;                             // maybe an edge in this bucket
+            }
+        }
+        const unsigned long long pos = warp_append(out_cnt, keep ? 1u : 0u);
+        if (keep) carry_out[pos] = u;
+        const int64_t b = work ? off[u] : 0;
+        const uint32_t d = work ? (uint32_t)min(off[u + 1] - b, (int64_t)0xFFFFFFFF) : 0u;
+        uint32_t incl = d;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (unsigned)o) incl += t;
+        }
+        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t excl = incl - d;
+        scanned += lane == 0 ? tot : 0u;
+        for (uint32_t t0 = 0; t0 < tot; t0 += 32) {
+            const uint32_t t = t0 + lane;
+            int lo = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const uint32_t pe = __shfl_sync(0xffffffffu, excl, lo + step);
+                if (pe <= t) lo += step;
+            }
+            const uint32_t ou = __shfl_sync(0xffffffffu, u, lo);
+            const int64_t ob = __shfl_sync(0xffffffffu, b, lo);
+            const uint32_t oex = __shfl_sync(0xffffffffu, excl, lo);
+            if (t < tot) {
+                const int64_t e = ob + (t - oex);
+                const float x = w[e];
+                const double xd = (double)x;
+                if (xd >= blo && xd < bhi) {
+                    const uint32_t v = adj[e];
+                    hooks += link<MODE>(P, ou, v, ForestW{F, Fw, x});
+                }
+            }
+            __syncwarp();
+        }
+    }
+    if (cnt) {
+        warp_count(&cnt->amsf_visits, visits);
+        warp_count(&cnt->amsf_hooks, hooks);
+        const unsigned long long sc = __reduce_add_sync(0xffffffffu, (uint32_t)min(scanned, 0xFFFFFFFFull));
+        if (lane == 0 && sc) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt->amsf_edges), sc);
+    }
+}
+
+__global__ void k_amsf_next(AmsfCtl* ac, int in_slot, cc_counters* cnt)
+{
+    ac->cnt[in_slot] = 0;                                      // becomes the next round's output
+    if (cnt) {
+        cnt->amsf_rounds += 1;
+        cnt->amsf_rebuilds += ac->rebuild;
+    }
+}
+
+// sum of the forest weights (fp64)
+__global__ void __launch_bounds__(kBlock) k_amsf_total(const float* ew, const int64_t* ne, double* total)
+{
+    const uint64_t k = (uint64_t)*ne;
+    double s = 0.0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += (uint64_t)gridDim.x * blockDim.x)
+        s += (double)ew[i];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0 && s != 0.0) atomicAdd(total, s);
+}
+
+template <int MODE>
+cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint32_t n, int64_t m, double eps,
+                   uint32_t* edges, float* edge_w, int64_t* num_edges, double* total, const cc_opts& o,
+                   cudaStream_t s)
+{
+    const int sms = num_sms();
+    const bool skip = !(o.flags & CC_FLAG_NO_SKIP);
+    const bool plain = (o.flags & CC_FLAG_AMSF_PLAIN) != 0;
+    AmsfCtl* ac = nullptr;
+    uint32_t *P = nullptr, *wlo = nullptr, *whi = nullptr, *fb = nullptr, *order = nullptr;
+    uint32_t* carry[2] = {nullptr, nullptr};
+    uint2* F = nullptr;
+    float* Fw = nullptr;
+    double* bd = nullptr;
+    unsigned long long *start = nullptr, *cursor = nullptr;
+    uint32_t* fcnt = nullptr;
+    unsigned long long* foff = nullptr;
+    const uint32_t nfb = (uint32_t)(((uint64_t)n + kFTile - 1) / kFTile);
+    auto body = [&]() -> cc_status {
+        CC_CUDA_TRY(scratch_alloc((void**)&ac, sizeof(AmsfCtl), s));
+        CC_CUDA_TRY(scratch_alloc((void**)&P, sizeof(uint32_t) * n, s));
+        CC_CUDA_TRY(scratch_alloc((void**)&wlo, sizeof(uint32_t) * n, s));
+        CC_CUDA_TRY(scratch_alloc((void**)&whi, sizeof(uint32_t) * n, s));
+        CC_CUDA_TRY(scratch_alloc((void**)&F, sizeof(uint2) * n, s));
+        CC_CUDA_TRY(scratch_alloc((void**)&Fw, sizeof(float) * n, s));
+        AmsfCtl h0{};
+        h0.wmin_bits = kPosInfBits;
+        h0.anchor = kSentinel;
+        h0.skip_root = kSentinel;
+        CC_CUDA_TRY(cudaMemcpyAsync(ac, &h0, sizeof(h0), cudaMemcpyHostToDevice, s));
+        k_amsf_init<<<sms * 8, kBlock, 0, s>>>(P, wlo, whi, F, n);
+        CC_LAUNCH_CHECK("k_amsf_init");
+        if (m > 0) {
+            k_amsf_wrange<<<sms * 16, kBlock, 0, s>>>(off, w, n, m, wlo, whi, ac);
+            CC_LAUNCH_CHECK("k_amsf_wrange");
+        }
+        AmsfCtl h{};
+        CC_CUDA_TRY(cudaMemcpyAsync(&h, ac, sizeof(h), cudaMemcpyDeviceToHost, s));
+        CC_CUDA_TRY(cudaStreamSynchronize(s));
+        if (h.bad) {
+            set_error("cc_amsf: a weight is <= 0 or not finite");
+            return CC_EINVAL;
+        }
+        uint32_t nb = 0;
+        std::vector<double> b;
+        if (m > 0) {
+            // bucket boundaries (reading R25): b_0 = W_min, b_(i+1) = b_i * (1 + eps), up to
+            // the first one above W_max -- the same fp64 product chain as the oracle
+            float fmin, fmax;
+            std::memcpy(&fmin, &h.wmin_bits, 4);
+            std::memcpy(&fmax, &h.wmax_bits, 4);
+            const double wmin = fmin, wmax = fmax;
+            const double g = 1.0 + eps;
+            b.push_back(wmin);
+            while (b.back() * g <= wmax) {
+                b.push_back(b.back() * g);
+                if (b.size() > (1u << 24)) {
+                    set_error("cc_amsf: more than 2^24 weight buckets (eps too small)");
+                    return CC_ERANGE;
+                }
+            }
+            b.push_back(b.back() * g);
+            nb = (uint32_t)(b.size() - 1);
+            CC_CUDA_TRY(scratch_alloc((void**)&bd, sizeof(double) * b.size(), s));
+            CC_CUDA_TRY(cudaMemcpyAsync(bd, b.data(), sizeof(double) * b.size(), cudaMemcpyHostToDevice, s));
+            CC_CUDA_TRY(scratch_alloc((void**)&fb, sizeof(uint32_t) * n, s));
+            CC_CUDA_TRY(scratch_alloc((void**)&order, sizeof(uint32_t) * n, s));
+            CC_CUDA_TRY(scratch_alloc((void**)&carry[0], sizeof(uint32_t) * n, s));
+            CC_CUDA_TRY(scratch_alloc((void**)&carry[1], sizeof(uint32_t) * n, s));
+            CC_CUDA_TRY(scratch_alloc((void**)&start, sizeof(unsigned long long) * (nb + 1), s));
+            CC_CUDA_TRY(scratch_alloc((void**)&cursor, sizeof(unsigned long long) * (nb + 1), s));
+            CC_CUDA_TRY(cudaMemsetAsync(start, 0, sizeof(unsigned long long) * (nb + 1), s));
+            // activation order: non-isolated vertices by the bucket of their lightest edge
+            k_amsf_first<<<sms * 8, kBlock, 0, s>>>(wlo, whi, n, bd, nb, plain, fb, start);
+            CC_LAUNCH_CHECK("k_amsf_first");
+            k_amsf_scan<<<1, kBlock, 0, s>>>(start, nb);
+            CC_LAUNCH_CHECK("k_amsf_scan");
+            CC_CUDA_TRY(cudaMemcpyAsync(cursor, start, sizeof(unsigned long long) * (nb + 1), cudaMemcpyDeviceToDevice, s));
+            k_amsf_scatter<<<sms * 8, kBlock, 0, s>>>(whi, fb, n, cursor, order);
+            CC_LAUNCH_CHECK("k_amsf_scatter");
+        }
+        // the rounds: bucket i = [b_i, b_(i+1)), lightest first
+        for (uint32_t i = 0; i < nb; ++i) {
+            const int in_slot = i & 1;
+            if (skip) {
+                k_amsf_lmax<<<1, 1024, 0, s>>>(P, n, o.seed, i, o.samples, ac);
+                CC_LAUNCH_CHECK("k_amsf_lmax");
+            }
+            k_amsf_round<MODE><<<sms * 8, kBlock, 0, s>>>(off, adj, w, P, wlo, whi, order, start, i, b[i], b[i + 1],
+                                                          carry[in_slot], ac, in_slot, carry[in_slot ^ 1],
+                                                          skip, plain, F, Fw, o.counters);
+            CC_LAUNCH_CHECK("k_amsf_round");
+            k_amsf_next<<<1, 1, 0, s>>>(ac, in_slot, o.counters);
+            CC_LAUNCH_CHECK("k_amsf_next");
+        }
+        // Filter: the non-empty slots, in slot order, with their weights
+        CC_CUDA_TRY(scratch_alloc((void**)&fcnt, sizeof(uint32_t) * nfb, s));
+        CC_CUDA_TRY(scratch_alloc((void**)&foff, sizeof(unsigned long long) * nfb, s));
+        k_forest_count<<<nfb, kBlock, 0, s>>>(F, n, fcnt);
+        CC_LAUNCH_CHECK("k_forest_count");
+        k_forest_scan<<<1, kBlock, 0, s>>>(fcnt, nfb, foff, num_edges);
+        CC_LAUNCH_CHECK("k_forest_scan");
+        float* ew = edge_w;
+        if (!ew && total) {
+            CC_CUDA_TRY(scratch_alloc((void**)&ew, sizeof(float) * n, s));
+        }
+        k_forest_write<<<nfb, kBlock, 0, s>>>(F, n, foff, edges, Fw, ew);
+        CC_LAUNCH_CHECK("k_forest_write");
+        if (total) {
+            CC_CUDA_TRY(cudaMemsetAsync(total, 0, sizeof(double), s));
+            k_amsf_total<<<sms * 4, kBlock, 0, s>>>(ew, num_edges, total);
+            CC_LAUNCH_CHECK("k_amsf_total");
+        }
+        if (ew != edge_w) scratch_free(ew, s);
+        return CC_OK;
+    };
+    const cc_status rc = body();
+    for (void* p : {(void*)ac, (void*)P, (void*)wlo, (void*)whi, (void*)fb, (void*)order, (void*)carry[0],
+                    (void*)carry[1], (void*)F, (void*)Fw, (void*)bd, (void*)start, (void*)cursor, (void*)fcnt,
+                    (void*)foff})
+        scratch_free(p, s);
+    return rc;
+}
+
+}  // namespace
+
+cc_status amsf_pipeline(const int64_t* off, const uint32_t* adj, const float* w, uint32_t n, int64_t m, double eps,
+                        uint32_t* edges, float* edge_w, int64_t* num_edges, double* total, const cc_opts& o,
+                        cudaStream_t s)
+{
+    if (o.flags & CC_FLAG_UF_ASYNC) return amsf_run<2>(off, adj, w, n, m, eps, edges, edge_w, num_edges, total, o, s);
+    if (o.flags & CC_FLAG_HALVE) return amsf_run<1>(off, adj, w, n, m, eps, edges, edge_w, num_edges, total, o, s);
+    return amsf_run<0>(off, adj, w, n, m, eps, edges, edge_w, num_edges, total, o, s);
+}
+
+}  // namespace ccb

@@ -51,6 +51,9 @@ constexpr int kBlock = 256;
 cc_status static_pipeline(const int64_t* off, const uint32_t* adj, uint32_t n, int64_t m, uint32_t* P,
                           uint32_t* labels_out, uint32_t* edges, int64_t* num_edges, bool sf, const cc_opts& o,
                           cudaStream_t s);
+cc_status amsf_pipeline(const int64_t* off, const uint32_t* adj, const float* w, uint32_t n, int64_t m, double eps,
+                        uint32_t* edges, float* edge_w, int64_t* num_edges, double* total, const cc_opts& o,
+                        cudaStream_t s);
 cc_status validate_csr(const int64_t* off, const uint32_t* adj, uint32_t n, int64_t m, cudaStream_t s);
 
 }  // namespace ccb

@@ -1,0 +1,163 @@
+"""GPU parity of cc_amsf (AMSF-NF-S, NEXT-4) vs the CPU oracle.
+
+Several forests are correct, so the comparison is on what is unique:
+* the forest is a spanning forest of the input (oracle.forest_check);
+* every returned weight is the input weight of its edge;
+* the number of forest edges in each weight bucket equals the oracle's --
+  bit-exact: both sides take the bucket decision b_i <= w < b_(i+1) on the same
+  fp64 boundaries (reading R25), and the per-bucket count is the rank increase
+  of the prefix graph, a property of the bucketing alone;
+* W(F_OPT) <= W(F) <= (1+eps) W(F_OPT) against Kruskal (fp64 sums, 1e-9 slack);
+* the returned total equals the fp64 sum of the returned weights.
+Everything goes through the C ABI (libcc.so).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from inputs import gen
+from tests.helpers import fixtures, to_dev, u32
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2008_03909_b200 as pkg  # noqa: E402
+from paper_2008_03909_b200 import cc  # noqa: E402
+
+OPTS = [
+    dict(flags=0),
+    dict(flags=cc.FLAG_NO_SKIP),
+    dict(flags=cc.FLAG_AMSF_PLAIN),
+    dict(flags=cc.FLAG_AMSF_PLAIN | cc.FLAG_NO_SKIP),
+    dict(flags=cc.FLAG_HALVE, seed=3),
+    dict(flags=cc.FLAG_UF_ASYNC, seed=4),
+]
+
+
+def run(off, adj, w, eps, **kw):
+    d_off, d_adj = to_dev(off, adj)
+    d_w = torch.from_numpy(np.ascontiguousarray(w, dtype=np.float32)).cuda()
+    E, W, tot = pkg.amsf(d_off, d_adj, d_w, eps, **kw)
+    torch.cuda.synchronize()
+    return u32(E).reshape(-1, 2), W.cpu().numpy(), tot
+
+
+def check(off, adj, w, eps, E, W, tot, want=None, exact_opt=True):
+    n = off.size - 1
+    lab = oracle.cc_bfs(off, adj)
+    c = int(np.sum(lab == np.arange(n)))
+    rc, bad = oracle.forest_check(off, adj, c, E)
+    assert rc == 0, (oracle.FOREST_ERRORS[rc], bad)
+    if E.shape[0]:
+        # each weight is its edge's input weight
+        for (a, b_), x in zip(E[:200], W[:200]):
+            lo, hi = off[a], off[a + 1]
+            j = lo + np.searchsorted(adj[lo:hi], b_)
+            assert w[j] == x
+    assert tot == pytest.approx(float(np.sum(W.astype(np.float64))), rel=1e-12, abs=1e-12)
+    if adj.size == 0:
+        assert E.shape[0] == 0 and tot == 0.0
+        return
+    want = oracle.amsf(off, adj, w, eps) if want is None else want
+    b = oracle.amsf_bounds(w.min(), w.max(), eps)
+    got_hist = np.bincount(oracle.amsf_bucket(W, b), minlength=want["nbuckets"])
+    want_hist = np.bincount(want["buckets"], minlength=want["nbuckets"])
+    assert np.array_equal(got_hist, want_hist), np.nonzero(got_hist != want_hist)[0][:5]
+    if exact_opt:
+        wopt = oracle.kruskal(off, adj, w)[0]
+        assert wopt * (1 - 1e-9) <= tot <= (1 + eps) * wopt * (1 + 1e-9)
+
+
+def graphs():
+    G = [(name, off, adj) for name, off, adj in fixtures()]
+    G.append(("er", *gen.er(seed=3, n0=5000, pairs=6000, isolated=37)))
+    G.append(("grid", *gen.grid(seed=5, rows=67, cols=131)))
+    G.append(("rmat10", *gen.rmat(seed=6, scale=10)))
+    G.append(("rmat13_unperm", *gen.rmat(seed=7, scale=13, permuted=False)))
+    return G
+
+
+@pytest.mark.parametrize("opt", OPTS, ids=lambda o: f"f{o['flags']}")
+def test_amsf_small(opt):
+    for name, off, adj in graphs():
+        w = gen.exp_weights(off, adj, 17)
+        E, W, tot = run(off, adj, w, 0.25, **opt)
+        check(off, adj, w, 0.25, E, W, tot)
+
+
+@pytest.mark.parametrize("eps", [0.01, 0.1, 1.0, 4.0])
+def test_amsf_eps(eps):
+    off, adj = gen.rmat(seed=8, scale=12)
+    w = gen.exp_weights(off, adj, 8)
+    for opt in (OPTS[0], OPTS[2]):
+        check(off, adj, w, eps, *run(off, adj, w, eps, **opt))
+
+
+def test_amsf_several_tiles_ragged():
+    for off, adj in (gen.rmat(seed=9, scale=15), gen.er(seed=4, n0=70001, pairs=150000, isolated=333),
+                     gen.grid(seed=6, rows=301, cols=257)):
+        w = gen.exp_weights(off, adj, 2)
+        want = oracle.amsf(off, adj, w, 0.25)
+        for opt in OPTS[:3]:
+            check(off, adj, w, 0.25, *run(off, adj, w, 0.25, **opt), want=want)
+
+
+def test_amsf_equal_weights_exact_and_ties():
+    off, adj = gen.er(seed=5, n0=3000, pairs=5000, isolated=2)
+    w = np.full(adj.size, 0.75, dtype=np.float32)
+    E, W, tot = run(off, adj, w, 0.25)
+    check(off, adj, w, 0.25, E, W, tot)
+    assert tot == pytest.approx(oracle.kruskal(off, adj, w)[0], rel=1e-12)      # one bucket: exact
+    # integer weights 1..4 with eps = 1: buckets [1,2) [2,4) [4,8): many ties
+    w = (1 + (np.arange(adj.size) % 4)).astype(np.float32)
+    src = np.repeat(np.arange(off.size - 1), np.diff(off))
+    w = (1 + ((np.minimum(src, adj) * 7 + np.maximum(src, adj)) % 4)).astype(np.float32)   # symmetric
+    check(off, adj, w, 1.0, *run(off, adj, w, 1.0))
+
+
+def test_amsf_rejects_bad_input():
+    off, adj = gen.er(seed=6, n0=100, pairs=300, isolated=0)
+    d_off, d_adj = to_dev(off, adj)
+    for bad in (0.0, -1.0, np.inf, np.nan):
+        w = gen.exp_weights(off, adj, 1)
+        w[5] = bad
+        with pytest.raises(cc.CCError):
+            pkg.amsf(d_off, d_adj, torch.from_numpy(w).cuda(), 0.25)
+    w = torch.from_numpy(gen.exp_weights(off, adj, 1)).cuda()
+    for eps in (0.0, -0.5, float("inf")):
+        with pytest.raises(cc.CCError):
+            pkg.amsf(d_off, d_adj, w, eps)
+    with pytest.raises(cc.CCError):                     # host weights: device memory only
+        pkg.amsf(d_off, d_adj, w.cpu(), 0.25)
+
+
+def test_amsf_counters():
+    off, adj = gen.rmat(seed=10, scale=13)
+    w = gen.exp_weights(off, adj, 10)
+    d_off, d_adj = to_dev(off, adj)
+    d_w = torch.from_numpy(w).cuda()
+    ctr = torch.zeros(len(cc.COUNTER_FIELDS), dtype=torch.int64, device="cuda")
+    E, W, tot = pkg.amsf(d_off, d_adj, d_w, 0.25, counters=ctr)
+    c = dict(zip(cc.COUNTER_FIELDS, ctr.cpu().tolist()))
+    want = oracle.amsf(off, adj, w, 0.25)
+    assert c["amsf_rounds"] == want["nbuckets"]
+    assert c["amsf_hooks"] == E.shape[0] == want["pairs"].shape[0]
+    ctr.zero_()
+    pkg.amsf(d_off, d_adj, d_w, 0.25, counters=ctr, flags=cc.FLAG_AMSF_PLAIN | cc.FLAG_NO_SKIP)
+    c2 = dict(zip(cc.COUNTER_FIELDS, ctr.cpu().tolist()))
+    # plain NF without the skip inspects every adjacency entry in every round
+    assert c2["amsf_edges"] == adj.size * want["nbuckets"]
+    assert c["amsf_edges"] < c2["amsf_edges"]
+
+
+def test_amsf_repeat_stress():
+    off, adj = gen.rmat(seed=11, scale=12)
+    w = gen.exp_weights(off, adj, 11)
+    want = oracle.amsf(off, adj, w, 0.25)
+    rng = np.random.default_rng(3)
+    for it in range(40):
+        opt = OPTS[int(rng.integers(0, len(OPTS)))]
+        check(off, adj, w, 0.25, *run(off, adj, w, 0.25, **opt), want=want, exact_opt=(it % 10 == 0))

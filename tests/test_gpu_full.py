@@ -75,3 +75,32 @@ def test_incremental_config_bit_exact():
     assert bad.size == 0, bad[:5]
     assert np.array_equal(lab, want_lab)
     print(f"C5: {got.size} answers, {int(want.sum())} true")
+
+
+def test_amsf_c3_bucket_counts():
+    """NEXT-4 at C3 size (RMAT-24, Exp(1) weights from the CUDA generator, eps =
+    0.25): a valid spanning forest whose per-bucket edge counts equal the oracle's
+    (which, with every weight inside its bucket, implies the (1+eps) sandwich)."""
+    cfg = inputs.C3
+    d_off, d_adj = ggen.config_graph(cfg)
+    d_w = ggen.exp_weights(d_off, d_adj, cfg.seed)
+    E, W, tot = pkg.amsf(d_off, d_adj, d_w, 0.25)
+    torch.cuda.synchronize()
+    E = u32(E).reshape(-1, 2)
+    W = W.cpu().numpy()
+    off = host(d_off, np.int64)
+    adj = host(d_adj, np.uint32)
+    w = d_w.cpu().numpy()
+    del d_off, d_adj, d_w
+    torch.cuda.empty_cache()
+    n = off.size - 1
+    lab = oracle.cc_bfs(off, adj)
+    c = int(np.sum(lab == np.arange(n)))
+    rc, idx = oracle.forest_check(off, adj, c, E)
+    assert rc == 0, (oracle.FOREST_ERRORS[rc], idx)
+    want = oracle.amsf(off, adj, w, 0.25)
+    b = oracle.amsf_bounds(w.min(), w.max(), 0.25)
+    assert np.array_equal(np.bincount(oracle.amsf_bucket(W, b), minlength=want["nbuckets"]),
+                          np.bincount(want["buckets"], minlength=want["nbuckets"]))
+    assert tot == pytest.approx(float(W.astype(np.float64).sum()), rel=1e-12)
+    print(f"C3 AMSF: n={n} forest={E.shape[0]} W={tot:.6g} oracle W={want['total']:.6g} buckets={want['nbuckets']}")

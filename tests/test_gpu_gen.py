@@ -42,3 +42,15 @@ def test_incr_batches_bytes():
         hi, hq = gen.incr_batch(5, 14, b, 1000, 111)
         assert np.array_equal(ins.cpu().numpy().view(np.uint32), hi)
         assert np.array_equal(qs.cpu().numpy().view(np.uint32), hq)
+
+
+@pytest.mark.parametrize("scale", [10, 16])
+def test_exp_weights_bytes(scale):
+    off, adj = gen.rmat(3, scale)
+    d_off, d_adj = ggen.rmat(3, scale)
+    w = ggen.exp_weights(d_off, d_adj, 3)
+    assert np.array_equal(w.cpu().numpy().view(np.uint32), gen.exp_weights(off, adj, 3).view(np.uint32))
+    go, ga = ggen.grid(2, 64, 70)
+    ho, ha = gen.grid(2, 64, 70)
+    assert np.array_equal(ggen.exp_weights(go, ga, 11).cpu().numpy().view(np.uint32),
+                          gen.exp_weights(ho, ha, 11).view(np.uint32))
