@@ -57,7 +57,10 @@ struct AmsfCtl {
     unsigned int anchor;         // a vertex of the component whose vertices are being dropped
     unsigned int skip_root;      // its root at the start of the current round
     unsigned int rebuild;        // this round's input is order[0 .. start[i+1])
+    unsigned long long chunks;   // long-list pieces queued this round
 };
+
+constexpr int64_t kAmsfChunk = 2048;   // lists longer than this are split across warps
 
 // Record for AMSF hooks: the edge and its weight at the hooked root.
 struct ForestW {
@@ -292,7 +295,7 @@ __global__ void __launch_bounds__(kBlock) k_amsf_round(
     const uint32_t* __restrict__ wlo, const uint32_t* __restrict__ whi, const uint32_t* __restrict__ order,
     const unsigned long long* __restrict__ start, uint32_t round, double blo, double bhi,
     const uint32_t* __restrict__ carry_in, AmsfCtl* ac, int in_slot, uint32_t* carry_out, bool skip, bool plain,
-    uint2* F, float* Fw, cc_counters* cnt)
+    uint2* F, float* Fw, uint2* chq, cc_counters* cnt)
 {
     const unsigned lane = threadIdx.x & 31;
     const bool rebuild = ac->rebuild != 0;
@@ -323,7 +326,15 @@ __global__ void __launch_bounds__(kBlock) k_amsf_round(
         const unsigned long long pos = warp_append(out_cnt, keep ? 1u : 0u);
         if (keep) carry_out[pos] = u;
         const int64_t b = work ? off[u] : 0;
-        const uint32_t d = work ? (uint32_t)min(off[u + 1] - b, (int64_t)0xFFFFFFFF) : 0u;
+        const int64_t dfull = work ? off[u + 1] - b : 0;
+        // a long list is cut into kAmsfChunk-entry pieces for k_amsf_chunks (any warp)
+        const bool big = dfull > kAmsfChunk;
+        if (big) {
+            const uint32_t nch = (uint32_t)((dfull + kAmsfChunk - 1) / kAmsfChunk);
+            const unsigned long long q = atomicAdd(&ac->chunks, (unsigned long long)nch);
+            for (uint32_t c = 0; c < nch; ++c) chq[q + c] = make_uint2(u, c);
+        }
+        const uint32_t d = big ? 0u : (uint32_t)dfull;
         uint32_t incl = d;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -364,8 +375,41 @@ __global__ void __launch_bounds__(kBlock) k_amsf_round(
     }
 }
 
+// The long lists of this round: one warp per kAmsfChunk-entry piece.
+template <int MODE>
+__global__ void __launch_bounds__(kBlock) k_amsf_chunks(const int64_t* __restrict__ off,
+                                                        const uint32_t* __restrict__ adj, const float* __restrict__ w,
+                                                        uint32_t* P, double blo, double bhi,
+                                                        const uint2* __restrict__ chq, const AmsfCtl* ac, uint2* F,
+                                                        float* Fw, cc_counters* cnt)
+{
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned long long total = ac->chunks;
+    const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    uint32_t hooks = 0;
+    unsigned long long scanned = 0;
+    for (unsigned long long q = warp; q < total; q += nwarps) {
+        const uint2 item = chq[q];
+        const int64_t b = off[item.x] + (int64_t)item.y * kAmsfChunk;
+        const int64_t e = min(off[item.x + 1], b + kAmsfChunk);
+        scanned += lane == 0 ? (unsigned long long)(e - b) : 0ull;
+        for (int64_t x = b + lane; x < e; x += 32) {
+            const float wx = w[x];
+            const double xd = (double)wx;
+            if (xd >= blo && xd < bhi) hooks += link<MODE>(P, item.x, adj[x], ForestW{F, Fw, wx});
+        }
+    }
+    if (cnt) {
+        warp_count(&cnt->amsf_hooks, hooks);
+        const unsigned long long sc = __reduce_add_sync(0xffffffffu, (uint32_t)min(scanned, 0xFFFFFFFFull));
+        if (lane == 0 && sc) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt->amsf_edges), sc);
+    }
+}
+
 __global__ void k_amsf_next(AmsfCtl* ac, int in_slot, cc_counters* cnt)
 {
+    ac->chunks = 0;
     ac->cnt[in_slot] = 0;                                      // becomes the next round's output
     if (cnt) {
         cnt->amsf_rounds += 1;
@@ -396,6 +440,7 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
     uint32_t *P = nullptr, *wlo = nullptr, *whi = nullptr, *fb = nullptr, *order = nullptr;
     uint32_t* carry[2] = {nullptr, nullptr};
     uint2* F = nullptr;
+    uint2* chq = nullptr;
     float* Fw = nullptr;
     double* bd = nullptr;
     unsigned long long *start = nullptr, *cursor = nullptr;
@@ -453,6 +498,8 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
             CC_CUDA_TRY(scratch_alloc((void**)&order, sizeof(uint32_t) * n, s));
             CC_CUDA_TRY(scratch_alloc((void**)&carry[0], sizeof(uint32_t) * n, s));
             CC_CUDA_TRY(scratch_alloc((void**)&carry[1], sizeof(uint32_t) * n, s));
+            // long-list pieces of one round: at most one per kAmsfChunk adjacency entries (+1 per vertex)
+            CC_CUDA_TRY(scratch_alloc((void**)&chq, sizeof(uint2) * (size_t)(m / kAmsfChunk + std::min<int64_t>(n, m / kAmsfChunk + 1) + 1), s));
             CC_CUDA_TRY(scratch_alloc((void**)&start, sizeof(unsigned long long) * (nb + 1), s));
             CC_CUDA_TRY(scratch_alloc((void**)&cursor, sizeof(unsigned long long) * (nb + 1), s));
             CC_CUDA_TRY(cudaMemsetAsync(start, 0, sizeof(unsigned long long) * (nb + 1), s));
@@ -474,8 +521,11 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
             }
             k_amsf_round<MODE><<<sms * 8, kBlock, 0, s>>>(off, adj, w, P, wlo, whi, order, start, i, b[i], b[i + 1],
                                                           carry[in_slot], ac, in_slot, carry[in_slot ^ 1],
-                                                          skip, plain, F, Fw, o.counters);
+                                                          skip, plain, F, Fw, chq, o.counters);
             CC_LAUNCH_CHECK("k_amsf_round");
+            k_amsf_chunks<MODE><<<sms * 8, kBlock, 0, s>>>(off, adj, w, P, b[i], b[i + 1], chq, ac, F, Fw,
+                                                           o.counters);
+            CC_LAUNCH_CHECK("k_amsf_chunks");
             k_amsf_next<<<1, 1, 0, s>>>(ac, in_slot, o.counters);
             CC_LAUNCH_CHECK("k_amsf_next");
         }
@@ -502,7 +552,7 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
     };
     const cc_status rc = body();
     for (void* p : {(void*)ac, (void*)P, (void*)wlo, (void*)whi, (void*)fb, (void*)order, (void*)carry[0],
-                    (void*)carry[1], (void*)F, (void*)Fw, (void*)bd, (void*)start, (void*)cursor, (void*)fcnt,
+                    (void*)carry[1], (void*)F, (void*)Fw, (void*)chq, (void*)bd, (void*)start, (void*)cursor, (void*)fcnt,
                     (void*)foff})
         scratch_free(p, s);
     return rc;
