@@ -94,6 +94,11 @@ typedef int cc_status;
                                           on C3/C4                               */
 #define CC_FLAG_NO_REFILL   (1u << 11) /* k-out links: one warp step per slowest lane (the
                                           round-1 kernel) instead of lane refill           */
+#define CC_FLAG_FINISH_CRFA (1u << 13) /* finish with the Liu-Tarjan CRFA rounds (Connect,
+                                          RootUp, FullShortcut, Alter)
+                                          instead of UF-Rem-CAS; one host sync per round.
+                                          (CC_FLAG_FINISH_SV is the root-based PRF instance:
+                                          ParentConnect + RootUp + FullShortcut)             */
 #define CC_FLAG_AMSF_PLAIN  (1u << 12) /* cc_amsf: inspect every edge of every non-skipped
                                           vertex in every round, as AMSF-NF-S is stated
                                           (P:1819-1822), instead of consulting the per-

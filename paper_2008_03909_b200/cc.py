@@ -34,6 +34,7 @@ FLAG_FINISH_SV = 1 << 9
 FLAG_CONTRACT = 1 << 10
 FLAG_NO_REFILL = 1 << 11
 FLAG_AMSF_PLAIN = 1 << 12
+FLAG_FINISH_CRFA = 1 << 13
 
 # every symbol include/cc.h and include/cc_bench.h declare
 EXPORTS = [

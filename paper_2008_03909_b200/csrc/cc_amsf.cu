@@ -159,17 +159,29 @@ __device__ __forceinline__ uint32_t bucket_of(const double* b, uint32_t nb, floa
 }
 
 // activation bucket of every non-isolated vertex (its lightest edge's bucket;
-// 0 in PLAIN mode) and the histogram of those buckets
+// 0 in PLAIN mode) and the histogram of those buckets: per block a shared-
+// memory histogram (when the buckets fit), one global atomic per non-empty bin
+constexpr uint32_t kSmemBins = 4096;
 __global__ void __launch_bounds__(kBlock) k_amsf_first(const uint32_t* wlo, const uint32_t* whi, uint32_t n,
                                                        const double* b, uint32_t nb, bool plain, uint32_t* fb,
                                                        unsigned long long* hist)
 {
+    __shared__ uint32_t sh[kSmemBins];
+    const bool local = nb <= kSmemBins;
+    if (local)
+        for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
     for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
         if (!whi[v]) continue;                                // isolated
         const uint32_t f = plain ? 0u : bucket_of(b, nb, __uint_as_float(wlo[v]));
         fb[v] = f;
-        atomicAdd(hist + f, 1ull);
+        if (local) atomicAdd(sh + f, 1u);
+        else atomicAdd(hist + f, 1ull);
     }
+    __syncthreads();
+    if (local)
+        for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x)
+            if (sh[i]) atomicAdd(hist + i, (unsigned long long)sh[i]);
 }
 
 // exclusive scan of the histogram (nb + 1 entries, one block)
@@ -200,12 +212,31 @@ __global__ void __launch_bounds__(kBlock) k_amsf_scan(unsigned long long* hist, 
     }
 }
 
+// order[] by activation bucket: per tile of kBlock vertices, ranks within the
+// block from shared atomics, one global range per non-empty bin and tile
 __global__ void __launch_bounds__(kBlock) k_amsf_scatter(const uint32_t* whi, const uint32_t* fb, uint32_t n,
-                                                         unsigned long long* cursor, uint32_t* order)
+                                                         uint32_t nb, unsigned long long* cursor, uint32_t* order)
 {
-    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
-        if (!whi[v]) continue;
-        order[atomicAdd(cursor + fb[v], 1ull)] = (uint32_t)v;
+    __shared__ uint32_t sc[kSmemBins];
+    __shared__ unsigned long long sb[kSmemBins];
+    const bool local = nb <= kSmemBins;
+    for (uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x; t0 < n; t0 += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t v = t0 + threadIdx.x;
+        const bool act = v < n && whi[v] != 0;
+        const uint32_t f = act ? fb[v] : 0u;
+        if (!local) {
+            if (act) order[atomicAdd(cursor + f, 1ull)] = (uint32_t)v;
+            continue;
+        }
+        // clear only the bins this tile touches
+        if (act) sc[f] = 0;
+        __syncthreads();
+        const uint32_t rank = act ? atomicAdd(sc + f, 1u) : 0u;
+        __syncthreads();
+        if (act && rank == 0) sb[f] = atomicAdd(cursor + f, (unsigned long long)sc[f]);
+        __syncthreads();
+        if (act) order[sb[f] + rank] = (uint32_t)v;
+        __syncthreads();
     }
 }
 
@@ -344,25 +375,32 @@ __global__ void __launch_bounds__(kBlock) k_amsf_round(
         const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
         const uint32_t excl = incl - d;
         scanned += lane == 0 ? tot : 0u;
-        for (uint32_t t0 = 0; t0 < tot; t0 += 32) {
-            const uint32_t t = t0 + lane;
-            int lo = 0;
+        // 4 entries per lane per sweep step: owners by shuffle search, then the 4 weight
+        // loads in flight together
+        for (uint32_t t0 = 0; t0 < tot; t0 += 128) {
+            uint32_t ou[4];
+            int64_t ex[4];
+            float x[4];
 #pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                const uint32_t pe = __shfl_sync(0xffffffffu, excl, lo + step);
-                if (pe <= t) lo += step;
-            }
-            const uint32_t ou = __shfl_sync(0xffffffffu, u, lo);
-            const int64_t ob = __shfl_sync(0xffffffffu, b, lo);
-            const uint32_t oex = __shfl_sync(0xffffffffu, excl, lo);
-            if (t < tot) {
-                const int64_t e = ob + (t - oex);
-                const float x = w[e];
-                const double xd = (double)x;
-                if (xd >= blo && xd < bhi) {
-                    const uint32_t v = adj[e];
-                    hooks += link<MODE>(P, ou, v, ForestW{F, Fw, x});
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t t = t0 + 32 * j + lane;
+                int lo = 0;
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1) {
+                    const uint32_t pe = __shfl_sync(0xffffffffu, excl, lo + step);
+                    if (pe <= t) lo += step;
                 }
+                ou[j] = __shfl_sync(0xffffffffu, u, lo);
+                const int64_t ob = __shfl_sync(0xffffffffu, b, lo);
+                const uint32_t oex = __shfl_sync(0xffffffffu, excl, lo);
+                ex[j] = t < tot ? ob + (t - oex) : -1;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) x[j] = ex[j] >= 0 ? w[ex[j]] : 0.0f;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const double xd = (double)x[j];
+                if (ex[j] >= 0 && xd >= blo && xd < bhi) hooks += link<MODE>(P, ou[j], adj[ex[j]], ForestW{F, Fw, x[j]});
             }
             __syncwarp();
         }
@@ -394,10 +432,17 @@ __global__ void __launch_bounds__(kBlock) k_amsf_chunks(const int64_t* __restric
         const int64_t b = off[item.x] + (int64_t)item.y * kAmsfChunk;
         const int64_t e = min(off[item.x + 1], b + kAmsfChunk);
         scanned += lane == 0 ? (unsigned long long)(e - b) : 0ull;
-        for (int64_t x = b + lane; x < e; x += 32) {
-            const float wx = w[x];
-            const double xd = (double)wx;
-            if (xd >= blo && xd < bhi) hooks += link<MODE>(P, item.x, adj[x], ForestW{F, Fw, wx});
+        // 8 weight loads in flight per lane (the sweep is latency-bound otherwise)
+        for (int64_t x0 = b + lane; x0 < e; x0 += 32 * 8) {
+            float wx[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) wx[j] = x0 + 32 * j < e ? w[x0 + 32 * j] : 0.0f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const double xd = (double)wx[j];
+                if (xd >= blo && xd < bhi)
+                    hooks += link<MODE>(P, item.x, adj[x0 + 32 * j], ForestW{F, Fw, wx[j]});
+            }
         }
     }
     if (cnt) {
@@ -509,7 +554,7 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
             k_amsf_scan<<<1, kBlock, 0, s>>>(start, nb);
             CC_LAUNCH_CHECK("k_amsf_scan");
             CC_CUDA_TRY(cudaMemcpyAsync(cursor, start, sizeof(unsigned long long) * (nb + 1), cudaMemcpyDeviceToDevice, s));
-            k_amsf_scatter<<<sms * 8, kBlock, 0, s>>>(whi, fb, n, cursor, order);
+            k_amsf_scatter<<<sms * 8, kBlock, 0, s>>>(whi, fb, n, nb, cursor, order);
             CC_LAUNCH_CHECK("k_amsf_scatter");
         }
         // the rounds: bucket i = [b_i, b_(i+1)), lightest first

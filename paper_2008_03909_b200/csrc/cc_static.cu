@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <type_traits>
 
 #include "cc_common.cuh"
 #include "cc_device.cuh"
@@ -1099,10 +1100,89 @@ __global__ void __launch_bounds__(kBlock) k_sv_record(const uint32_t* P, const u
     }
 }
 
+// Liu-Tarjan CRFA (the framework of P:866-905 / P:4019-4048): each round
+// Connect (the endpoints of an edge are candidates for each other), RootUp (only a
+// vertex that is a root at the start of the round takes a candidate), FullShortcut,
+// then Alter (every edge is replaced by the labels of its endpoints; edges that
+// became self-loops are dropped, so the edge list shrinks round by round).  Every
+// update is a writeMin.  Edges: uint4 (a, b, u, v) = current endpoints + the input
+// edge (for the forest record); without SF only (a, b) is kept.
+template <bool SF>
+using LtEdge = typename std::conditional<SF, uint4, uint2>::type;
+
+template <bool SF>
+__global__ void __launch_bounds__(kBlock) k_lt_init(const uint2* __restrict__ e, unsigned long long ne, LtEdge<SF>* out)
+{
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < ne;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const uint2 x = e[i];
+        if constexpr (SF) out[i] = make_uint4(x.x, x.y, x.x, x.y);
+        else out[i] = x;
+    }
+}
+
+template <bool SF>
+__global__ void __launch_bounds__(kBlock) k_lt_connect(uint32_t* P, const LtEdge<SF>* __restrict__ e,
+                                                       const unsigned long long* ne, const uint32_t* __restrict__ bits,
+                                                       unsigned int* changed)
+{
+    unsigned int ch = 0;
+    const unsigned long long total = *ne;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const LtEdge<SF> x = e[i];
+        const uint32_t h = max(x.x, x.y), l = min(x.x, x.y);
+        if (h == l || !((bits[h >> 5] >> (h & 31)) & 1u)) continue;     // RootUp: h a root at round start
+        ch |= atomicMin(P + h, l) > l ? 1u : 0u;                          // Connect, writeMin
+    }
+    if (__any_sync(0xffffffffu, ch != 0) && (threadIdx.x & 31) == 0) atomicOr(changed, 1u);
+}
+
+// SF: the edge whose candidate won at h (P[h] == l after the connect phase)
+__global__ void __launch_bounds__(kBlock) k_lt_record(const uint32_t* P, const uint4* __restrict__ e,
+                                                      const unsigned long long* ne, const uint32_t* __restrict__ bits,
+                                                      uint2* F)
+{
+    const unsigned long long total = *ne;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const uint4 x = e[i];
+        const uint32_t h = max(x.x, x.y), l = min(x.x, x.y);
+        if (h == l || !((bits[h >> 5] >> (h & 31)) & 1u)) continue;
+        if (P[h] == l) F[h] = make_uint2(x.z, x.w);
+    }
+}
+
+// Alter after the FullShortcut (P[x] is x's root): keep (P[a], P[b]) unless equal
+template <bool SF>
+__global__ void __launch_bounds__(kBlock) k_lt_alter(const uint32_t* P, const LtEdge<SF>* __restrict__ e,
+                                                     const unsigned long long* ne, LtEdge<SF>* out,
+                                                     unsigned long long* ne_out)
+{
+    const unsigned long long total = *ne;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x; base < total; base += stride) {
+        const unsigned long long i = base + threadIdx.x;
+        LtEdge<SF> x{};
+        bool keep = false;
+        if (i < total) {
+            x = e[i];
+            x.x = P[x.x];
+            x.y = P[x.y];
+            keep = x.x != x.y;
+        }
+        const unsigned long long pos = warp_append(ne_out, keep ? 1u : 0u);
+        if (keep) out[pos] = x;
+    }
+}
+
 template <bool SF>
 static cc_status sv_finish(const int64_t* off, const uint32_t* adj, uint32_t* P, uint32_t n, const uint32_t* cq,
-                           Ctl* ctl, uint32_t skip_prefix, uint2* F, cc_counters* cnt, cudaStream_t s)
+                           Ctl* ctl, uint32_t skip_prefix, uint2* F, cc_counters* cnt, cudaStream_t s,
+                           bool crfa = false)
 {
+    void* le[2] = {nullptr, nullptr};
+    unsigned long long* lcnt = nullptr;
     unsigned long long cand = 0;
     CC_CUDA_TRY(cudaMemcpyAsync(&cand, &ctl->cand_count, sizeof(cand), cudaMemcpyDeviceToHost, s));
     CC_CUDA_TRY(cudaStreamSynchronize(s));
@@ -1134,6 +1214,40 @@ static cc_status sv_finish(const int64_t* off, const uint32_t* adj, uint32_t* P,
         k_sv_fill<<<(unsigned)nbk, kBlock, 0, s>>>(off, adj, cq, deg, bsum, cand, skip_prefix, edges);
         CC_LAUNCH_CHECK("k_sv_fill");
         const unsigned nbv = (unsigned)(((uint64_t)n + kBlock - 1) / kBlock);
+        if (crfa) {
+            // Liu-Tarjan CRFA: rounds until Alter leaves no edge
+            CC_CUDA_TRY(scratch_alloc((void**)&le[0], sizeof(LtEdge<SF>) * ne, s));
+            CC_CUDA_TRY(scratch_alloc((void**)&le[1], sizeof(LtEdge<SF>) * ne, s));
+            CC_CUDA_TRY(scratch_alloc((void**)&lcnt, 2 * sizeof(unsigned long long), s));
+            k_lt_init<SF><<<sms * 8, kBlock, 0, s>>>(edges, ne, (LtEdge<SF>*)le[0]);
+            CC_LAUNCH_CHECK("k_lt_init");
+            CC_CUDA_TRY(cudaMemcpyAsync(lcnt, &ne, sizeof(ne), cudaMemcpyHostToDevice, s));
+            for (uint64_t round = 1;; ++round) {
+                const int a = (round - 1) & 1;
+                k_sv_rootbits<<<nbv, kBlock, 0, s>>>(P, n, bits);
+                CC_LAUNCH_CHECK("k_sv_rootbits(LT)");
+                CC_CUDA_TRY(cudaMemsetAsync(changed, 0, sizeof(unsigned int), s));
+                k_lt_connect<SF><<<sms * 8, kBlock, 0, s>>>(P, (const LtEdge<SF>*)le[a], lcnt + a, bits, changed);
+                CC_LAUNCH_CHECK("k_lt_connect");
+                if constexpr (SF) {
+                    k_lt_record<<<sms * 8, kBlock, 0, s>>>(P, (const uint4*)le[a], lcnt + a, bits, F);
+                    CC_LAUNCH_CHECK("k_lt_record");
+                }
+                cc_status r = launch_compress(P, n, nullptr, nullptr, s, "k_compress(LT FullShortcut)");
+                if (r) return r;
+                CC_CUDA_TRY(cudaMemsetAsync(lcnt + (a ^ 1), 0, sizeof(unsigned long long), s));
+                k_lt_alter<SF><<<sms * 8, kBlock, 0, s>>>(P, (const LtEdge<SF>*)le[a], lcnt + a, (LtEdge<SF>*)le[a ^ 1],
+                                                          lcnt + (a ^ 1));
+                CC_LAUNCH_CHECK("k_lt_alter");
+                unsigned long long left = 0;
+                CC_CUDA_TRY(cudaMemcpyAsync(&left, lcnt + (a ^ 1), sizeof(left), cudaMemcpyDeviceToHost, s));
+                CC_CUDA_TRY(cudaStreamSynchronize(s));
+                if (cnt) CC_CUDA_TRY(cudaMemcpyAsync(&cnt->sv_rounds, &round, sizeof(round), cudaMemcpyHostToDevice, s));
+                if (!left) break;
+            }
+            CC_CUDA_TRY(cudaStreamSynchronize(s));
+            return CC_OK;
+        }
         for (uint64_t round = 1;; ++round) {
             k_sv_rootbits<<<nbv, kBlock, 0, s>>>(P, n, bits);        // prev_labels[h] == h
             CC_LAUNCH_CHECK("k_sv_rootbits");
@@ -1162,6 +1276,9 @@ static cc_status sv_finish(const int64_t* off, const uint32_t* adj, uint32_t* P,
     scratch_free(edges, s);
     scratch_free(bits, s);
     scratch_free(changed, s);
+    scratch_free(le[0], s);
+    scratch_free(le[1], s);
+    scratch_free(lcnt, s);
     return rc;
 }
 
@@ -1382,8 +1499,9 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
             CC_LAUNCH_CHECK("k_finish");
         }
         CC_CUDA_TRY(mark(CC_MARK_FINISH));
-        if (o.flags & CC_FLAG_FINISH_SV) {
-            cc_status r = sv_finish<SF>(off, adj, P, n, cq, ctl, skip_prefix, F, o.counters, s);
+        if (o.flags & (CC_FLAG_FINISH_SV | CC_FLAG_FINISH_CRFA)) {
+            cc_status r = sv_finish<SF>(off, adj, P, n, cq, ctl, skip_prefix, F, o.counters, s,
+                                        (o.flags & CC_FLAG_FINISH_CRFA) != 0);
             if (r) return r;
         } else {
             k_finish_proc<MODE, SF><<<sms * 8, kBlock, 0, s>>>(off, adj, P, cq, ctl, skip_prefix, big, F, o.counters);

@@ -47,6 +47,10 @@ OPTION_GRID = [
     dict(k=2, variant="pure", flags=cc.FLAG_CONTRACT | cc.FLAG_UF_ASYNC, seed=9),
     dict(k=2, variant="afforest", flags=cc.FLAG_NO_REFILL),
     dict(k=3, variant="hybrid", flags=cc.FLAG_NO_REFILL, seed=3),
+    # Liu-Tarjan CRFA finish (NEXT-3)
+    dict(k=2, variant="afforest", flags=cc.FLAG_FINISH_CRFA),
+    dict(k=0, variant="afforest", flags=cc.FLAG_FINISH_CRFA),
+    dict(k=1, variant="hybrid", flags=cc.FLAG_FINISH_CRFA | cc.FLAG_NO_SKIP, seed=3),
 ]
 
 
@@ -205,6 +209,8 @@ def test_empty_and_degenerate_abi():
                                  dict(k=2, variant="afforest", flags=cc.FLAG_CONTRACT),
                                  dict(k=3, variant="pure", flags=cc.FLAG_CONTRACT | cc.FLAG_HALVE, seed=4),
                                  dict(k=2, variant="afforest", flags=cc.FLAG_NO_REFILL),
+                                 dict(k=2, variant="afforest", flags=cc.FLAG_FINISH_CRFA),
+                                 dict(k=0, variant="afforest", flags=cc.FLAG_FINISH_CRFA),
                                  dict(k=1, variant="hybrid", flags=0, seed=6)],
                          ids=lambda o: f"k{o['k']}-{o['variant']}-f{o['flags']}")
 def test_spanning_forest_valid(opt):
@@ -241,7 +247,8 @@ def test_repeat_stress_random_options():
     rng = np.random.default_rng(1)
     d_off, d_adj = to_dev(off, adj)
     flags_pool = [0, cc.FLAG_HALVE, cc.FLAG_UF_ASYNC, cc.FLAG_NO_SKIP, cc.FLAG_NO_MIDCOMPRESS, cc.FLAG_NO_DEGSKIP,
-                  cc.FLAG_MIDCOMPRESS, cc.FLAG_FINISH_SV, cc.FLAG_CONTRACT, cc.FLAG_NO_REFILL]
+                  cc.FLAG_MIDCOMPRESS, cc.FLAG_FINISH_SV, cc.FLAG_CONTRACT, cc.FLAG_NO_REFILL,
+                  cc.FLAG_FINISH_CRFA]
     for it in range(200):
         k = int(rng.integers(0, 5))
         variant = ["afforest", "hybrid", "pure"][int(rng.integers(0, 3))]
