@@ -104,3 +104,60 @@ def test_amsf_c3_bucket_counts():
                           np.bincount(want["buckets"], minlength=want["nbuckets"]))
     assert tot == pytest.approx(float(W.astype(np.float64).sum()), rel=1e-12)
     print(f"C3 AMSF: n={n} forest={E.shape[0]} W={tot:.6g} oracle W={want['total']:.6g} buckets={want['nbuckets']}")
+
+
+def test_maximum_n_labels_and_forest():
+    """n = 0xFFFFFFFE, the largest the ABI accepts (uint32 ids, 0xFFFFFFFF is the
+    sentinel): every grid, tile tail and 32/64-bit index path at its limit.
+    A few edges join vertices at both ends of the id range; everything else is
+    isolated.  (34 GB offsets + 17 GB labels + scratch, on one B200.)"""
+    n = 0xFFFFFFFE
+    pairs = [(0, n - 1), (n - 1, 1 << 31), (1 << 31, (1 << 31) + 1), ((1 << 31) + 1, 12345), (n - 2, n - 3),
+             (1 << 32 - 2, 7)]
+    adjl = {}
+    for a, b in pairs:
+        adjl.setdefault(a, []).append(b)
+        adjl.setdefault(b, []).append(a)
+    verts = sorted(adjl)
+    adj = np.array([x for v in verts for x in sorted(adjl[v])], dtype=np.uint32)
+    off = torch.zeros(n + 1, dtype=torch.int64, device="cuda")
+    acc = 0
+    for v in verts:                                       # off[v+1:] += deg(v), as a step function
+        acc_next = acc + len(adjl[v])
+        off[v + 1:] += len(adjl[v])
+        acc = acc_next
+    d_adj = torch.from_numpy(adj.view(np.int32)).cuda()
+    lab = pkg.connected_components(off, d_adj)
+    torch.cuda.synchronize()
+    # expected: min id per component
+    comp = {}
+    par = {v: v for v in verts}
+
+    def find(x):
+        while par[x] != x:
+            x = par[x]
+        return x
+    for a, b in pairs:
+        ra, rb = find(a), find(b)
+        if ra != rb:
+            par[max(ra, rb)] = min(ra, rb)
+    for v in verts:
+        comp[v] = find(v)
+    got = {v: int(np.uint32(lab[v].item() & 0xFFFFFFFF)) for v in verts}
+    assert got == comp, (got, comp)
+    # everything else is its own label: count the non-identity slots chunk by chunk
+    moved = 0
+    step = 1 << 30
+    for s0 in range(0, n, step):
+        s1 = min(n, s0 + step)
+        ids = torch.arange(s0, s1, dtype=torch.int64, device="cuda")
+        moved += int(((lab[s0:s1].to(torch.int64) & 0xFFFFFFFF) != ids).sum().item())
+        del ids
+    assert moved == sum(1 for v in verts if comp[v] != v)
+    del lab
+    torch.cuda.empty_cache()
+    edges, lab2 = pkg.spanning_forest(off, d_adj, with_labels=False)
+    E = u32(edges).reshape(-1, 2)
+    assert E.shape[0] == sum(1 for v in verts if comp[v] != v)
+    for a, b in E.tolist():
+        assert b in adjl[a] and find(a) == find(b)
