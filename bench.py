@@ -235,8 +235,9 @@ def byte_model(off_h_deg_pos, n, m, k, ctr, sampled, final, mid_ran, f0=None):
         "k_finish": 4 * n + n // 8 + 4 * ctr["finish_gathers"] + 4 * ctr["compress_writes"] + 4 * fin_v,
         # H5 edge work: queue read + offsets pair + adj + P[v] gather per edge + hook CAS
         "k_finish_proc": 4 * fin_v + 16 * fin_v + 8 * fin_e + 4 * ctr["finish_hooks"],
-        # P read + first-level parent reads + changed-label writes
-        "k_compress_H6": 4 * n + 4 * ctr["h6_gathers"] + 4 * ctr["h6_writes"],
+        # P read + changed-label writes (its root checks P[P[v]] land on the few root slots
+        # of the non-isolated vertices -- L2 hits, not counted)
+        "k_compress_H6": 4 * n + 4 * ctr["h6_writes"],
     }
     if f0 is not None:
         # contracted link: + the F0-root bitmap words in k_sample_init;
