@@ -531,7 +531,7 @@ def run_ours_incr(a, rank, ws, cfg):
     stream = torch.cuda.current_stream()
 
     def stream_once(ev=None):
-        h = cc.Incr(n)
+        h = cc.Incr(n, flags=a.flags)
         for b in range(nb):
             if ev is not None:
                 ev[b][0].record(stream)

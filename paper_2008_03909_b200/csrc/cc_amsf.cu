@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(kBlock) k_amsf_round(
 }
 
 // The long lists of this round: one warp per kAmsfChunk-entry piece.
-template <int MODE>
+template <int MODE, bool VEC>
 __global__ void __launch_bounds__(kBlock) k_amsf_chunks(const int64_t* __restrict__ off,
                                                         const uint32_t* __restrict__ adj, const float* __restrict__ w,
                                                         uint32_t* P, double blo, double bhi,
@@ -432,16 +432,39 @@ __global__ void __launch_bounds__(kBlock) k_amsf_chunks(const int64_t* __restric
         const int64_t b = off[item.x] + (int64_t)item.y * kAmsfChunk;
         const int64_t e = min(off[item.x + 1], b + kAmsfChunk);
         scanned += lane == 0 ? (unsigned long long)(e - b) : 0ull;
-        // 8 weight loads in flight per lane (the sweep is latency-bound otherwise)
-        for (int64_t x0 = b + lane; x0 < e; x0 += 32 * 8) {
-            float wx[8];
+        if (VEC) {
+            // 16-byte weight loads from the aligned quad containing b: 4 in flight per lane
+            // (16 weights), entries outside [b, e) ignored
+            const float4* w4 = reinterpret_cast<const float4*>(w);
+            for (int64_t q0 = (b >> 2) + lane; q0 * 4 < e; q0 += 32 * 4) {
+                float4 wq[4];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) wx[j] = x0 + 32 * j < e ? w[x0 + 32 * j] : 0.0f;
+                for (int j = 0; j < 4; ++j)
+                    wq[j] = (q0 + 32 * j) * 4 < e ? w4[q0 + 32 * j] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const double xd = (double)wx[j];
-                if (xd >= blo && xd < bhi)
-                    hooks += link<MODE>(P, item.x, adj[x0 + 32 * j], ForestW{F, Fw, wx[j]});
+                for (int j = 0; j < 4; ++j) {
+                    const float v4[4] = {wq[j].x, wq[j].y, wq[j].z, wq[j].w};
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const int64_t x = (q0 + 32 * j) * 4 + c;
+                        const double xd = (double)v4[c];
+                        if (x >= b && x < e && xd >= blo && xd < bhi)
+                            hooks += link<MODE>(P, item.x, adj[x], ForestW{F, Fw, v4[c]});
+                    }
+                }
+            }
+        } else {
+            // 8 weight loads in flight per lane (the sweep is latency-bound otherwise)
+            for (int64_t x0 = b + lane; x0 < e; x0 += 32 * 8) {
+                float wx[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) wx[j] = x0 + 32 * j < e ? w[x0 + 32 * j] : 0.0f;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const double xd = (double)wx[j];
+                    if (xd >= blo && xd < bhi)
+                        hooks += link<MODE>(P, item.x, adj[x0 + 32 * j], ForestW{F, Fw, wx[j]});
+                }
             }
         }
     }
@@ -568,8 +591,12 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
                                                           carry[in_slot], ac, in_slot, carry[in_slot ^ 1],
                                                           skip, plain, F, Fw, chq, o.counters);
             CC_LAUNCH_CHECK("k_amsf_round");
-            k_amsf_chunks<MODE><<<sms * 8, kBlock, 0, s>>>(off, adj, w, P, b[i], b[i + 1], chq, ac, F, Fw,
-                                                           o.counters);
+            if (((uintptr_t)w & 15u) == 0)
+                k_amsf_chunks<MODE, true><<<sms * 8, kBlock, 0, s>>>(off, adj, w, P, b[i], b[i + 1], chq, ac, F, Fw,
+                                                                     o.counters);
+            else
+                k_amsf_chunks<MODE, false><<<sms * 8, kBlock, 0, s>>>(off, adj, w, P, b[i], b[i + 1], chq, ac, F,
+                                                                      Fw, o.counters);
             CC_LAUNCH_CHECK("k_amsf_chunks");
             k_amsf_next<<<1, 1, 0, s>>>(ac, in_slot, o.counters);
             CC_LAUNCH_CHECK("k_amsf_next");

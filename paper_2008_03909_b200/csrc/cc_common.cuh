@@ -7,6 +7,7 @@
 
 #include <cstdint>
 
+#include "cc_device.cuh"
 #include "cc_internal.h"
 
 namespace ccb {
@@ -128,6 +129,115 @@ static __global__ void __launch_bounds__(kBlock) k_forest_write(const uint2* F, 
             if (out_w) out_w[o] = Fw[base + j];
             ++o;
         }
+}
+
+// ---------------------------------------------------------------------------
+// K1': UF-Rem-CAS + SplitAtomicOne links with lane refill (the static k-out link
+// and the incremental insert phase).
+//
+// The link kernel is latency-bound: every Rem-loop step is a dependent random
+// load, and in k_link_pending a warp keeps stepping until its slowest lane's
+// link is done, so on average half the lanes idle (ncu: 15 of 32 threads per
+// instruction).  Here each warp streams its pending links through a 32-entry
+// register buffer (one coalesced pend load + the P[u], P[v] gathers of all 32
+// entries, issued one buffer ahead so they are in flight while the current one
+// is consumed); a lane whose link finished takes the next buffered entry by a
+// shuffle, and entries whose first parents are already equal retire without
+// occupying a lane.  Every loop iteration then does one Rem step (one load, or
+// a CAS) on every lane that holds a link.  The step is exactly link_rem_from's
+// iteration (readings R1, R6), so the result is the same partition.
+#ifndef CC_REFILL_MINB
+#define CC_REFILL_MINB 6
+#endif
+// The link count is *count_dev when given (the static path: k_sample_init's
+// append counter), else count_host (an incremental batch).
+template <bool SF>
+static __global__ void __launch_bounds__(kBlock, CC_REFILL_MINB) k_link_refill(
+    uint32_t* P, const uint2* __restrict__ pend, const unsigned long long* count_dev, unsigned long long count_host,
+    uint2* F, cc_counters* cnt)
+{
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const unsigned long long total = count_dev ? *count_dev : count_host;
+    const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    unsigned long long chunk = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    // next buffer: entry chunk*32 + lane with its first two parent reads in flight
+    uint2 nb = make_uint2(0u, 0u);
+    uint32_t npu = 0, npv = 0, navail = 0;
+    auto fetch = [&]() {
+        const unsigned long long b0 = chunk * 32;
+        navail = b0 < total ? (uint32_t)min(32ull, total - b0) : 0u;
+        const bool ok = lane < navail;
+        nb = ok ? pend[b0 + lane] : make_uint2(0u, 0u);
+        npu = ok ? ld_relaxed(P + nb.x) : 0u;
+        npv = ok ? ld_relaxed(P + nb.y) : 0u;
+        chunk += nwarps;
+    };
+    fetch();
+    uint2 cb = nb;
+    uint32_t cpu = npu, cpv = npv, cavail = navail, cpos = 0;
+    if (cavail) fetch();
+    bool act = false;
+    uint32_t u = 0, v = 0, ru = 0, rv = 0, pu = 0, pv = 0;
+    uint32_t hooked = 0, steps = 0, fails = 0;
+    while (true) {
+        // refill idle lanes from the buffer (warp-uniform loop)
+        unsigned need = __ballot_sync(0xffffffffu, !act);
+        while (need && cavail) {
+            const uint32_t src = cpos + __popc(need & lt_mask);
+            const uint32_t sl = src & 31;
+            const uint32_t xu = __shfl_sync(0xffffffffu, cb.x, sl), xv = __shfl_sync(0xffffffffu, cb.y, sl);
+            const uint32_t xpu = __shfl_sync(0xffffffffu, cpu, sl), xpv = __shfl_sync(0xffffffffu, cpv, sl);
+            if (!act && src < cavail && xpu != xpv) {        // equal first parents: already one set
+                act = true;
+                u = ru = xu;
+                v = rv = xv;
+                pu = xpu;
+                pv = xpv;
+            }
+            cpos = min(cavail, cpos + (uint32_t)__popc(need));
+            if (cpos == cavail) {                            // buffer used up: rotate in the prefetched one
+                cb = nb;
+                cpu = npu;
+                cpv = npv;
+                cavail = navail;
+                cpos = 0;
+                if (cavail) fetch();
+            }
+            need = __ballot_sync(0xffffffffu, !act);
+        }
+        if (!__any_sync(0xffffffffu, act)) break;           // buffer empty and every link done
+        if (act) {                                           // one iteration of link_rem_from
+            ++steps;
+            if (pu < pv) {
+                uint32_t t = ru; ru = rv; rv = t;
+                t = pu; pu = pv; pv = t;
+            }
+            if (ru == pu) {                                  // ru is a root: hook it under pv
+                const uint32_t old = cas(P + ru, ru, pv);
+                if (old == ru) {
+                    if (SF) F[ru] = make_uint2(u, v);
+                    ++hooked;
+                    act = false;
+                } else {
+                    ++fails;
+                    pu = old;
+                    pv = ld_relaxed(P + rv);
+                }
+            } else {
+                const uint32_t w = ld_relaxed(P + pu);       // SplitAtomicOne on ru
+                if (w != pu) cas(P + ru, pu, w);
+                ru = pu;
+                pu = w;
+            }
+            if (act && pu == pv) act = false;
+        }
+    }
+    if (cnt) {
+        warp_count(&cnt->sample_hooks, hooked);
+        warp_count(&cnt->link_steps, steps);
+        warp_count(&cnt->cas_failures, fails);
+    }
 }
 
 }  // namespace ccb

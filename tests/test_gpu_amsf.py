@@ -161,3 +161,14 @@ def test_amsf_repeat_stress():
     for it in range(40):
         opt = OPTS[int(rng.integers(0, len(OPTS)))]
         check(off, adj, w, 0.25, *run(off, adj, w, 0.25, **opt), want=want, exact_opt=(it % 10 == 0))
+
+
+def test_amsf_unaligned_weights():
+    """A weight buffer that is not 16-byte aligned takes the scalar sweep."""
+    off, adj = gen.rmat(seed=12, scale=13)
+    w = gen.exp_weights(off, adj, 12)
+    d_off, d_adj = to_dev(off, adj)
+    buf = torch.empty(adj.size + 1, dtype=torch.float32, device="cuda")
+    buf[1:] = torch.from_numpy(w).cuda()
+    E, W, tot = pkg.amsf(d_off, d_adj, buf[1:], 0.25)
+    check(off, adj, w, 0.25, u32(E).reshape(-1, 2), W.cpu().numpy(), tot)
