@@ -735,8 +735,8 @@ def run_amsf(a):
     from inputs import gpu as ggen
     from paper_2008_03909_b200 import cc
     stream = torch.cuda.current_stream()
-    variants = [("nf_s_range", 0), ("nf_s_plain", cc.FLAG_AMSF_PLAIN), ("nf_range", cc.FLAG_NO_SKIP),
-                ("nf_plain", cc.FLAG_AMSF_PLAIN | cc.FLAG_NO_SKIP)]
+    variants = [("nf_s_index", 0), ("nf_s_range", cc.FLAG_AMSF_NO_INDEX), ("nf_s_plain", cc.FLAG_AMSF_PLAIN),
+                ("nf_index", cc.FLAG_NO_SKIP), ("nf_plain", cc.FLAG_AMSF_PLAIN | cc.FLAG_NO_SKIP)]
     rows = []
     for cfg in (inputs.C3, inputs.C4):
         d_off, d_adj = ggen.config_graph(cfg)
@@ -767,12 +767,16 @@ def run_amsf(a):
             # algorithmic bytes: one weight per inspected entry, the endpoint of every
             # in-bucket entry (<= m), offsets + weight range per visit
             byts = 4 * c["amsf_edges"] + 4 * m + 24 * c["amsf_visits"]
+            peak, _ = peaks()
             rows.append({"workload": cfg.name, "variant": name, "flags": flags, "eps": a.eps, "ms": round(ms, 3),
                          "GTEPS": round(m / (ms * 1e-3) / 1e9, 2), "rounds": c["amsf_rounds"],
                          "visits": c["amsf_visits"], "weights_inspected": c["amsf_edges"],
                          "inspected_per_entry": round(c["amsf_edges"] / m, 3), "forest_edges": int(num.item()),
                          "forest_weight": float(tot.item()), "rebuilds": c["amsf_rebuilds"],
-                         "algorithmic_GBps": round(byts / (ms * 1e-3) / 1e9, 1)})
+                         "algorithmic_GBps": round(byts / (ms * 1e-3) / 1e9, 1),
+                         "roofline": {"bound": "hbm", "achieved": round(byts / (ms * 1e-3) / 1e9, 1), "peak": peak,
+                                      "unit": "GB/s", "frac": round(byts / (ms * 1e-3) / 1e9 / peak, 4),
+                                      "bytes": int(byts)}})
             print(json.dumps(rows[-1]), file=sys.stderr, flush=True)
         del d_off, d_adj, d_w, edges, ew
         torch.cuda.empty_cache()

@@ -99,6 +99,9 @@ typedef int cc_status;
                                           instead of UF-Rem-CAS; one host sync per round.
                                           (CC_FLAG_FINISH_SV is the root-based PRF instance:
                                           ParentConnect + RootUp + FullShortcut)             */
+#define CC_FLAG_AMSF_NO_INDEX (1u << 14) /* cc_amsf: scan the whole list of a long (> 2048
+                                          entries) list every active round instead of only
+                                          its current bucket's entries (hub bucket index)   */
 #define CC_FLAG_AMSF_PLAIN  (1u << 12) /* cc_amsf: inspect every edge of every non-skipped
                                           vertex in every round, as AMSF-NF-S is stated
                                           (P:1819-1822), instead of consulting the per-

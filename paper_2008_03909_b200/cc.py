@@ -35,6 +35,7 @@ FLAG_CONTRACT = 1 << 10
 FLAG_NO_REFILL = 1 << 11
 FLAG_AMSF_PLAIN = 1 << 12
 FLAG_FINISH_CRFA = 1 << 13
+FLAG_AMSF_NO_INDEX = 1 << 14
 
 # every symbol include/cc.h and include/cc_bench.h declare
 EXPORTS = [

@@ -162,6 +162,7 @@ __device__ __forceinline__ uint32_t bucket_of(const double* b, uint32_t nb, floa
 // 0 in PLAIN mode) and the histogram of those buckets: per block a shared-
 // memory histogram (when the buckets fit), one global atomic per non-empty bin
 constexpr uint32_t kSmemBins = 4096;
+constexpr uint32_t kIdxBins = 4000;      // the hub bucket index is built when nb <= this
 __global__ void __launch_bounds__(kBlock) k_amsf_first(const uint32_t* wlo, const uint32_t* whi, uint32_t n,
                                                        const double* b, uint32_t nb, bool plain, uint32_t* fb,
                                                        unsigned long long* hist)
@@ -326,7 +327,8 @@ __global__ void __launch_bounds__(kBlock) k_amsf_round(
     const uint32_t* __restrict__ wlo, const uint32_t* __restrict__ whi, const uint32_t* __restrict__ order,
     const unsigned long long* __restrict__ start, uint32_t round, double blo, double bhi,
     const uint32_t* __restrict__ carry_in, AmsfCtl* ac, int in_slot, uint32_t* carry_out, bool skip, bool plain,
-    uint2* F, float* Fw, uint2* chq, cc_counters* cnt)
+    uint2* F, float* Fw, uint2* chq, const uint32_t* __restrict__ hid, const uint32_t* __restrict__ hstart,
+    uint32_t nbk, cc_counters* cnt)
 {
     const unsigned lane = threadIdx.x & 31;
     const bool rebuild = ac->rebuild != 0;
@@ -361,8 +363,14 @@ __global__ void __launch_bounds__(kBlock) k_amsf_round(
         // a long list is cut into kAmsfChunk-entry pieces for k_amsf_chunks (any warp)
         const bool big = dfull > kAmsfChunk;
         if (big) {
-            const uint32_t nch = (uint32_t)((dfull + kAmsfChunk - 1) / kAmsfChunk);
-            const unsigned long long q = atomicAdd(&ac->chunks, (unsigned long long)nch);
+            // with the hub index: only this bucket's entries of the hub, else its whole list
+            int64_t len = dfull;
+            if (hstart) {
+                const uint32_t* hs = hstart + (uint64_t)hid[u] * (nbk + 1);
+                len = (int64_t)hs[round + 1] - (int64_t)hs[round];
+            }
+            const uint32_t nch = (uint32_t)((len + kAmsfChunk - 1) / kAmsfChunk);
+            const unsigned long long q = nch ? atomicAdd(&ac->chunks, (unsigned long long)nch) : 0ull;
             for (uint32_t c = 0; c < nch; ++c) chq[q + c] = make_uint2(u, c);
         }
         const uint32_t d = big ? 0u : (uint32_t)dfull;
@@ -410,6 +418,147 @@ __global__ void __launch_bounds__(kBlock) k_amsf_round(
         warp_count(&cnt->amsf_hooks, hooks);
         const unsigned long long sc = __reduce_add_sync(0xffffffffu, (uint32_t)min(scanned, 0xFFFFFFFFull));
         if (lane == 0 && sc) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt->amsf_edges), sc);
+    }
+}
+
+// The long lists of this round, indexed (hub bucket index): a piece is up to
+// kAmsfChunk of the hub's entries of THIS bucket, read through hidx -- every entry
+// is in the bucket, so no weight test is needed and each hub edge is read in one
+// round only.
+template <int MODE>
+__global__ void __launch_bounds__(kBlock) k_amsf_hub_pieces(const int64_t* __restrict__ off,
+                                                            const uint32_t* __restrict__ adj,
+                                                            const float* __restrict__ w, uint32_t* P, uint32_t round,
+                                                            const uint2* __restrict__ chq, const AmsfCtl* ac,
+                                                            const uint32_t* __restrict__ hid,
+                                                            const uint32_t* __restrict__ hstart,
+                                                            const unsigned long long* __restrict__ hbase,
+                                                            const uint32_t* __restrict__ hidx, uint32_t nbk, uint2* F,
+                                                            float* Fw, cc_counters* cnt)
+{
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned long long total = ac->chunks;
+    const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    uint32_t hooks = 0;
+    unsigned long long scanned = 0;
+    for (unsigned long long q = warp; q < total; q += nwarps) {
+        const uint2 item = chq[q];
+        const uint32_t h = hid[item.x];
+        const uint32_t* hs = hstart + (uint64_t)h * (nbk + 1);
+        const unsigned long long s0 = hbase[h] + hs[round] + (unsigned long long)item.y * kAmsfChunk;
+        const unsigned long long s1 = min(hbase[h] + hs[round + 1], s0 + kAmsfChunk);
+        const int64_t o = off[item.x];
+        scanned += lane == 0 ? s1 - s0 : 0ull;
+        for (unsigned long long x0 = s0 + lane; x0 < s1; x0 += 32 * 4) {
+            int64_t e[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) e[j] = x0 + 32 * j < s1 ? o + hidx[x0 + 32 * j] : -1;
+            float wx[4];
+            uint32_t vx[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                wx[j] = e[j] >= 0 ? w[e[j]] : 0.0f;
+                vx[j] = e[j] >= 0 ? adj[e[j]] : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (e[j] >= 0) hooks += link<MODE>(P, item.x, vx[j], ForestW{F, Fw, wx[j]});
+        }
+    }
+    if (cnt) {
+        warp_count(&cnt->amsf_hooks, hooks);
+        const unsigned long long sc = __reduce_add_sync(0xffffffffu, (uint32_t)min(scanned, 0xFFFFFFFFull));
+        if (lane == 0 && sc) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt->amsf_edges), sc);
+    }
+}
+
+// Hub bucket index (built once): the vertices with more than kAmsfChunk entries,
+// hid[v] = their index, and per hub its entries (offsets relative to off[v])
+// grouped by bucket: hidx[hbase[h] + hstart[h][i] ..] are the bucket-i entries.
+__global__ void __launch_bounds__(kBlock) k_amsf_hubs(const int64_t* __restrict__ off, uint32_t n, uint32_t* hubs,
+                                                      uint32_t* hid, unsigned long long* hcount,
+                                                      unsigned long long* hdeg)
+{
+    for (uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x; t0 < n; t0 += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t v = t0 + threadIdx.x;
+        const int64_t d = v < n ? off[v + 1] - off[v] : 0;
+        const bool hub = d > kAmsfChunk;
+        const unsigned long long pos = warp_append(hcount, hub ? 1u : 0u);
+        if (hub) {
+            hubs[pos] = (uint32_t)v;
+            hid[v] = (uint32_t)pos;
+            hdeg[pos] = (unsigned long long)d;
+        }
+    }
+}
+
+// one block per hub: bucket histogram in shared memory, exclusive scan, then the
+// entries placed by a shared cursor (order within a bucket is arbitrary)
+__global__ void __launch_bounds__(kBlock) k_amsf_hub_index(const int64_t* __restrict__ off,
+                                                           const float* __restrict__ w, const uint32_t* hubs,
+                                                           const unsigned long long* hcount,
+                                                           const unsigned long long* hbase, const double* bnd,
+                                                           uint32_t nbk, uint32_t* hstart, uint32_t* hidx)
+{
+    __shared__ uint32_t sh[kIdxBins + 1];
+    __shared__ double sb[kIdxBins + 1];
+    for (uint32_t i = threadIdx.x; i <= nbk; i += blockDim.x) sb[i] = bnd[i];
+    const unsigned long long H = *hcount;
+    for (unsigned long long h = blockIdx.x; h < H; h += gridDim.x) {
+        const uint32_t v = hubs[h];
+        const int64_t b = off[v], d = off[v + 1] - b;
+        for (uint32_t i = threadIdx.x; i <= nbk; i += blockDim.x) sh[i] = 0;
+        __syncthreads();
+        for (int64_t x = threadIdx.x; x < d; x += blockDim.x) atomicAdd(sh + bucket_of(sb, nbk, w[b + x]), 1u);
+        __syncthreads();
+        if (threadIdx.x == 0) {                               // exclusive scan (nbk <= kIdxBins)
+            uint32_t acc = 0;
+            for (uint32_t i = 0; i <= nbk; ++i) {
+                const uint32_t c = sh[i];
+                sh[i] = acc;
+                acc += c;
+            }
+        }
+        __syncthreads();
+        uint32_t* hs = hstart + h * (nbk + 1);
+        for (uint32_t i = threadIdx.x; i <= nbk; i += blockDim.x) hs[i] = sh[i];
+        __syncthreads();
+        for (int64_t x = threadIdx.x; x < d; x += blockDim.x) {
+            const uint32_t bi = bucket_of(sb, nbk, w[b + x]);
+            hidx[hbase[h] + atomicAdd(sh + bi, 1u)] = (uint32_t)x;
+        }
+        __syncthreads();
+    }
+}
+
+// exclusive scan of the hub degrees (one block, 64-bit)
+__global__ void __launch_bounds__(kBlock) k_amsf_hub_scan(const unsigned long long* hdeg,
+                                                          const unsigned long long* hcount, unsigned long long* hbase)
+{
+    __shared__ unsigned long long ws[kBlock / 32];
+    __shared__ unsigned long long carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const unsigned lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    const unsigned long long H = *hcount;
+    for (unsigned long long base = 0; base < H; base += kBlock) {
+        const unsigned long long i = base + threadIdx.x;
+        const unsigned long long x = i < H ? hdeg[i] : 0ull;
+        unsigned long long incl = x;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (unsigned)o) incl += t;
+        }
+        if (lane == 31) ws[wi] = incl;
+        __syncthreads();
+        unsigned long long wb = 0;
+        for (unsigned j = 0; j < wi; ++j) wb += ws[j];
+        const unsigned long long c = carry;
+        if (i < H) hbase[i] = c + wb + incl - x;
+        __syncthreads();
+        if (threadIdx.x == kBlock - 1) carry = c + wb + incl;
+        __syncthreads();
     }
 }
 
@@ -504,11 +653,14 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
     const int sms = num_sms();
     const bool skip = !(o.flags & CC_FLAG_NO_SKIP);
     const bool plain = (o.flags & CC_FLAG_AMSF_PLAIN) != 0;
+    bool index = false;                       // hub bucket index (set once nb is known)
     AmsfCtl* ac = nullptr;
     uint32_t *P = nullptr, *wlo = nullptr, *whi = nullptr, *fb = nullptr, *order = nullptr;
     uint32_t* carry[2] = {nullptr, nullptr};
     uint2* F = nullptr;
     uint2* chq = nullptr;
+    uint32_t *hubs = nullptr, *hid = nullptr, *hstart = nullptr, *hidx = nullptr;
+    unsigned long long *hdeg = nullptr, *hbase = nullptr, *hcount = nullptr;
     float* Fw = nullptr;
     double* bd = nullptr;
     unsigned long long *start = nullptr, *cursor = nullptr;
@@ -560,6 +712,7 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
             }
             b.push_back(b.back() * g);
             nb = (uint32_t)(b.size() - 1);
+            index = !plain && nb <= kIdxBins && !(o.flags & CC_FLAG_AMSF_NO_INDEX);
             CC_CUDA_TRY(scratch_alloc((void**)&bd, sizeof(double) * b.size(), s));
             CC_CUDA_TRY(cudaMemcpyAsync(bd, b.data(), sizeof(double) * b.size(), cudaMemcpyHostToDevice, s));
             CC_CUDA_TRY(scratch_alloc((void**)&fb, sizeof(uint32_t) * n, s));
@@ -579,6 +732,24 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
             CC_CUDA_TRY(cudaMemcpyAsync(cursor, start, sizeof(unsigned long long) * (nb + 1), cudaMemcpyDeviceToDevice, s));
             k_amsf_scatter<<<sms * 8, kBlock, 0, s>>>(whi, fb, n, nb, cursor, order);
             CC_LAUNCH_CHECK("k_amsf_scatter");
+            if (index) {
+                // hub bucket index: lists longer than kAmsfChunk grouped by bucket, once
+                const uint64_t hcap = std::max<uint64_t>(1, std::min<uint64_t>(n, (uint64_t)m / (kAmsfChunk + 1) + 1));
+                CC_CUDA_TRY(scratch_alloc((void**)&hubs, sizeof(uint32_t) * hcap, s));
+                CC_CUDA_TRY(scratch_alloc((void**)&hid, sizeof(uint32_t) * n, s));
+                CC_CUDA_TRY(scratch_alloc((void**)&hdeg, sizeof(unsigned long long) * hcap, s));
+                CC_CUDA_TRY(scratch_alloc((void**)&hbase, sizeof(unsigned long long) * hcap, s));
+                CC_CUDA_TRY(scratch_alloc((void**)&hcount, sizeof(unsigned long long), s));
+                CC_CUDA_TRY(scratch_alloc((void**)&hstart, sizeof(uint32_t) * hcap * (nb + 1), s));
+                CC_CUDA_TRY(scratch_alloc((void**)&hidx, sizeof(uint32_t) * (size_t)m, s));
+                CC_CUDA_TRY(cudaMemsetAsync(hcount, 0, sizeof(unsigned long long), s));
+                k_amsf_hubs<<<sms * 8, kBlock, 0, s>>>(off, n, hubs, hid, hcount, hdeg);
+                CC_LAUNCH_CHECK("k_amsf_hubs");
+                k_amsf_hub_scan<<<1, kBlock, 0, s>>>(hdeg, hcount, hbase);
+                CC_LAUNCH_CHECK("k_amsf_hub_scan");
+                k_amsf_hub_index<<<sms * 4, kBlock, 0, s>>>(off, w, hubs, hcount, hbase, bd, nb, hstart, hidx);
+                CC_LAUNCH_CHECK("k_amsf_hub_index");
+            }
         }
         // the rounds: bucket i = [b_i, b_(i+1)), lightest first
         for (uint32_t i = 0; i < nb; ++i) {
@@ -589,9 +760,13 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
             }
             k_amsf_round<MODE><<<sms * 8, kBlock, 0, s>>>(off, adj, w, P, wlo, whi, order, start, i, b[i], b[i + 1],
                                                           carry[in_slot], ac, in_slot, carry[in_slot ^ 1],
-                                                          skip, plain, F, Fw, chq, o.counters);
+                                                          skip, plain, F, Fw, chq, hid, index ? hstart : nullptr,
+                                                          nb, o.counters);
             CC_LAUNCH_CHECK("k_amsf_round");
-            if (((uintptr_t)w & 15u) == 0)
+            if (index)
+                k_amsf_hub_pieces<MODE><<<sms * 8, kBlock, 0, s>>>(off, adj, w, P, i, chq, ac, hid, hstart, hbase, hidx,
+                                                                   nb, F, Fw, o.counters);
+            else if (((uintptr_t)w & 15u) == 0)
                 k_amsf_chunks<MODE, true><<<sms * 8, kBlock, 0, s>>>(off, adj, w, P, b[i], b[i + 1], chq, ac, F, Fw,
                                                                      o.counters);
             else
@@ -624,7 +799,8 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
     };
     const cc_status rc = body();
     for (void* p : {(void*)ac, (void*)P, (void*)wlo, (void*)whi, (void*)fb, (void*)order, (void*)carry[0],
-                    (void*)carry[1], (void*)F, (void*)Fw, (void*)chq, (void*)bd, (void*)start, (void*)cursor, (void*)fcnt,
+                    (void*)carry[1], (void*)F, (void*)Fw, (void*)chq, (void*)hubs, (void*)hid, (void*)hstart,
+                    (void*)hidx, (void*)hdeg, (void*)hbase, (void*)hcount, (void*)bd, (void*)start, (void*)cursor, (void*)fcnt,
                     (void*)foff})
         scratch_free(p, s);
     return rc;

@@ -34,6 +34,7 @@ OPTS = [
     dict(flags=cc.FLAG_AMSF_PLAIN | cc.FLAG_NO_SKIP),
     dict(flags=cc.FLAG_HALVE, seed=3),
     dict(flags=cc.FLAG_UF_ASYNC, seed=4),
+    dict(flags=cc.FLAG_AMSF_NO_INDEX),
 ]
 
 
@@ -172,3 +173,19 @@ def test_amsf_unaligned_weights():
     buf[1:] = torch.from_numpy(w).cuda()
     E, W, tot = pkg.amsf(d_off, d_adj, buf[1:], 0.25)
     check(off, adj, w, 0.25, u32(E).reshape(-1, 2), W.cpu().numpy(), tot)
+
+
+def test_amsf_hubs_bucket_index():
+    """Lists far longer than the 2048-entry piece size (hub bucket index, several
+    pieces per bucket), with and without the index, with and without the skip."""
+    rng = np.random.default_rng(5)
+    n = 30000
+    pairs = [(0, v) for v in range(1, 12001)] + [(1, v) for v in range(2, 30000, 3)]
+    pairs += [tuple(rng.integers(0, n, 2)) for _ in range(20000)]
+    off, adj = oracle.csr_from_pairs(n, pairs)
+    assert np.diff(off).max() > 4 * 2048
+    for seed, eps in ((1, 0.25), (2, 0.05), (3, 1.0)):
+        w = gen.exp_weights(off, adj, seed)
+        want = oracle.amsf(off, adj, w, eps)
+        for opt in (OPTS[0], OPTS[1], OPTS[6], dict(flags=cc.FLAG_HALVE)):
+            check(off, adj, w, eps, *run(off, adj, w, eps, **opt), want=want)
