@@ -76,55 +76,109 @@ struct ForestW {
 
 __device__ __forceinline__ bool good_weight(float x) { return x > 0.0f && x < __int_as_float((int)kPosInfBits); }
 
-// Per-vertex lightest / heaviest edge weight and the global range.  Edge-balanced:
-// warp c owns entries [c*4096, (c+1)*4096) and follows their owners with a
-// monotone pointer, flushing one atomicMin / atomicMax per (lane, owner) run.
-constexpr int64_t kChunk = 4096;
+// Per-vertex lightest / heaviest edge weight and the global range.  A warp takes
+// 32 consecutive vertices; their lists (<= kAmsfChunk entries each) are swept 32
+// entries at a time, each lane finding its entry's owner by a shuffle search, and
+// a segmented min/max scan over the lanes leaves one result per (owner, step) that
+// the segment's last lane folds into the warp's shared slot of that owner -- no
+// atomics.  A longer list is reduced by the whole warp on its own.
 __global__ void __launch_bounds__(kBlock) k_amsf_wrange(const int64_t* __restrict__ off, const float* __restrict__ w,
                                                         uint32_t n, int64_t m, uint32_t* wlo, uint32_t* whi,
                                                         AmsfCtl* ac)
 {
+    __shared__ uint32_t s_lo[kBlock], s_hi[kBlock];
     const unsigned lane = threadIdx.x & 31;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    uint32_t* mlo = s_lo + (threadIdx.x & ~31u);
+    uint32_t* mhi = s_hi + (threadIdx.x & ~31u);
+    const uint64_t ntiles = ((uint64_t)n + 31) / 32;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     uint32_t gmin = kPosInfBits, gmax = 0, bad = 0;
-    for (int64_t c0 = warp * kChunk; c0 < m; c0 += nwarps * kChunk) {
-        const int64_t c1 = min(c0 + kChunk, m);
-        uint32_t lo = 0, hi = n;                              // largest u with off[u] <= c0
-        if (lane == 0) {
-            while (hi - lo > 1) {
-                const uint32_t mid = lo + (hi - lo) / 2;
-                if (off[mid] <= c0) lo = mid; else hi = mid;
-            }
+    for (uint64_t tile = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; tile < ntiles; tile += nwarps) {
+        const uint64_t u = tile * 32 + lane;
+        const int64_t b = u < n ? off[u] : 0;
+        const int64_t dfull = u < n ? off[u + 1] - b : 0;
+        const bool hub = dfull > kAmsfChunk;
+        const uint32_t d = hub ? 0u : (uint32_t)dfull;
+        mlo[lane] = kPosInfBits;
+        mhi[lane] = 0u;
+        uint32_t incl = d;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (unsigned)o) incl += t;
         }
-        uint32_t own = __shfl_sync(0xffffffffu, lo, 0);
-        int64_t own_end = off[own + 1];
-        uint32_t rlo = kPosInfBits, rhi = 0;
-        for (int64_t i = c0 + lane; i < c1; i += 32) {
-            const float x = w[i];
-            if (!good_weight(x)) bad = 1;
-            const uint32_t b = __float_as_uint(x) & 0x7FFFFFFFu;
-            if (i >= own_end) {
-                if (rhi) {
-                    atomicMin(wlo + own, rlo);
-                    atomicMax(whi + own, rhi);
+        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t excl = incl - d;
+        __syncwarp();
+        for (uint32_t t0 = 0; t0 < tot; t0 += 32) {
+            const uint32_t t = t0 + lane;
+            int lo = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const uint32_t pe = __shfl_sync(0xffffffffu, excl, lo + step);
+                if (pe <= t) lo += step;
+            }
+            const int64_t ob = __shfl_sync(0xffffffffu, b, lo);
+            const uint32_t oex = __shfl_sync(0xffffffffu, excl, lo);
+            const bool valid = t < tot;
+            const float x = valid ? w[ob + (t - oex)] : 1.0f;
+            if (valid && !good_weight(x)) bad = 1;
+            const uint32_t owner = valid ? (uint32_t)lo : 32u;
+            uint32_t vlo = valid ? (__float_as_uint(x) & 0x7FFFFFFFu) : kPosInfBits;
+            uint32_t vhi = valid ? (__float_as_uint(x) & 0x7FFFFFFFu) : 0u;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {                  // segmented inclusive min / max
+                const uint32_t po = __shfl_up_sync(0xffffffffu, owner, o);
+                const uint32_t pl = __shfl_up_sync(0xffffffffu, vlo, o);
+                const uint32_t ph = __shfl_up_sync(0xffffffffu, vhi, o);
+                if (lane >= (unsigned)o && po == owner) {
+                    vlo = min(vlo, pl);
+                    vhi = max(vhi, ph);
                 }
-                rlo = kPosInfBits;
-                rhi = 0;
-                do {
-                    ++own;
-                    own_end = off[own + 1];
-                } while (own_end <= i);
             }
-            rlo = min(rlo, b);
-            rhi = max(rhi, b);
-            gmin = min(gmin, b);
-            gmax = max(gmax, b);
+            const uint32_t nxt = __shfl_down_sync(0xffffffffu, owner, 1);
+            if (valid && (lane == 31 || nxt != owner)) {       // the segment's last lane
+                mlo[owner] = min(mlo[owner], vlo);
+                mhi[owner] = max(mhi[owner], vhi);
+                gmin = min(gmin, vlo);
+                gmax = max(gmax, vhi);
+            }
+            __syncwarp();
         }
-        if (rhi) {
-            atomicMin(wlo + own, rlo);
-            atomicMax(whi + own, rhi);
+        // long lists: the whole warp, one list at a time
+        for (unsigned hm = __ballot_sync(0xffffffffu, hub); hm; hm &= hm - 1) {
+            const int j = __ffs(hm) - 1;
+            const int64_t hb = __shfl_sync(0xffffffffu, b, j);
+            const int64_t he = hb + __shfl_sync(0xffffffffu, dfull, j);
+            uint32_t vlo = kPosInfBits, vhi = 0;
+            for (int64_t x0 = hb + lane; x0 < he; x0 += 32 * 4) {
+                float xs[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) xs[q] = x0 + 32 * q < he ? w[x0 + 32 * q] : 1.0f;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (x0 + 32 * q >= he) continue;
+                    if (!good_weight(xs[q])) bad = 1;
+                    const uint32_t bits = __float_as_uint(xs[q]) & 0x7FFFFFFFu;
+                    vlo = min(vlo, bits);
+                    vhi = max(vhi, bits);
+                }
+            }
+            vlo = __reduce_min_sync(0xffffffffu, vlo);
+            vhi = __reduce_max_sync(0xffffffffu, vhi);
+            if (lane == (unsigned)j) {
+                mlo[j] = vlo;
+                mhi[j] = vhi;
+            }
+            gmin = min(gmin, vlo);
+            gmax = max(gmax, vhi);
         }
+        __syncwarp();
+        if (u < n) {
+            wlo[u] = mlo[lane];
+            whi[u] = mhi[lane];
+        }
+        __syncwarp();
     }
     gmin = __reduce_min_sync(0xffffffffu, gmin);
     gmax = __reduce_max_sync(0xffffffffu, gmax);
@@ -213,30 +267,44 @@ __global__ void __launch_bounds__(kBlock) k_amsf_scan(unsigned long long* hist, 
     }
 }
 
-// order[] by activation bucket: per tile of kBlock vertices, ranks within the
-// block from shared atomics, one global range per non-empty bin and tile
+// order[] by activation bucket: per block tile of 8 * kBlock vertices, ranks within
+// the tile from shared atomics, one global range per non-empty bin and tile
 __global__ void __launch_bounds__(kBlock) k_amsf_scatter(const uint32_t* whi, const uint32_t* fb, uint32_t n,
                                                          uint32_t nb, unsigned long long* cursor, uint32_t* order)
 {
+    constexpr int V = 8;
     __shared__ uint32_t sc[kSmemBins];
     __shared__ unsigned long long sb[kSmemBins];
     const bool local = nb <= kSmemBins;
-    for (uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x; t0 < n; t0 += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t v = t0 + threadIdx.x;
-        const bool act = v < n && whi[v] != 0;
-        const uint32_t f = act ? fb[v] : 0u;
+    for (uint64_t t0 = (uint64_t)blockIdx.x * (kBlock * V); t0 < n; t0 += (uint64_t)gridDim.x * (kBlock * V)) {
+        bool act[V];
+        uint32_t f[V], rank[V];
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+            const uint64_t v = t0 + (uint64_t)k * kBlock + threadIdx.x;
+            act[k] = v < n && whi[v] != 0;
+            f[k] = act[k] ? fb[v] : 0u;
+        }
         if (!local) {
-            if (act) order[atomicAdd(cursor + f, 1ull)] = (uint32_t)v;
+#pragma unroll
+            for (int k = 0; k < V; ++k)
+                if (act[k]) order[atomicAdd(cursor + f[k], 1ull)] = (uint32_t)(t0 + (uint64_t)k * kBlock + threadIdx.x);
             continue;
         }
-        // clear only the bins this tile touches
-        if (act) sc[f] = 0;
+#pragma unroll
+        for (int k = 0; k < V; ++k)
+            if (act[k]) sc[f[k]] = 0;                        // clear only the bins this tile touches
         __syncthreads();
-        const uint32_t rank = act ? atomicAdd(sc + f, 1u) : 0u;
+#pragma unroll
+        for (int k = 0; k < V; ++k) rank[k] = act[k] ? atomicAdd(sc + f[k], 1u) : 0u;
         __syncthreads();
-        if (act && rank == 0) sb[f] = atomicAdd(cursor + f, (unsigned long long)sc[f]);
+#pragma unroll
+        for (int k = 0; k < V; ++k)
+            if (act[k] && rank[k] == 0) sb[f[k]] = atomicAdd(cursor + f[k], (unsigned long long)sc[f[k]]);
         __syncthreads();
-        if (act) order[sb[f] + rank] = (uint32_t)v;
+#pragma unroll
+        for (int k = 0; k < V; ++k)
+            if (act[k]) order[sb[f[k]] + rank[k]] = (uint32_t)(t0 + (uint64_t)k * kBlock + threadIdx.x);
         __syncthreads();
     }
 }
@@ -248,6 +316,9 @@ __global__ void __launch_bounds__(kBlock) k_amsf_scatter(const uint32_t* whi, co
 // different component -- seen by more samples than the anchor's -- the anchor
 // moves there and this round rebuilds its input from every activated vertex.
 constexpr int kIdTable = 4096;
+#ifndef CC_AMSF_ANCHOR_DIV
+#define CC_AMSF_ANCHOR_DIV 256
+#endif
 __global__ void __launch_bounds__(1024) k_amsf_lmax(const uint32_t* P, uint32_t n, uint64_t seed, uint32_t round,
                                                     uint32_t samples, AmsfCtl* ac)
 {
@@ -301,10 +372,10 @@ __global__ void __launch_bounds__(1024) k_amsf_lmax(const uint32_t* P, uint32_t 
         if (t == 0) {
             const uint32_t lm = kSentinel - (uint32_t)(key & 0xFFFFFFFFull);
             const uint32_t cnt_lm = (uint32_t)(key >> 32);
-            // a component seen by under 1/64 of the samples is not worth skipping (while the
+            // a component seen by under 1/256 of the samples (4 of 1024) is not worth skipping (while the
             // labeling is all singletons every sample is its own mode): start, or move, the
             // anchor only for a component at least that large
-            const bool big = (uint64_t)cnt_lm * 64 >= samples;
+            const bool big = (uint64_t)cnt_lm * CC_AMSF_ANCHOR_DIV >= samples;
             ac->rebuild = 0;
             if (s_ra == kSentinel) {
                 if (big) ac->anchor = lm;                 // nothing dropped yet: no rebuild needed
@@ -494,12 +565,25 @@ __global__ void __launch_bounds__(kBlock) k_amsf_hubs(const int64_t* __restrict_
 }
 
 // one block per hub: bucket histogram in shared memory, exclusive scan, then the
-// entries placed by a shared cursor (order within a bucket is arbitrary)
-__global__ void __launch_bounds__(kBlock) k_amsf_hub_index(const int64_t* __restrict__ off,
-                                                           const float* __restrict__ w, const uint32_t* hubs,
-                                                           const unsigned long long* hcount,
-                                                           const unsigned long long* hbase, const double* bnd,
-                                                           uint32_t nbk, uint32_t* hstart, uint32_t* hidx)
+// entries placed by a shared cursor (order within a bucket is arbitrary).  The
+// bucket of a weight is estimated from log2(x / W_min) / log2(1 + eps) and then
+// settled by the exact fp64 comparisons b_i <= x < b_(i+1) (reading R25).
+__device__ __forceinline__ uint32_t bucket_fast(const double* b, uint32_t nb, float x, float wmin, float inv_l2g)
+{
+    int i = (int)(__log2f(x / wmin) * inv_l2g);
+    i = max(0, min((int)nb - 1, i));
+    const double d = (double)x;
+    while (i + 1 < (int)nb && b[i + 1] <= d) ++i;
+    while (i > 0 && b[i] > d) --i;
+    return (uint32_t)i;
+}
+
+__global__ void __launch_bounds__(1024) k_amsf_hub_index(const int64_t* __restrict__ off,
+                                                         const float* __restrict__ w, const uint32_t* hubs,
+                                                         const unsigned long long* hcount,
+                                                         const unsigned long long* hbase, const double* bnd,
+                                                         uint32_t nbk, float wmin, float inv_l2g, uint32_t* hstart,
+                                                         uint32_t* hidx)
 {
     __shared__ uint32_t sh[kIdxBins + 1];
     __shared__ double sb[kIdxBins + 1];
@@ -510,14 +594,21 @@ __global__ void __launch_bounds__(kBlock) k_amsf_hub_index(const int64_t* __rest
         const int64_t b = off[v], d = off[v + 1] - b;
         for (uint32_t i = threadIdx.x; i <= nbk; i += blockDim.x) sh[i] = 0;
         __syncthreads();
-        for (int64_t x = threadIdx.x; x < d; x += blockDim.x) atomicAdd(sh + bucket_of(sb, nbk, w[b + x]), 1u);
+        for (int64_t x = threadIdx.x; x < d; x += blockDim.x)
+            atomicAdd(sh + bucket_fast(sb, nbk, w[b + x], wmin, inv_l2g), 1u);
         __syncthreads();
-        if (threadIdx.x == 0) {                               // exclusive scan (nbk <= kIdxBins)
-            uint32_t acc = 0;
-            for (uint32_t i = 0; i <= nbk; ++i) {
-                const uint32_t c = sh[i];
-                sh[i] = acc;
-                acc += c;
+        if (threadIdx.x < 32) {                               // exclusive scan (nbk <= kIdxBins), one warp
+            uint32_t carry = 0;
+            for (uint32_t base = 0; base <= nbk; base += 32) {
+                const uint32_t i = base + threadIdx.x;
+                const uint32_t c = i <= nbk ? sh[i] : 0u;
+                uint32_t incl = c;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (threadIdx.x >= (unsigned)o) incl += t;
+                }
+                if (i <= nbk) sh[i] = carry + incl - c;
+                carry += __shfl_sync(0xffffffffu, incl, 31);
             }
         }
         __syncthreads();
@@ -525,7 +616,7 @@ __global__ void __launch_bounds__(kBlock) k_amsf_hub_index(const int64_t* __rest
         for (uint32_t i = threadIdx.x; i <= nbk; i += blockDim.x) hs[i] = sh[i];
         __syncthreads();
         for (int64_t x = threadIdx.x; x < d; x += blockDim.x) {
-            const uint32_t bi = bucket_of(sb, nbk, w[b + x]);
+            const uint32_t bi = bucket_fast(sb, nbk, w[b + x], wmin, inv_l2g);
             hidx[hbase[h] + atomicAdd(sh + bi, 1u)] = (uint32_t)x;
         }
         __syncthreads();
@@ -747,7 +838,8 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
                 CC_LAUNCH_CHECK("k_amsf_hubs");
                 k_amsf_hub_scan<<<1, kBlock, 0, s>>>(hdeg, hcount, hbase);
                 CC_LAUNCH_CHECK("k_amsf_hub_scan");
-                k_amsf_hub_index<<<sms * 4, kBlock, 0, s>>>(off, w, hubs, hcount, hbase, bd, nb, hstart, hidx);
+                k_amsf_hub_index<<<sms * 2, 1024, 0, s>>>(off, w, hubs, hcount, hbase, bd, nb, (float)b[0],
+                                                          (float)(1.0 / std::log2(1.0 + eps)), hstart, hidx);
                 CC_LAUNCH_CHECK("k_amsf_hub_index");
             }
         }
