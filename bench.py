@@ -51,6 +51,7 @@ def parse():
     p.add_argument("--study", action="store_true", help="NEXT-1 sampling variant x k sweep on C2-C4")
     p.add_argument("--incr-sweep", action="store_true", help="NEXT-2 incremental variants sweep")
     p.add_argument("--amsf", action="store_true", help="NEXT-4 AMSF-NF-S study on C3/C4 with Exp(1) weights")
+    p.add_argument("--table4", action="store_true", help="NEXT-2(b): Table 4 insert-only protocol, RM stream")
     p.add_argument("--eps", type=float, default=0.25)
     return p.parse_args()
 
@@ -717,6 +718,58 @@ def run_incr_sweep(a):
     print(json.dumps({"study": "NEXT-2 incremental variants", **out}), flush=True)
 
 
+def run_table4(a):
+    """NEXT-2 (b): the paper's Table 4 protocol: maximum
+    insert throughput, one batch, no queries, on the RM stream -- RMAT n = 2^30,
+    m = 10n, (a, b, c) = (.5, .1, .1), unpermuted.  The 10.7e9 inserts are fed as
+    consecutive sub-batches of 2^28 pairs (no queries in between, so the same as one
+    batch); generation is outside the timed region, each sub-batch's insert call is
+    timed with CUDA events on the launching stream.  Also the same protocol on the
+    C5 stream shape (RMAT-26 Graph500 parameters, permuted) for comparison."""
+    import torch
+
+    from inputs import gen
+    from inputs import gpu as ggen
+    from paper_2008_03909_b200 import cc
+    stream = torch.cuda.current_stream()
+    rows = []
+    for name, s, total, t, perm in (("RM n=2^30 m=10n (.5,.1,.1) unpermuted", 30, 10 << 30, gen.RM_T, False),
+                                    ("C5 shape: RMAT-26 Graph500, permuted, 2^28 inserts", 26, 1 << 28,
+                                     (gen.RMAT_T1, gen.RMAT_T2, gen.RMAT_T3), True)):
+        n = 1 << s
+        chunk = 1 << 28
+        buf = torch.empty((chunk, 2), dtype=torch.int32, device="cuda")
+        empty_q = torch.empty((0, 2), dtype=torch.int32, device="cuda")
+        no_ans = torch.empty(1, dtype=torch.uint8, device="cuda")
+        best = None
+        for rep in range(max(1, a.steps)):
+            h = cc.Incr(n, flags=a.flags)
+            ms = 0.0
+            for first in range(0, total, chunk):
+                cnt = min(chunk, total - first)
+                ggen.rmat_stream(s, s, first, cnt, t=t, permuted=perm, out=buf[:cnt])
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                h.batch(buf[:cnt], cnt, empty_q, 0, no_ans)
+                e1.record(stream)
+                e1.synchronize()
+                ms += e0.elapsed_time(e1)
+            lab = torch.empty(n, dtype=torch.int32, device="cuda")
+            h.labels(lab)
+            comps = int((lab == torch.arange(n, device="cuda", dtype=torch.int32)).sum().item())
+            h.close()
+            del lab
+            best = ms if best is None else min(best, ms)
+        rows.append({"stream": name, "n": n, "inserts": total, "ms": round(best, 3),
+                     "inserts_per_s": round(total / (best * 1e-3), 1), "components": comps,
+                     "paper_72core_inserts_per_s": 8.78e8 if s == 30 else None})
+        print(json.dumps(rows[-1]), file=sys.stderr, flush=True)
+        del buf
+        torch.cuda.empty_cache()
+    print(json.dumps({"study": "NEXT-2(b) Table 4 protocol", "rows": rows}), flush=True)
+
+
 def run_amsf(a):
     """NEXT-4: AMSF-NF-S on C3 / C4 with the seeded
     Exp(1) weights (the paper's weighted inputs are not here),
@@ -805,6 +858,8 @@ def main():
         run_study(a)
     elif a.amsf:
         run_amsf(a)
+    elif a.table4:
+        run_table4(a)
     elif a.incr_sweep:
         run_incr_sweep(a)
     elif a.impl == "reference":

@@ -65,6 +65,27 @@ Perm make_perm(uint64_t seed, int s)
     return p;
 }
 
+__device__ __forceinline__ void rmat_draw_t(uint64_t seed, int s, uint64_t i, uint32_t t1, uint32_t t2, uint32_t t3,
+                                            uint64_t* pu, uint64_t* pv)
+{
+    const uint64_t L = (uint64_t)((s + 1) / 2);
+    uint64_t u = 0, v = 0, r = 0;
+    for (int l = 0; l < s; ++l) {
+        uint32_t x;
+        if ((l & 1) == 0) {
+            r = mix(seed, RMAT_STREAM, i * L + (uint64_t)(l / 2));
+            x = (uint32_t)(r & 0xFFFFFFFFull);
+        } else {
+            x = (uint32_t)(r >> 32);
+        }
+        const uint64_t bit = 1ull << (s - 1 - l);
+        if (x >= t2) u |= bit;
+        if ((x >= t1 && x < t2) || x >= t3) v |= bit;
+    }
+    *pu = u;
+    *pv = v;
+}
+
 __device__ __forceinline__ void rmat_draw(uint64_t seed, int s, uint64_t i, uint64_t* pu, uint64_t* pv)
 {
     const uint64_t L = (uint64_t)((s + 1) / 2);
@@ -198,6 +219,20 @@ __global__ void k_incr(uint64_t seed, int s, Perm perm, uint64_t first, uint64_t
             qs[2 * j] = (uint32_t)scale_u32(r & 0xFFFFFFFFull, n);
             qs[2 * j + 1] = (uint32_t)scale_u32(r >> 32, n);
         }
+    }
+}
+
+// RMAT draws first .. first+count-1 on 2^s vertices with the thresholds
+// t1 = a, t2 = a+b, t3 = a+b+c (fixed point, x 2^32), optionally permuted
+__global__ void k_rmat_stream(uint64_t seed, int s, Perm perm, int permuted, uint32_t t1, uint32_t t2, uint32_t t3,
+                              uint64_t first, uint64_t count, uint32_t* out)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+        uint64_t u, v;
+        rmat_draw_t(seed, s, first + i, t1, t2, t3, &u, &v);
+        out[2 * i] = (uint32_t)(permuted ? perm(u) : u);
+        out[2 * i + 1] = (uint32_t)(permuted ? perm(v) : v);
     }
 }
 
@@ -415,6 +450,17 @@ int gen_incr_batch(uint64_t seed, int s, uint64_t b, uint64_t n_ins, uint64_t n_
 {
     Perm perm = make_perm(seed, s);
     k_incr<<<grid_blocks(), 256, 0, (cudaStream_t)stream>>>(seed, s, perm, b * n_ins, n_ins, b * n_q, n_q, ins, qs);
+    TRY(cudaGetLastError());
+    return 0;
+}
+
+// RMAT pair stream with explicit (a, b, c) thresholds (inputs/gen.py rmat_pairs)
+int gen_rmat_stream(uint64_t seed, int s, uint64_t first, uint64_t count, uint32_t t1, uint32_t t2, uint32_t t3,
+                    int permuted, uint32_t* out, void* stream)
+{
+    Perm perm = make_perm(seed, s);
+    k_rmat_stream<<<grid_blocks(), 256, 0, (cudaStream_t)stream>>>(seed, s, perm, permuted, t1, t2, t3, first, count,
+                                                                   out);
     TRY(cudaGetLastError());
     return 0;
 }

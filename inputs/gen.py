@@ -82,8 +82,13 @@ def permute(x, seed: int, s: int) -> np.ndarray:
     return x
 
 
-def rmat_pairs(seed: int, s: int, first: int, count: int, permuted: bool = True):
-    """RMAT draws first..first+count-1 on 2^s vertices (Graph500 a,b,c = .57,.19,.19).
+RM_T = (2147483648, 2576980377, 3006477107)   # the paper's RM stream: a, b, c = .5, .1, .1
+
+
+def rmat_pairs(seed: int, s: int, first: int, count: int, permuted: bool = True,
+               t=(RMAT_T1, RMAT_T2, RMAT_T3)):
+    """RMAT draws first..first+count-1 on 2^s vertices (Graph500 a,b,c = .57,.19,.19
+    unless t = floor((a, a+b, a+b+c) * 2^32) says otherwise).
 
     Level l (0-based, most significant first) uses the 32-bit half (l & 1) of
     mix(seed, RMAT, i*L + l//2), L = ceil(s/2), and sets bit s-1-l of (u, v)."""
@@ -100,8 +105,8 @@ def rmat_pairs(seed: int, s: int, first: int, count: int, permuted: bool = True)
         else:
             x = hi32(r)
         bit = np.uint64(1) << np.uint64(s - 1 - lvl)
-        ub = x >= np.uint64(RMAT_T2)                       # quadrants (1,0), (1,1)
-        vb = ((x >= np.uint64(RMAT_T1)) & (x < np.uint64(RMAT_T2))) | (x >= np.uint64(RMAT_T3))
+        ub = x >= np.uint64(t[1])                          # quadrants (1,0), (1,1)
+        vb = ((x >= np.uint64(t[0])) & (x < np.uint64(t[1]))) | (x >= np.uint64(t[2]))
         u |= np.where(ub, bit, np.uint64(0))
         v |= np.where(vb, bit, np.uint64(0))
     if permuted:

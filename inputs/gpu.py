@@ -31,7 +31,10 @@ def _load():
         lib.gen_csr_abort.argtypes = [P]
         lib.gen_incr_batch.argtypes = [U64, ctypes.c_int, U64, U64, U64, P, P, P]
         lib.gen_exp_weights.argtypes = [P, P, ctypes.c_uint32, ctypes.c_int64, U64, P, P]
-        for f in (lib.gen_csr_begin, lib.gen_csr_finish, lib.gen_incr_batch, lib.gen_exp_weights):
+        lib.gen_rmat_stream.argtypes = [U64, ctypes.c_int, U64, U64, ctypes.c_uint32, ctypes.c_uint32,
+                                        ctypes.c_uint32, ctypes.c_int, P, P]
+        for f in (lib.gen_csr_begin, lib.gen_csr_finish, lib.gen_incr_batch, lib.gen_exp_weights,
+                  lib.gen_rmat_stream):
             f.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -102,3 +105,14 @@ def exp_weights(d_off, d_adj, seed: int, stream=None):
     if rc:
         raise RuntimeError(f"gen_exp_weights failed: {rc}")
     return w[:m]
+
+
+def rmat_stream(seed: int, s: int, first: int, count: int, t=gen.RM_T, permuted: bool = False, out=None,
+                stream=None):
+    """Device (count, 2) int32 RMAT pairs (gen.rmat_pairs' values) -- the Table 4 RM stream by default."""
+    out = torch.empty((count, 2), dtype=torch.int32, device="cuda") if out is None else out
+    st = torch.cuda.current_stream().cuda_stream if stream is None else stream
+    rc = _load().gen_rmat_stream(seed, s, first, count, t[0], t[1], t[2], 1 if permuted else 0, out.data_ptr(), st)
+    if rc:
+        raise RuntimeError(f"gen_rmat_stream failed: {rc}")
+    return out

@@ -54,3 +54,11 @@ def test_exp_weights_bytes(scale):
     ho, ha = gen.grid(2, 64, 70)
     assert np.array_equal(ggen.exp_weights(go, ga, 11).cpu().numpy().view(np.uint32),
                           gen.exp_weights(ho, ha, 11).view(np.uint32))
+
+
+def test_rm_stream_bytes():
+    """The Table 4 RM stream (a,b,c = .5,.1,.1, unpermuted) equals gen.rmat_pairs."""
+    for s, first, count, perm in ((10, 0, 5000, False), (30, 123456, 4096, False), (20, 7, 3000, True)):
+        d = ggen.rmat_stream(3, s, first, count, permuted=perm).cpu().numpy().view(np.uint32)
+        u, v = gen.rmat_pairs(3, s, first, count, permuted=perm, t=gen.RM_T)
+        assert np.array_equal(d[:, 0], u.astype(np.uint32)) and np.array_equal(d[:, 1], v.astype(np.uint32))
