@@ -392,8 +392,11 @@ __global__ void __launch_bounds__(1024) k_amsf_lmax(const uint32_t* P, uint32_t 
 // vertices activated in this bucket (order[start[i] .. start[i+1])), or, after
 // an anchor move, order[0 .. start[i+1]).  Survivors are appended to the next
 // carry list.
+#ifndef CC_AMSF_ROUND_MINB
+#define CC_AMSF_ROUND_MINB 1
+#endif
 template <int MODE>
-__global__ void __launch_bounds__(kBlock) k_amsf_round(
+__global__ void __launch_bounds__(kBlock, CC_AMSF_ROUND_MINB) k_amsf_round(
     const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, const float* __restrict__ w, uint32_t* P,
     const uint32_t* __restrict__ wlo, const uint32_t* __restrict__ whi, const uint32_t* __restrict__ order,
     const unsigned long long* __restrict__ start, uint32_t round, double blo, double bhi,
