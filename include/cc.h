@@ -79,6 +79,9 @@ typedef int cc_status;
 #define CC_FLAG_UF_ASYNC    (1u << 2)  /* UF-Async link rule instead of UF-Rem-CAS */
 #define CC_FLAG_HALVE       (1u << 3)  /* HalveAtomicOne instead of SplitAtomicOne */
 #define CC_FLAG_FIND_SPLIT  (1u << 4)  /* incremental queries use FindAtomicSplit  */
+#define CC_FLAG_FIND_NAIVE  (1u << 15) /* incremental queries use FindNaive; default:
+                                          path halving with plain stores (no hook runs in
+                                          the query phase)                                 */
 #define CC_FLAG_NO_DEGSKIP  (1u << 5)  /* also finish vertices whose whole list was sampled      */
 #define CC_FLAG_NO_MIDCOMPRESS (1u << 6) /* never run the compress between k-out rounds        */
 #define CC_FLAG_MIDCOMPRESS (1u << 7)  /* always run it (default: a 1024-sample probe of the

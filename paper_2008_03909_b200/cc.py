@@ -36,6 +36,7 @@ FLAG_NO_REFILL = 1 << 11
 FLAG_AMSF_PLAIN = 1 << 12
 FLAG_FINISH_CRFA = 1 << 13
 FLAG_AMSF_NO_INDEX = 1 << 14
+FLAG_FIND_NAIVE = 1 << 15
 
 # every symbol include/cc.h and include/cc_bench.h declare
 EXPORTS = [

@@ -319,7 +319,7 @@ constexpr int kIdTable = 4096;
 #ifndef CC_AMSF_ANCHOR_DIV
 #define CC_AMSF_ANCHOR_DIV 256
 #endif
-__global__ void __launch_bounds__(1024) k_amsf_lmax(const uint32_t* P, uint32_t n, uint64_t seed, uint32_t round,
+__global__ void __launch_bounds__(1024) k_amsf_lmax(uint32_t* P, uint32_t n, uint64_t seed, uint32_t round,
                                                     uint32_t samples, AmsfCtl* ac)
 {
     __shared__ uint32_t keys[kIdTable];
@@ -332,13 +332,13 @@ __global__ void __launch_bounds__(1024) k_amsf_lmax(const uint32_t* P, uint32_t 
         cnts[i] = 0;
     }
     if (t == 0) {
-        s_ra = ac->anchor == kSentinel ? kSentinel : find_naive(P, ac->anchor);   // no hook runs now
+        s_ra = ac->anchor == kSentinel ? kSentinel : find_halve_quiet(P, ac->anchor);   // no hook runs now
         s_cnt_ra = 0;
     }
     __syncthreads();
     for (int i = t; i < (int)samples; i += blockDim.x) {
         const uint32_t sv = uniform_below(mix(seed, AMSF_IDENT_STREAM, ((uint64_t)round << 20) + (uint64_t)i), n);
-        const uint32_t lab = find_naive(P, sv);
+        const uint32_t lab = find_halve_quiet(P, sv);
         if (lab == s_ra) atomicAdd(&s_cnt_ra, 1u);
         uint32_t h = (lab * 0x9E3779B1u) >> 20;
         while (true) {
@@ -425,7 +425,8 @@ __global__ void __launch_bounds__(kBlock, CC_AMSF_ROUND_MINB) k_amsf_round(
             ++visits;
             const double hi_w = plain ? INFINITY : (double)__uint_as_float(whi[u]);
             const double lo_w = plain ? 0.0 : (double)__uint_as_float(wlo[u]);
-            if (hi_w >= blo && !(skip_root != kSentinel && find_naive(P, u) == skip_root)) {
+            // FindAtomicSplit (hooks run concurrently): walks stay short on chain-shaped inputs
+            if (hi_w >= blo && !(skip_root != kSentinel && find_split(P, u) == skip_root)) {
                 keep = hi_w >= bhi;                            // edges left for later buckets
                 work = lo_w < bhi;                             // maybe an edge in this bucket
             }

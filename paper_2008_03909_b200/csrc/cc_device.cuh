@@ -76,6 +76,23 @@ __device__ __forceinline__ uint32_t find_split(uint32_t* P, uint32_t u)
     return v;
 }
 
+// Path halving without atomics, for phases in which no hook runs (the query
+// phase of a type (3) batch): each step stores the grandparent (an ancestor)
+// into the node; loads are device-scope so a root is never judged from a
+// stale L1 line.
+__device__ __forceinline__ uint32_t find_halve_quiet(uint32_t* P, uint32_t x)
+{
+    uint32_t p = ld_relaxed(P + x);
+    while (p != x) {
+        const uint32_t g = ld_relaxed(P + p);
+        if (g == p) return p;
+        P[x] = g;
+        x = g;
+        p = ld_relaxed(P + x);
+    }
+    return x;
+}
+
 struct NoForest {
     __device__ __forceinline__ void record(uint32_t, uint32_t, uint32_t) const {}
 };

@@ -43,23 +43,28 @@ __global__ void __launch_bounds__(kBlock) k_insert(uint32_t* P, const uint2* __r
 // Queries run after the insert kernel: no hook can happen concurrently, so
 // roots are fixed and FindNaive needs no L2-forced loads; with SPLIT the finds
 // also shorten paths (FindAtomicSplit) for later batches.
-template <bool SPLIT>
+// FIND: 0 = path halving without atomics (default: no hook runs in the query
+// phase, so pointing a node at its grandparent is a plain store of an ancestor;
+// it keeps adversarial chains -- a path inserted in id order -- from costing
+// O(length) per query: 29 s -> 4 ms for 2^20 queries on a 2^24 path), 1 =
+// FindAtomicSplit, 2 = FindNaive.
+template <int FIND>
+__device__ __forceinline__ uint32_t query_find(uint32_t* P, uint32_t x)
+{
+    if constexpr (FIND == 1) return find_split(P, x);
+    else if constexpr (FIND == 2) return find_naive(P, x);
+    else return find_halve_quiet(P, x);
+}
+
+template <int FIND>
 __global__ void __launch_bounds__(kBlock) k_query(uint32_t* P, const uint2* __restrict__ q, int64_t n_q,
                                                   uint8_t* __restrict__ ans)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_q) return;
     const uint2 e = q[i];
-    uint32_t ra, rb;
-    if constexpr (SPLIT) {
-        ra = find_split(P, e.x);
-        rb = find_split(P, e.y);
-    } else {
-        ra = e.x;
-        for (uint32_t p = P[ra]; p != ra; p = P[ra]) ra = p;
-        rb = e.y;
-        for (uint32_t p = P[rb]; p != rb; p = P[rb]) rb = p;
-    }
+    const uint32_t ra = query_find<FIND>(P, e.x);
+    const uint32_t rb = query_find<FIND>(P, e.y);
     ans[i] = ra == rb ? 1 : 0;
 }
 
@@ -107,7 +112,7 @@ __global__ void __launch_bounds__(kBlock) k_mixed(uint32_t* P, const uint2* __re
 // relaxed device-scope loads, so the barrier also orders their visibility.
 constexpr int64_t kSmallBatch = 8192;
 
-template <int MODE, bool SPLIT>
+template <int MODE, int FIND>
 __global__ void __launch_bounds__(1024) k_small_batch(uint32_t* P, const uint2* __restrict__ ins, int64_t n_ins,
                                                       const uint2* __restrict__ q, int64_t n_q,
                                                       uint8_t* __restrict__ ans)
@@ -119,14 +124,14 @@ __global__ void __launch_bounds__(1024) k_small_batch(uint32_t* P, const uint2* 
     __syncthreads();
     for (int64_t i = threadIdx.x; i < n_q; i += blockDim.x) {
         const uint2 e = q[i];
-        const uint32_t ra = SPLIT ? find_split(P, e.x) : find_naive(P, e.x);
-        const uint32_t rb = SPLIT ? find_split(P, e.y) : find_naive(P, e.y);
+        const uint32_t ra = query_find<FIND>(P, e.x);
+        const uint32_t rb = query_find<FIND>(P, e.y);
         ans[i] = ra == rb ? 1 : 0;
     }
 }
 
 // The multi-batch form of k_small_batch: one CTA walks the whole batch sequence.
-template <int MODE, bool SPLIT>
+template <int MODE, int FIND>
 __global__ void __launch_bounds__(1024) k_small_batches(uint32_t* P, const uint2* __restrict__ ins,
                                                         const uint2* __restrict__ q, uint8_t* __restrict__ ans,
                                                         const int64_t* __restrict__ oi, const int64_t* __restrict__ oq,
@@ -140,8 +145,8 @@ __global__ void __launch_bounds__(1024) k_small_batches(uint32_t* P, const uint2
         __syncthreads();                         // the batch's insert/query barrier
         for (int64_t i = oq[b] + threadIdx.x; i < oq[b + 1]; i += blockDim.x) {
             const uint2 e = q[i];
-            const uint32_t ra = SPLIT ? find_split(P, e.x) : find_naive(P, e.x);
-            const uint32_t rb = SPLIT ? find_split(P, e.y) : find_naive(P, e.y);
+            const uint32_t ra = query_find<FIND>(P, e.x);
+            const uint32_t rb = query_find<FIND>(P, e.y);
             ans[i] = ra == rb ? 1 : 0;
         }
         __syncthreads();                         // batch b+1 starts after batch b's queries
@@ -200,16 +205,19 @@ static cc_status insert_query(cc_incr* h, const uint32_t* ins, int64_t n_ins, co
     if (n_ins + n_q <= kSmallBatch && !(h->flags & CC_FLAG_WAIT_FREE)) {
         const uint2* e = reinterpret_cast<const uint2*>(ins);
         const uint2* q = reinterpret_cast<const uint2*>(qs);
-        const bool split = (h->flags & CC_FLAG_FIND_SPLIT) != 0;
+        const int find = (h->flags & CC_FLAG_FIND_SPLIT) ? 1 : (h->flags & CC_FLAG_FIND_NAIVE) ? 2 : 0;
         if (h->flags & CC_FLAG_UF_ASYNC) {
-            if (split) k_small_batch<2, true><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
-            else k_small_batch<2, false><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
+            if (find == 1) k_small_batch<2, 1><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
+            else if (find == 2) k_small_batch<2, 2><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
+            else k_small_batch<2, 0><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
         } else if (h->flags & CC_FLAG_HALVE) {
-            if (split) k_small_batch<1, true><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
-            else k_small_batch<1, false><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
+            if (find == 1) k_small_batch<1, 1><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
+            else if (find == 2) k_small_batch<1, 2><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
+            else k_small_batch<1, 0><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
         } else {
-            if (split) k_small_batch<0, true><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
-            else k_small_batch<0, false><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
+            if (find == 1) k_small_batch<0, 1><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
+            else if (find == 2) k_small_batch<0, 2><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
+            else k_small_batch<0, 0><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
         }
         CC_LAUNCH_CHECK("k_small_batch");
         return CC_OK;
@@ -236,8 +244,9 @@ static cc_status insert_query(cc_incr* h, const uint32_t* ins, int64_t n_ins, co
     // ---- kernel boundary: the insert/query barrier of type (3) ----
     if (n_q > 0) {
         const uint2* q = reinterpret_cast<const uint2*>(qs);
-        if (h->flags & CC_FLAG_FIND_SPLIT) k_query<true><<<nblocks(n_q), kBlock, 0, s>>>(h->P, q, n_q, ans);
-        else k_query<false><<<nblocks(n_q), kBlock, 0, s>>>(h->P, q, n_q, ans);
+        if (h->flags & CC_FLAG_FIND_SPLIT) k_query<1><<<nblocks(n_q), kBlock, 0, s>>>(h->P, q, n_q, ans);
+        else if (h->flags & CC_FLAG_FIND_NAIVE) k_query<2><<<nblocks(n_q), kBlock, 0, s>>>(h->P, q, n_q, ans);
+        else k_query<0><<<nblocks(n_q), kBlock, 0, s>>>(h->P, q, n_q, ans);
         CC_LAUNCH_CHECK("k_query");
     }
     return CC_OK;
@@ -389,18 +398,21 @@ cc_status cc_incr_batches(cc_incr* h, int64_t nb, const int64_t* ins_counts, con
         CC_CUDA_TRY(cudaMemcpyAsync(d_off, both.data(), sizeof(int64_t) * both.size(), cudaMemcpyHostToDevice, s));
         const uint2* e = reinterpret_cast<const uint2*>(d_ins);
         const uint2* q = reinterpret_cast<const uint2*>(d_q);
-        const bool split = (h->flags & CC_FLAG_FIND_SPLIT) != 0;
+        const int find = (h->flags & CC_FLAG_FIND_SPLIT) ? 1 : (h->flags & CC_FLAG_FIND_NAIVE) ? 2 : 0;
         const int64_t* po = d_off;
         const int64_t* pq = d_off + nb + 1;
         if (h->flags & CC_FLAG_UF_ASYNC) {
-            if (split) k_small_batches<2, true><<<1, 1024, 0, s>>>(h->P, e, q, d_ans, po, pq, nb);
-            else k_small_batches<2, false><<<1, 1024, 0, s>>>(h->P, e, q, d_ans, po, pq, nb);
+            if (find == 1) k_small_batches<2, 1><<<1, 1024, 0, s>>>(h->P, e, q, d_ans, po, pq, nb);
+            else if (find == 2) k_small_batches<2, 2><<<1, 1024, 0, s>>>(h->P, e, q, d_ans, po, pq, nb);
+            else k_small_batches<2, 0><<<1, 1024, 0, s>>>(h->P, e, q, d_ans, po, pq, nb);
         } else if (h->flags & CC_FLAG_HALVE) {
-            if (split) k_small_batches<1, true><<<1, 1024, 0, s>>>(h->P, e, q, d_ans, po, pq, nb);
-            else k_small_batches<1, false><<<1, 1024, 0, s>>>(h->P, e, q, d_ans, po, pq, nb);
+            if (find == 1) k_small_batches<1, 1><<<1, 1024, 0, s>>>(h->P, e, q, d_ans, po, pq, nb);
+            else if (find == 2) k_small_batches<1, 2><<<1, 1024, 0, s>>>(h->P, e, q, d_ans, po, pq, nb);
+            else k_small_batches<1, 0><<<1, 1024, 0, s>>>(h->P, e, q, d_ans, po, pq, nb);
         } else {
-            if (split) k_small_batches<0, true><<<1, 1024, 0, s>>>(h->P, e, q, d_ans, po, pq, nb);
-            else k_small_batches<0, false><<<1, 1024, 0, s>>>(h->P, e, q, d_ans, po, pq, nb);
+            if (find == 1) k_small_batches<0, 1><<<1, 1024, 0, s>>>(h->P, e, q, d_ans, po, pq, nb);
+            else if (find == 2) k_small_batches<0, 2><<<1, 1024, 0, s>>>(h->P, e, q, d_ans, po, pq, nb);
+            else k_small_batches<0, 0><<<1, 1024, 0, s>>>(h->P, e, q, d_ans, po, pq, nb);
         }
         CC_LAUNCH_CHECK("k_small_batches");
         // the host vector `both` must outlive the async copy: synchronise before returning

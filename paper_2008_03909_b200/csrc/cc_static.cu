@@ -231,12 +231,40 @@ __device__ __forceinline__ uint32_t root_plain(const uint32_t* P, uint32_t r)
     return r;
 }
 
+// Root walk with path halving, for passes in which no hook runs (compress, the
+// finish scan): each step points x at its grandparent.  Plain walks were
+// quadratic on long chains -- every thread of every resident block walking the
+// same uncompressed chain (an id-ordered path: 1.6 s for 16M vertices); with
+// halving the concurrent walkers shorten it for each other.  The halving store
+// is a CAS on the value just read: a pass's owner thread writes the ROOT into
+// its slots, and a plain halving store landing after it would replace that root
+// by a mere ancestor (wrong final labels); the CAS fails instead.
+__device__ __forceinline__ uint32_t root_halve(uint32_t* P, uint32_t x)
+{
+    uint32_t p = P[x];
+    // the first steps walk without writes (normal trees are shallow after a link
+    // phase that splits as it goes), halving only deeper chains
+#pragma unroll 1
+    for (int i = 0; i < 16 && p != x; ++i) {
+        x = p;
+        p = P[x];
+    }
+    while (p != x) {
+        const uint32_t g = P[p];
+        if (g == p) return p;
+        atomicCAS(P + x, p, g);
+        x = g;
+        p = P[x];
+    }
+    return x;
+}
+
 // Roots of 8 slots with their first-level gathers issued together (8
 // independent loads in flight instead of 8 dependent walks); deeper walks,
 // rare after a compress, continue one slot at a time.  (A level-by-level
 // variant that batches every level measured slower on C4: more registers
 // and a serial live-mask loop for little extra parallelism.)
-__device__ __forceinline__ uint32_t roots8(const uint32_t* P, const uint32_t (&vv)[8], const uint32_t (&pp)[8],
+__device__ __forceinline__ uint32_t roots8(uint32_t* P, const uint32_t (&vv)[8], const uint32_t (&pp)[8],
                                            uint32_t (&rr)[8], uint32_t known_root = kSentinel)
 {
     uint32_t q[8], gathers = 0;
@@ -247,7 +275,7 @@ __device__ __forceinline__ uint32_t roots8(const uint32_t* P, const uint32_t (&v
         gathers += g;
     }
 #pragma unroll
-    for (int s = 0; s < 8; ++s) rr[s] = q[s] == pp[s] ? pp[s] : root_plain(P, q[s]);
+    for (int s = 0; s < 8; ++s) rr[s] = q[s] == pp[s] ? pp[s] : root_halve(P, q[s]);
     return gathers;                                      // first-level parent reads issued
 }
 
@@ -288,7 +316,7 @@ __global__ void __launch_bounds__(kBlock, CC_COMPRESS_MINB) k_compress(uint32_t*
             for (uint64_t v64 = base + threadIdx.x; v64 < n; v64 += kBlock) {      // ragged tail
                 const uint32_t v = (uint32_t)v64;
                 const uint32_t p = P[v];
-                const uint32_t r = p == v ? v : root_plain(P, p);
+                const uint32_t r = p == v ? v : root_halve(P, p);
                 if (CNT) gathers += p != v;
                 if (r != p) {
                     P[v] = r;
@@ -314,7 +342,7 @@ __global__ void __launch_bounds__(kBlock) k_compress_scalar(uint32_t* P, uint32_
     if (v64 < n) {
         const uint32_t v = (uint32_t)v64;
         const uint32_t p = P[v];
-        const uint32_t r = p == v ? v : root_plain(P, p);
+        const uint32_t r = p == v ? v : root_halve(P, p);
         if (r != p) { P[v] = r; writes = 1; }
         if (out) out[v] = r;
     }
@@ -593,7 +621,7 @@ __global__ void __launch_bounds__(kBlock) k_rank_fill(uint2* rbw, uint32_t nw, c
 // atomicAdd on the count), then a max-reduction of (count, -label).
 constexpr int kIdTable = 4096;                       // 2 * max samples (2048)
 
-__global__ void __launch_bounds__(1024) k_identify(const uint32_t* P, uint32_t n, uint64_t seed,
+__global__ void __launch_bounds__(1024) k_identify(uint32_t* P, uint32_t n, uint64_t seed,
                                                    uint32_t samples, const uint32_t* force, Ctl* ctl,
                                                    uint32_t* lmax_out, const uint2* rbw, const uint32_t* rid)
 {
@@ -616,7 +644,7 @@ __global__ void __launch_bounds__(1024) k_identify(const uint32_t* P, uint32_t n
     for (int i = t; i < (int)samples; i += blockDim.x) {
         const uint32_t sv = uniform_below(mix(seed, IDENT_STREAM, (uint64_t)i), n);
         // no hook runs concurrently; contracted: P[sv] is sv's F0 root
-        const uint32_t lab = rbw ? expand_root(rbw, rid, P[sv]) : root_plain(P, sv);
+        const uint32_t lab = rbw ? expand_root(rbw, rid, P[sv]) : root_halve(P, sv);
         uint32_t h = (lab * 0x9E3779B1u) >> 20;      // 12-bit multiplicative hash
         while (true) {
             const uint32_t old = atomicCAS(&keys[h], kSentinel, lab);

@@ -189,3 +189,20 @@ def test_amsf_hubs_bucket_index():
         want = oracle.amsf(off, adj, w, eps)
         for opt in (OPTS[0], OPTS[1], OPTS[6], dict(flags=cc.FLAG_HALVE)):
             check(off, adj, w, eps, *run(off, adj, w, eps, **opt), want=want)
+
+
+def test_amsf_chain_shaped():
+    """A path whose weights grow along it: every bucket hooks the next stretch under
+    the previous one (one long chain); the finds must stay exact and fast."""
+    import time
+    n = 1 << 18
+    ids = np.arange(n - 1, dtype=np.uint64)
+    off, adj = oracle.csr_from_pairs(n, np.stack([ids, ids + 1], 1))
+    src = np.repeat(np.arange(n, dtype=np.uint64), np.diff(off))
+    w = (1.0 + np.minimum(src, adj.astype(np.uint64)).astype(np.float64) / 1000.0).astype(np.float32)
+    want = oracle.amsf(off, adj, w, 0.25)
+    for opt in (OPTS[0], OPTS[1]):
+        t0 = time.time()
+        E, W, tot = run(off, adj, w, 0.25, **opt)
+        assert time.time() - t0 < 10.0
+        check(off, adj, w, 0.25, E, W, tot, want=want)

@@ -41,7 +41,7 @@ def static_labels(n, batches):
     return oracle.cc_bfs(off, adj)
 
 
-@pytest.mark.parametrize("flags", [0, cc.FLAG_HALVE, cc.FLAG_UF_ASYNC, cc.FLAG_FIND_SPLIT])
+@pytest.mark.parametrize("flags", [0, cc.FLAG_HALVE, cc.FLAG_UF_ASYNC, cc.FLAG_FIND_SPLIT, cc.FLAG_FIND_NAIVE])
 @pytest.mark.parametrize("batch", [1, 10, 1000, 1 << 14])
 def test_stream_bit_exact(flags, batch):
     scale = 12
@@ -162,7 +162,7 @@ def test_wait_free_prefix_soundness(flags):
 
 
 @pytest.mark.parametrize("batch", [1, 10, 1000, 9000])
-@pytest.mark.parametrize("flags", [0, cc.FLAG_FIND_SPLIT | cc.FLAG_HALVE, cc.FLAG_VALIDATE])
+@pytest.mark.parametrize("flags", [0, cc.FLAG_FIND_SPLIT | cc.FLAG_HALVE, cc.FLAG_VALIDATE, cc.FLAG_FIND_NAIVE])
 def test_multi_batch_call_bit_exact(batch, flags):
     """cc_incr_batches == a sequence of cc_incr_batch calls == the oracle."""
     n = 1 << 12
@@ -181,3 +181,36 @@ def test_multi_batch_call_bit_exact(batch, flags):
     h.close()
     assert np.array_equal(ans.cpu().numpy(), want)
     assert np.array_equal(u32(lab), want_lab)
+
+
+def test_adversarial_chain_queries():
+    """A path inserted in id order builds one chain of length n (every hook puts
+    i+1 under i); the default halving queries must answer it exactly and fast,
+    in one batch and in many small batches (the single-CTA path)."""
+    import time
+    n = 1 << 20
+    ids = np.arange(n - 1, dtype=np.uint32)
+    path = np.stack([ids, ids + 1], 1)
+    rng = np.random.default_rng(4)
+    qs = rng.integers(0, n, (1 << 16, 2)).astype(np.uint32)
+    qs[:100, 1] = qs[:100, 0]
+    want, _ = oracle.incr_run(n, [(path, qs)])
+    for flags in (0, cc.FLAG_FIND_SPLIT):
+        inc = pkg.IncrementalCC(n, flags=flags)
+        t0 = time.time()
+        ans = inc.batch(torch.from_numpy(path.view(np.int32)).cuda(), torch.from_numpy(qs.view(np.int32)).cuda())
+        torch.cuda.synchronize()
+        assert time.time() - t0 < 5.0
+        assert np.array_equal(ans.cpu().numpy(), want)
+        inc.close()
+    # small batches: 256 inserts each, a query batch at the end (k_small_batches)
+    inc = pkg.IncrementalCC(4096)
+    small = path[:4095]
+    batches = [(small[i:i + 256], qs[:64] % 4096) for i in range(0, 4095, 256)]
+    want2, _ = oracle.incr_run(4096, batches)
+    got = []
+    for ins, q in batches:
+        got.append(inc.batch(torch.from_numpy(np.ascontiguousarray(ins).view(np.int32)).cuda(),
+                             torch.from_numpy(np.ascontiguousarray(q).view(np.int32)).cuda()).cpu().numpy())
+    assert np.array_equal(np.concatenate(got), want2)
+    inc.close()

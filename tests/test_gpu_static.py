@@ -345,3 +345,19 @@ def test_pinned_host_buffers_zero_copy():
     d_lab = torch.empty(n, dtype=torch.int32, device="cuda")
     cc.cc_labels(d_off, h_adj, n, adj.size, d_lab, cc.make_opts())
     assert np.array_equal(u32(d_lab), want)
+
+
+def test_adversarial_long_chains():
+    """Id-ordered paths make round 0 one chain of length n (P[u] = u - 1); the
+    compress and finish walks halve paths, so this stays fast and exact."""
+    import time
+    n = 1 << 21
+    ids = np.arange(n - 1, dtype=np.uint64)
+    for pairs in (np.stack([ids, ids + 1], 1), np.stack([ids[:-1], ids[:-1] + 2], 1)):
+        off, adj = oracle.csr_from_pairs(n, pairs)
+        want = oracle.cc_bfs(off, adj)
+        for opt in (OPTION_GRID[0], OPTION_GRID[1], dict(k=2, variant="afforest", flags=cc.FLAG_NO_MIDCOMPRESS)):
+            t0 = time.time()
+            got = run_labels(off, adj, **opt)
+            assert time.time() - t0 < 5.0, opt
+            assert np.array_equal(got, want), opt
