@@ -98,8 +98,10 @@ __global__ void __launch_bounds__(kBlock) k_mixed(uint32_t* P, const uint2* __re
     }
     const uint2 e = q[i];
     while (true) {
-        const uint32_t ra = find_naive(P, e.x);
-        const uint32_t rb = find_naive(P, e.y);
+        // FindAtomicSplit (safe next to concurrent hooks): each returned value was a root
+        // when it was read, which is all the linearization argument needs, and chains stay short
+        const uint32_t ra = find_split(P, e.x);
+        const uint32_t rb = find_split(P, e.y);
         if (ra == rb) { ans[i] = 1; return; }
         if (ld_relaxed(P + ra) == ra) { ans[i] = 0; return; }
     }

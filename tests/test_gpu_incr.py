@@ -203,6 +203,15 @@ def test_adversarial_chain_queries():
         assert time.time() - t0 < 5.0
         assert np.array_equal(ans.cpu().numpy(), want)
         inc.close()
+    # wait-free: answers are only prefix-sound here (everything connects during the batch);
+    # a == b must be 1, and it must stay fast on the chain
+    inc = pkg.IncrementalCC(n, flags=cc.FLAG_WAIT_FREE)
+    t0 = time.time()
+    ans = inc.batch(torch.from_numpy(path.view(np.int32)).cuda(), torch.from_numpy(qs.view(np.int32)).cuda())
+    torch.cuda.synchronize()
+    assert time.time() - t0 < 5.0
+    assert ans.cpu().numpy()[:100].all()
+    inc.close()
     # small batches: 256 inserts each, a query batch at the end (k_small_batches)
     inc = pkg.IncrementalCC(4096)
     small = path[:4095]
