@@ -857,6 +857,9 @@ __global__ void __launch_bounds__(kBlock) k_finish_proc(
     }
 }
 
+// The long lists (> kBigDeg entries): every CTA walks the (short) queue of big
+// vertices and takes a grid-strided share of each list, so one hub of millions
+// of entries is spread over the whole GPU instead of one CTA.
 template <int MODE, bool SF>
 __global__ void __launch_bounds__(512) k_finish_big(const int64_t* __restrict__ off,
                                                     const uint32_t* __restrict__ adj, uint32_t* P,
@@ -865,7 +868,9 @@ __global__ void __launch_bounds__(512) k_finish_big(const int64_t* __restrict__ 
 {
     __shared__ uint32_t s_ru;
     const unsigned long long total = ctl->big_count;
-    for (unsigned long long i = blockIdx.x; i < total; i += gridDim.x) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    uint32_t hooks = 0;
+    for (unsigned long long i = 0; i < total; ++i) {
         const uint32_t u = big[i];
         int64_t b = off[u];
         const int64_t e = off[u + 1];
@@ -874,15 +879,14 @@ __global__ void __launch_bounds__(512) k_finish_big(const int64_t* __restrict__ 
         if (threadIdx.x == 0) s_ru = find_naive(P, u);
         __syncthreads();
         const uint32_t ru = s_ru;
-        uint32_t hooks = 0;
-        for (int64_t x = b + threadIdx.x; x < e; x += blockDim.x) {
+        for (int64_t x = b + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < e; x += stride) {
             const uint32_t v = adj[x];
             if (ld_relaxed(P + v) == ru) continue;
             if constexpr (SF) hooks += link<MODE>(P, u, v, Forest{F});
             else hooks += link<MODE>(P, u, v, NoForest{});
         }
-        if (cnt) warp_count(&cnt->finish_hooks, hooks);
     }
+    if (cnt) warp_count(&cnt->finish_hooks, hooks);
 }
 
 // ---------------------------------------------------------------------------

@@ -31,20 +31,23 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 24
 for name, (off, adj) in shapes(n):
     d_off = torch.from_numpy(off).cuda()
     d_adj = torch.from_numpy(adj.view(np.int32)).cuda()
-    lab = pkg.connected_components(d_off, d_adj)
-    torch.cuda.synchronize()
-    ts = []
-    for _ in range(3):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        pkg.connected_components(d_off, d_adj, out=lab)
-        e1.record()
-        e1.synchronize()
-        ts.append(e0.elapsed_time(e1))
     t0 = time.time()
-    ok = np.array_equal(lab.cpu().numpy().view(np.uint32), oracle.cc_bfs(off, adj))
-    print(f"{name:24s} n={off.size - 1:9d} m={adj.size:10d} gpu {min(ts):8.3f} ms  bit-exact={ok}  (oracle {time.time() - t0:.1f}s)",
-          flush=True)
+    want = oracle.cc_bfs(off, adj)
+    t_or = time.time() - t0
+    for k in (2, 0):
+        lab = pkg.connected_components(d_off, d_adj, k=k)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            pkg.connected_components(d_off, d_adj, k=k, out=lab)
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ok = np.array_equal(lab.cpu().numpy().view(np.uint32), want)
+        print(f"{name:24s} k={k} n={off.size - 1:9d} m={adj.size:10d} gpu {min(ts):8.3f} ms  bit-exact={ok}"
+              f"  (oracle {t_or:.1f}s)", flush=True)
 
 # incremental: a path inserted in id order (one batch, then 16 batches), then 2^20 queries
 inc_n = n
