@@ -89,7 +89,7 @@ def test_amsf_small(opt):
         check(off, adj, w, 0.25, E, W, tot)
 
 
-@pytest.mark.parametrize("eps", [0.01, 0.1, 1.0, 4.0])
+@pytest.mark.parametrize("eps", [0.002, 0.01, 0.1, 1.0, 4.0])
 def test_amsf_eps(eps):
     off, adj = gen.rmat(seed=8, scale=12)
     w = gen.exp_weights(off, adj, 8)
