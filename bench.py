@@ -47,6 +47,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-scale", type=int, default=CPU_SAMPLE_SCALE)
+    p.add_argument("--cpu-batches", type=int, default=256, help="C5: batches the oracle replays for cpu_baseline")
     p.add_argument("--l2-fetch", type=int, default=-1, help="cudaLimitMaxL2FetchGranularity (bytes) or -1")
     p.add_argument("--study", action="store_true", help="NEXT-1 sampling variant x k sweep on C2-C4")
     p.add_argument("--incr-sweep", action="store_true", help="NEXT-2 incremental variants sweep")
@@ -429,6 +430,23 @@ def run_ours(a, rank, ws):
 
     # ---- measurement floors (K10, Table 8 analogue P:3732-3799), outside the timed region
     line["floors"] = floors(cc, d_off, d_adj, n, m, labels, stream, mean_ms)
+    # spanning forest on the same graph (Alg. 2): t_SF / t_CC
+    sf_edges = torch.empty((n, 2), dtype=torch.int32, device=dev)
+    sf_num = torch.zeros(1, dtype=torch.int64, device=dev)
+    sf_ms = []
+    for i in range(4):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        cc.cc_spanning_forest(d_off, d_adj, n, m, sf_edges, sf_num, None,
+                              cc.make_opts(k=a.k, variant=variant, flags=a.flags), stream)
+        e1.record(stream)
+        e1.synchronize()
+        if i:
+            sf_ms.append(e0.elapsed_time(e1))
+    line["spanning_forest"] = {"ms": round(statistics.mean(sf_ms), 4), "t_sf_over_t_cc": round(statistics.mean(sf_ms) / mean_ms, 3),
+                               "forest_edges": int(sf_num.item()), "n_minus_c": n - components}
+    del sf_edges
     # The link kernel is bound by dependent random 4-byte accesses into the 4n-byte
     # parent array, not by streaming bandwidth: set its random-access count (one
     # P[v] gather per pending link + one load or CAS per Rem-loop step + the hook
@@ -567,6 +585,88 @@ def run_ours_incr(a, rank, ws, cfg):
             "inserts_per_s": round(nb * cfg.n_ins / (mean_ms * 1e-3), 1),
             "batch_ms": {"p50": batch_ms[len(batch_ms) // 2], "p99": batch_ms[int(len(batch_ms) * 0.99)]},
             "gpu_launches": int(launches), "clocks": clocks}
+
+    # ---- roofline: algorithmic bytes per stream (insert 8 B pair + 8 B for
+    # P[u], P[v] + 4 B per hook; query 8 + 8 + 1 B), hooks = n - final components
+    h = cc.Incr(n, flags=a.flags)
+    for b in range(nb):
+        h.batch(ins[b], cfg.n_ins, qs[b], cfg.n_q, ans[b])
+    lab = torch.empty(n, dtype=torch.int32, device="cuda")
+    h.labels(lab)
+    comps = int((lab == torch.arange(n, device="cuda", dtype=torch.int32)).sum().item())
+    h.close()
+    del lab
+    hooks = n - comps
+    byts = nb * (16 * cfg.n_ins + 17 * cfg.n_q) + 4 * hooks
+    peak, peak_src = peaks()
+    gbs = byts / (mean_ms * 1e-3) / 1e9
+    rg_t = torch.zeros(1, dtype=torch.int32, device="cuda")
+    x = torch.zeros(n, dtype=torch.int32, device="cuda")
+    cnt = 1 << 28
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    cc.random_gather(x, n, cnt, 7, rg_t, stream)
+    e0.record(stream)
+    cc.random_gather(x, n, cnt, 7, rg_t, stream)
+    e1.record(stream)
+    e1.synchronize()
+    rg = cnt / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    acc = nb * 2 * (cfg.n_ins + cfg.n_q)                  # first parent reads: P[u], P[v] of every op
+    line["roofline"] = {"bound": "hbm", "kernel": "k_insert + k_query (whole stream)", "achieved": round(gbs, 1),
+                        "peak": peak, "unit": "GB/s", "frac": round(gbs / peak, 4), "traffic": None,
+                        "peak_source": peak_src, "algorithmic_bytes_per_stream": int(byts), "hooks": hooks,
+                        "random_access_view": {"first_parent_reads_per_stream": acc,
+                                               "achieved_Gaccess_per_s": round(acc / (mean_ms * 1e-3) / 1e9, 2),
+                                               "uniform_random_gather_Gloads_per_s": round(rg, 2),
+                                               "array_bytes": 4 * n}}
+    del x
+
+    # ---- e2e: the same stream through cc_incr_batch with the batches in pinned HOST memory
+    # (used in place through UVA) and the answers written to pinned host memory
+    if not a.no_e2e:
+        h_ins = torch.empty_like(ins, device="cpu").pin_memory()
+        h_qs = torch.empty_like(qs, device="cpu").pin_memory()
+        h_ans = torch.empty((nb, cfg.n_q), dtype=torch.uint8).pin_memory()
+        h_ins.copy_(ins)
+        h_qs.copy_(qs)
+        ts = []
+        for rep in range(2):
+            h = cc.Incr(n, flags=a.flags)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for b in range(nb):
+                h.batch(h_ins[b], cfg.n_ins, h_qs[b], cfg.n_q, h_ans[b])
+            e1.record(stream)
+            e1.synchronize()
+            h.close()
+            ts.append(e0.elapsed_time(e1))
+        e2e_ms = min(ts)
+        line["e2e"] = {"value": round(ops / (e2e_ms * 1e-3) / 1e9, 4), "unit": "Gops/s",
+                       "h2d_bytes_per_step": int(nb * 8 * (cfg.n_ins + cfg.n_q)), "d2h_bytes_per_step": int(nb * cfg.n_q),
+                       "ms_per_step": round(e2e_ms, 3),
+                       "path": "cc_incr_batch with pinned host inserts/queries/answers (zero-copy through UVA)",
+                       "answers_match_device_path": bool(torch.equal(h_ans, ans.cpu()))}
+        del h_ins, h_qs, h_ans
+
+    # ---- cpu_baseline: the oracle (sequential DSU, 1 thread) on the first batches of the
+    # same stream (the generator's bytes), answers checked against the GPU's
+    if not a.no_cpu_baseline and rank == 0:
+        import numpy as np
+
+        import oracle
+        nbs = min(nb, a.cpu_batches)
+        hi = ins[:nbs].cpu().numpy().view(np.uint32)
+        hq = qs[:nbs].cpu().numpy().view(np.uint32)
+        t0 = time.time()
+        want, _ = oracle.incr_run(n, [(hi[b], hq[b]) for b in range(nbs)])
+        t_or = time.time() - t0
+        ops_s = nbs * (cfg.n_ins + cfg.n_q)
+        line["cpu_baseline"] = {"value": round(ops_s / t_or / 1e9, 5), "unit": "Gops/s", "cores": 1, "kind": "oracle",
+                                "sample": f"oracle.incr_run (sequential union-find, 1 thread) on the first {nbs} "
+                                          f"batches of the C5 stream ({ops_s} ops), {t_or:.2f} s",
+                                "host_cores": os.cpu_count(),
+                                "gpu_answers_bit_exact_on_sample": bool(np.array_equal(
+                                    ans[:nbs].cpu().numpy().reshape(-1), want))}
     if rank == 0:
         print(json.dumps(line), flush=True)
 

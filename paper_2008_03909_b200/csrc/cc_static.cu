@@ -36,12 +36,14 @@ struct Ctl {
     unsigned long long pend_count;
     unsigned long long cand_count;
     unsigned long long big_count;
+    unsigned long long huge_count;   // lists > kHugeDeg, filled from the END of the big queue
     unsigned int lmax;
     unsigned int err;
     unsigned int skip_mid;      // set by k_probe: the round-0 chains are short
 };
 
 constexpr int kBigDeg = 4096;     // >  : one CTA per vertex (second kernel)
+constexpr int64_t kHugeDeg = 1 << 20;   // >  : every CTA takes a slice of the list
 
 // ---------------------------------------------------------------------------
 // K0: H1 + first k-out round + pending list + finish bitmap.
@@ -784,7 +786,8 @@ __global__ void __launch_bounds__(kBlock, CC_FINISH_MINB) k_finish(uint32_t* P, 
 template <int MODE, bool SF>
 __global__ void __launch_bounds__(kBlock) k_finish_proc(
     const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, uint32_t* P,
-    const uint32_t* __restrict__ cq, Ctl* ctl, uint32_t skip_prefix, uint32_t* big, uint2* F, cc_counters* cnt)
+    const uint32_t* __restrict__ cq, Ctl* ctl, uint32_t skip_prefix, uint32_t* big, unsigned long long big_cap,
+    uint2* F, cc_counters* cnt)
 {
     const unsigned long long total = ctl->cand_count;
     const unsigned lane = threadIdx.x & 31;
@@ -813,8 +816,11 @@ __global__ void __launch_bounds__(kBlock) k_finish_proc(
             warp_count(&cnt->finish_edges, cand ? (uint32_t)min(d, (int64_t)0xFFFFFFFF) : 0u);
             warp_count(&cnt->big_vertices, isbig ? 1u : 0u);
         }
-        const unsigned long long bpos = warp_append(&ctl->big_count, isbig ? 1u : 0u);
-        if (isbig) big[bpos] = u;
+        const bool ishuge = isbig && d > kHugeDeg;
+        const unsigned long long bpos = warp_append(&ctl->big_count, isbig && !ishuge ? 1u : 0u);
+        const unsigned long long hpos = warp_append(&ctl->huge_count, ishuge ? 1u : 0u);
+        if (isbig && !ishuge) big[bpos] = u;
+        if (ishuge) big[big_cap - 1 - hpos] = u;
         const uint32_t dd = isbig ? 0u : (uint32_t)d;   // <= kBigDeg
         uint32_t incl = dd;                             // inclusive prefix of list lengths
 #pragma unroll
@@ -857,33 +863,41 @@ __global__ void __launch_bounds__(kBlock) k_finish_proc(
     }
 }
 
-// The long lists (> kBigDeg entries): every CTA walks the (short) queue of big
-// vertices and takes a grid-strided share of each list, so one hub of millions
-// of entries is spread over the whole GPU instead of one CTA.
+// The long lists (> kBigDeg entries): one CTA per list (grid-strided over the
+// queue); a list longer than kHugeDeg is instead shared by every CTA (each CTA
+// walks the queue and takes a grid-strided slice of each huge list), so one hub
+// of millions of entries does not serialise on one CTA.
 template <int MODE, bool SF>
 __global__ void __launch_bounds__(512) k_finish_big(const int64_t* __restrict__ off,
                                                     const uint32_t* __restrict__ adj, uint32_t* P,
-                                                    const uint32_t* __restrict__ big, const Ctl* ctl,
-                                                    uint32_t skip_prefix, uint2* F, cc_counters* cnt)
+                                                    const uint32_t* __restrict__ big, unsigned long long big_cap,
+                                                    const Ctl* ctl, uint32_t skip_prefix, uint2* F, cc_counters* cnt)
 {
     __shared__ uint32_t s_ru;
-    const unsigned long long total = ctl->big_count;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const unsigned long long nbig = ctl->big_count, nhuge = ctl->huge_count;
     uint32_t hooks = 0;
-    for (unsigned long long i = 0; i < total; ++i) {
-        const uint32_t u = big[i];
-        int64_t b = off[u];
-        const int64_t e = off[u + 1];
-        b += min((int64_t)skip_prefix, e - b);
-        __syncthreads();
-        if (threadIdx.x == 0) s_ru = find_naive(P, u);
-        __syncthreads();
-        const uint32_t ru = s_ru;
-        for (int64_t x = b + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < e; x += stride) {
-            const uint32_t v = adj[x];
-            if (ld_relaxed(P + v) == ru) continue;
-            if constexpr (SF) hooks += link<MODE>(P, u, v, Forest{F});
-            else hooks += link<MODE>(P, u, v, NoForest{});
+    for (int pass = 0; pass < 2; ++pass) {
+        // pass 0: the big lists, one CTA each; pass 1: the huge lists (queue tail), all CTAs
+        const unsigned long long i0 = pass == 0 ? blockIdx.x : big_cap - nhuge;
+        const unsigned long long i1 = pass == 0 ? nbig : big_cap;
+        const unsigned long long di = pass == 0 ? gridDim.x : 1;
+        for (unsigned long long i = i0; i < i1; i += di) {
+            const uint32_t u = big[i];
+            int64_t b = off[u];
+            const int64_t e = off[u + 1];
+            b += min((int64_t)skip_prefix, e - b);
+            __syncthreads();
+            if (threadIdx.x == 0) s_ru = find_naive(P, u);
+            __syncthreads();
+            const uint32_t ru = s_ru;
+            const int64_t x0 = b + (pass == 1 ? (int64_t)blockIdx.x * blockDim.x : 0) + threadIdx.x;
+            const int64_t step = pass == 1 ? (int64_t)gridDim.x * blockDim.x : (int64_t)blockDim.x;
+            for (int64_t x = x0; x < e; x += step) {
+                const uint32_t v = adj[x];
+                if (ld_relaxed(P + v) == ru) continue;
+                if constexpr (SF) hooks += link<MODE>(P, u, v, Forest{F});
+                else hooks += link<MODE>(P, u, v, NoForest{});
+            }
         }
     }
     if (cnt) warp_count(&cnt->finish_hooks, hooks);
@@ -1431,9 +1445,10 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
                                         (o.flags & CC_FLAG_FINISH_CRFA) != 0);
             if (r) return r;
         } else {
-            k_finish_proc<MODE, SF><<<sms * 8, kBlock, 0, s>>>(off, adj, P, cq, ctl, skip_prefix, big, F, o.counters);
+            k_finish_proc<MODE, SF><<<sms * 8, kBlock, 0, s>>>(off, adj, P, cq, ctl, skip_prefix, big, big_cap, F,
+                                                               o.counters);
             CC_LAUNCH_CHECK("k_finish_proc");
-            k_finish_big<MODE, SF><<<sms * 2, 512, 0, s>>>(off, adj, P, big, ctl, skip_prefix, F, o.counters);
+            k_finish_big<MODE, SF><<<sms * 2, 512, 0, s>>>(off, adj, P, big, big_cap, ctl, skip_prefix, F, o.counters);
             CC_LAUNCH_CHECK("k_finish_big");
         }
         CC_CUDA_TRY(mark(CC_MARK_FINISH_BIG));
