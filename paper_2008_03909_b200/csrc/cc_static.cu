@@ -11,15 +11,23 @@
 //                     sampled edges (v0 > u, j = 1..k-1) go to a pending list;
 //                     a bitmap marks vertices whose list was not wholly sampled
 //                     (degree skip).
-//   Kc k_compress     pointer-jumping compress ("fully compress"; H6)
-//   K1 k_link_pending UF-Rem-CAS links of the pending sampled edges (H2)
+//   Kc k_compress     pointer-jumping compress ("fully compress"; H6),
+//                     root walks halving deep chains (root_halve)
+//   K1 k_link_refill  UF-Rem-CAS + SplitAtomicOne links of the pending sampled
+//                     edges with lane refill (H2; cc_common.cuh); k_link_pending
+//                     for Halve / UF-Async / CC_FLAG_NO_REFILL; k_link_contract
+//                     on the contracted forest with CC_FLAG_CONTRACT
 //   K4 k_identify     IdentifyFrequent over S seeded samples (R9)
 //   K5 k_finish       ONE pass over P fusing the sampling compress (H3) with
-//                     the finish (H5): every vertex is compressed to its root
-//                     r; a marked vertex with r != L_max has its list unioned
-//                     (P:4091-4100), degree-binned lane / warp / CTA-queue
+//                     the finish scan (H5): every vertex is compressed to its
+//                     root r; a marked vertex with r != L_max is queued, and
+//                     k_finish_proc / k_finish_big union its list,
+//                     degree-binned: warp-shared sweep / CTA per list / all
+//                     CTAs per huge list
+//   K5' sv_finish     the finish as Shiloach-Vishkin (= Liu-Tarjan PRF) or
+//                     Liu-Tarjan CRFA rounds (CC_FLAG_FINISH_SV / _CRFA)
 //   K7 forest         Filter of Alg. 2: compact non-sentinel slots in
-//                     slot order
+//                     slot order (cc_common.cuh)
 #include <cuda_runtime.h>
 
 #include <algorithm>
