@@ -229,8 +229,10 @@ cc_status cc_spanning_forest(const int64_t* offsets, const uint32_t* adj, uint32
  *   edge_w    (out, capacity n float, may be NULL): their weights.
  *   num_edges (out, one int64) = n - #components.
  *   total     (out, one double, may be NULL): sum of the forest weights (fp64).
- * All array arguments must be device memory (CC_EINVAL otherwise).  The call
- * synchronises `stream` once, to read W_min / W_max and size the buckets.
+ * Arrays may be device memory, or host memory (pinned or pageable), which is
+ * staged through device scratch (the outputs are copied back and the call
+ * returns after they landed).  The call synchronises `stream` once, to read
+ * W_min / W_max and size the buckets.
  * Errors: CC_EINVAL for eps <= 0 or a non-positive / non-finite weight
  * (checked on the device; outputs untouched). */
 cc_status cc_amsf(const int64_t* offsets, const uint32_t* adj, const float* w, uint32_t n, int64_t m, double eps,

@@ -274,7 +274,9 @@ cc_status cc_spanning_forest(const int64_t* offsets, const uint32_t* adj, uint32
     return CC_OK;
 }
 
-// AMSF-NF-S (include/cc.h): device memory only.
+// AMSF-NF-S (include/cc.h).  Host arrays (pinned or pageable) are staged
+// through device scratch -- the bucket rounds read every list many times, so
+// zero-copy would cross PCIe once per round -- and the outputs copied back.
 cc_status cc_amsf(const int64_t* offsets, const uint32_t* adj, const float* w, uint32_t n, int64_t m, double eps,
                   uint32_t* edges, float* edge_w, int64_t* num_edges, double* total, const cc_opts* opts,
                   void* stream)
@@ -286,23 +288,49 @@ cc_status cc_amsf(const int64_t* offsets, const uint32_t* adj, const float* w, u
     if (!num_edges) { set_error("num_edges is NULL"); return CC_EINVAL; }
     if (n > 0 && !edges) { set_error("edges is NULL"); return CC_EINVAL; }
     if (m > 0 && !w) { set_error("w is NULL"); return CC_EINVAL; }
-    for (const void* p : {(const void*)offsets, (const void*)adj, (const void*)w, (const void*)edges,
-                          (const void*)edge_w, (const void*)num_edges, (const void*)total})
-        if (p && mem_kind(p, nullptr) != MEM_DEVICE) {
-            set_error("cc_amsf: every array argument must be device memory");
-            return CC_EINVAL;
-        }
     cudaStream_t s = (cudaStream_t)stream;
+    auto dev = [](const void* p) { return !p || mem_kind(p, nullptr) == MEM_DEVICE; };
+    const bool host = !dev(offsets) || !dev(adj) || !dev(w) || !dev(edges) || !dev(edge_w) || !dev(num_edges) ||
+                      !dev(total);
+    Stage st{s, {}};
+    const int64_t* d_off = offsets;
+    const uint32_t* d_adj = adj;
+    const float* d_w = w;
+    uint32_t* d_edges = edges;
+    float* d_ew = edge_w;
+    int64_t* d_ne = num_edges;
+    double* d_tot = total;
+    if (!dev(offsets)) CC_CUDA_TRY(st.in(offsets, (size_t)n + 1, (int64_t**)&d_off));
+    if (!dev(adj)) CC_CUDA_TRY(st.in(adj, (size_t)m, (uint32_t**)&d_adj));
+    if (!dev(w)) CC_CUDA_TRY(st.in(w, (size_t)m, (float**)&d_w));
+    if (!dev(edges)) CC_CUDA_TRY(st.in((const uint32_t*)nullptr, 2 * (size_t)std::max<uint32_t>(n, 1), &d_edges));
+    if (!dev(edge_w)) CC_CUDA_TRY(st.in((const float*)nullptr, (size_t)std::max<uint32_t>(n, 1), &d_ew));
+    if (!dev(num_edges)) CC_CUDA_TRY(st.in((const int64_t*)nullptr, 1, &d_ne));
+    if (!dev(total)) CC_CUDA_TRY(st.in((const double*)nullptr, 1, &d_tot));
     if (n == 0) {
-        CC_CUDA_TRY(cudaMemsetAsync(num_edges, 0, sizeof(int64_t), s));
-        if (total) CC_CUDA_TRY(cudaMemsetAsync(total, 0, sizeof(double), s));
-        return CC_OK;
-    }
-    if (o.flags & CC_FLAG_VALIDATE) {
-        rc = validate_csr(offsets, adj, n, m, s);
+        CC_CUDA_TRY(cudaMemsetAsync(d_ne, 0, sizeof(int64_t), s));
+        if (d_tot) CC_CUDA_TRY(cudaMemsetAsync(d_tot, 0, sizeof(double), s));
+    } else {
+        if (o.flags & CC_FLAG_VALIDATE) {
+            rc = validate_csr(d_off, d_adj, n, m, s);
+            if (rc) return rc;
+        }
+        rc = amsf_pipeline(d_off, d_adj, d_w, n, m, eps, d_edges, d_ew, d_ne, d_tot, o, s);
         if (rc) return rc;
     }
-    return amsf_pipeline(offsets, adj, w, n, m, eps, edges, edge_w, num_edges, total, o, s);
+    if (host) {
+        int64_t ne = 0;
+        CC_CUDA_TRY(cudaMemcpyAsync(&ne, d_ne, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        CC_CUDA_TRY(cudaStreamSynchronize(s));
+        if (d_ne != num_edges) *num_edges = ne;
+        if (d_edges != edges && ne)
+            CC_CUDA_TRY(cudaMemcpyAsync(edges, d_edges, sizeof(uint32_t) * 2 * (size_t)ne, cudaMemcpyDeviceToHost, s));
+        if (d_ew != edge_w && ne)
+            CC_CUDA_TRY(cudaMemcpyAsync(edge_w, d_ew, sizeof(float) * (size_t)ne, cudaMemcpyDeviceToHost, s));
+        if (d_tot != total) CC_CUDA_TRY(cudaMemcpyAsync(total, d_tot, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CC_CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    return CC_OK;
 }
 
 }  // extern "C"

@@ -131,8 +131,6 @@ def test_amsf_rejects_bad_input():
     for eps in (0.0, -0.5, float("inf")):
         with pytest.raises(cc.CCError):
             pkg.amsf(d_off, d_adj, w, eps)
-    with pytest.raises(cc.CCError):                     # host weights: device memory only
-        pkg.amsf(d_off, d_adj, w.cpu(), 0.25)
 
 
 def test_amsf_counters():
@@ -206,3 +204,31 @@ def test_amsf_chain_shaped():
         E, W, tot = run(off, adj, w, 0.25, **opt)
         assert time.time() - t0 < 10.0
         check(off, adj, w, 0.25, E, W, tot, want=want)
+
+
+def test_amsf_host_buffers():
+    """Pageable numpy arrays and pinned tensors are staged; results equal the device call."""
+    off, adj = gen.rmat(seed=13, scale=12)
+    w = gen.exp_weights(off, adj, 13)
+    n, m = off.size - 1, adj.size
+    d_off, d_adj = to_dev(off, adj)
+    E0, W0, t0 = pkg.amsf(d_off, d_adj, torch.from_numpy(w).cuda(), 0.25)
+    want = (u32(E0).reshape(-1, 2), W0.cpu().numpy(), t0)
+    # pageable host (numpy) everywhere
+    edges = np.zeros((n, 2), dtype=np.uint32)
+    ew = np.zeros(n, dtype=np.float32)
+    num = np.zeros(1, dtype=np.int64)
+    tot = np.zeros(1, dtype=np.float64)
+    cc.cc_amsf(off, adj, w, n, m, 0.25, edges, ew, num, tot)
+    k = int(num[0])
+    check(off, adj, w, 0.25, edges[:k], ew[:k], float(tot[0]))
+    assert k == want[0].shape[0]
+    # pinned host inputs, device outputs
+    p_off = torch.from_numpy(off).pin_memory()
+    p_adj = torch.from_numpy(adj.view(np.int32)).pin_memory()
+    p_w = torch.from_numpy(w).pin_memory()
+    d_e = torch.empty((n, 2), dtype=torch.int32, device="cuda")
+    d_num = torch.zeros(1, dtype=torch.int64, device="cuda")
+    cc.cc_amsf(p_off, p_adj, p_w, n, m, 0.25, d_e, None, d_num, None)
+    torch.cuda.synchronize()
+    assert int(d_num.item()) == k
