@@ -895,6 +895,9 @@ def run_amsf(a):
         d_off, d_adj = ggen.config_graph(cfg)
         d_w = ggen.exp_weights(d_off, d_adj, cfg.seed)
         n, m = d_off.numel() - 1, d_adj.numel()
+        deg = torch.diff(d_off)
+        m_idx = int(deg[deg > 256].sum().item())         # entries of the indexed lists (cc_amsf.cu kIdxMin)
+        del deg
         edges = torch.empty((n, 2), dtype=torch.int32, device="cuda")
         ew = torch.empty(n, dtype=torch.float32, device="cuda")
         num = torch.zeros(1, dtype=torch.int64, device="cuda")
@@ -917,9 +920,13 @@ def run_amsf(a):
                 if i >= a.warmup:
                     ts.append(e0.elapsed_time(e1))
             ms = float(np.mean(ts))
-            # algorithmic bytes: one weight per inspected entry, the endpoint of every
+            # algorithmic bytes: the weight-range pass (4 B per entry), the bucket index of the
+            # lists longer than 256 (weights read twice, 4 B index entry written), one weight
+            # (+ one index entry when indexed) per inspected entry, the endpoint of every
             # in-bucket entry (<= m), offsets + weight range per visit
-            byts = 4 * c["amsf_edges"] + 4 * m + 24 * c["amsf_visits"]
+            indexed = not (flags & (cc.FLAG_AMSF_PLAIN | cc.FLAG_AMSF_NO_INDEX))
+            byts = (4 * m + (12 * m_idx if indexed else 0) + 4 * c["amsf_edges"]
+                    + (4 * min(c["amsf_edges"], m_idx) if indexed else 0) + 4 * m + 24 * c["amsf_visits"])
             peak, _ = peaks()
             rows.append({"workload": cfg.name, "variant": name, "flags": flags, "eps": a.eps, "ms": round(ms, 3),
                          "GTEPS": round(m / (ms * 1e-3) / 1e9, 2), "rounds": c["amsf_rounds"],

@@ -34,6 +34,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -61,6 +63,12 @@ struct AmsfCtl {
 };
 
 constexpr int64_t kAmsfChunk = 2048;   // lists longer than this are split across warps
+#ifndef CC_AMSF_IDX_MIN
+#define CC_AMSF_IDX_MIN 256
+#endif
+constexpr int64_t kIdxMin = CC_AMSF_IDX_MIN;   // lists longer than this get the bucket index
+constexpr int64_t kIdxWarpMax = 4096;  // ... built by one warp up to this length, else one CTA
+constexpr uint32_t kIdxWarpBins = 512; // the warp build needs nb + 1 <= this
 
 // Record for AMSF hooks: the edge and its weight at the hooked root.
 struct ForestW {
@@ -76,80 +84,35 @@ struct ForestW {
 
 __device__ __forceinline__ bool good_weight(float x) { return x > 0.0f && x < __int_as_float((int)kPosInfBits); }
 
-// Per-vertex lightest / heaviest edge weight and the global range.  A warp takes
-// 32 consecutive vertices; their lists (<= kAmsfChunk entries each) are swept 32
-// entries at a time, each lane finding its entry's owner by a shuffle search, and
-// a segmented min/max scan over the lanes leaves one result per (owner, step) that
-// the segment's last lane folds into the warp's shared slot of that owner -- no
-// atomics.  A longer list is reduced by the whole warp on its own.
+// Per-vertex lightest / heaviest edge weight and the global range.  A thread per
+// vertex walks a list of up to 32 entries (consecutive vertices' lists are
+// adjacent, so the warp's loads stay within a few lines); longer lists are then
+// reduced by the whole warp, coalesced, one at a time.  No atomics except the
+// global range.
 __global__ void __launch_bounds__(kBlock) k_amsf_wrange(const int64_t* __restrict__ off, const float* __restrict__ w,
                                                         uint32_t n, int64_t m, uint32_t* wlo, uint32_t* whi,
                                                         AmsfCtl* ac)
 {
-    __shared__ uint32_t s_lo[kBlock], s_hi[kBlock];
     const unsigned lane = threadIdx.x & 31;
-    uint32_t* mlo = s_lo + (threadIdx.x & ~31u);
-    uint32_t* mhi = s_hi + (threadIdx.x & ~31u);
-    const uint64_t ntiles = ((uint64_t)n + 31) / 32;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     uint32_t gmin = kPosInfBits, gmax = 0, bad = 0;
-    for (uint64_t tile = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; tile < ntiles; tile += nwarps) {
-        const uint64_t u = tile * 32 + lane;
+    for (uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x; t0 < n; t0 += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t u = t0 + threadIdx.x;
         const int64_t b = u < n ? off[u] : 0;
-        const int64_t dfull = u < n ? off[u + 1] - b : 0;
-        const bool hub = dfull > kAmsfChunk;
-        const uint32_t d = hub ? 0u : (uint32_t)dfull;
-        mlo[lane] = kPosInfBits;
-        mhi[lane] = 0u;
-        uint32_t incl = d;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= (unsigned)o) incl += t;
+        const int64_t d = u < n ? off[u + 1] - b : 0;
+        uint32_t lo = kPosInfBits, hi = 0;
+        if (d <= 32) {
+            for (int64_t x = 0; x < d; ++x) {
+                const float f = w[b + x];
+                if (!good_weight(f)) bad = 1;
+                const uint32_t bits = __float_as_uint(f) & 0x7FFFFFFFu;
+                lo = min(lo, bits);
+                hi = max(hi, bits);
+            }
         }
-        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-        const uint32_t excl = incl - d;
-        __syncwarp();
-        for (uint32_t t0 = 0; t0 < tot; t0 += 32) {
-            const uint32_t t = t0 + lane;
-            int lo = 0;
-#pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                const uint32_t pe = __shfl_sync(0xffffffffu, excl, lo + step);
-                if (pe <= t) lo += step;
-            }
-            const int64_t ob = __shfl_sync(0xffffffffu, b, lo);
-            const uint32_t oex = __shfl_sync(0xffffffffu, excl, lo);
-            const bool valid = t < tot;
-            const float x = valid ? w[ob + (t - oex)] : 1.0f;
-            if (valid && !good_weight(x)) bad = 1;
-            const uint32_t owner = valid ? (uint32_t)lo : 32u;
-            uint32_t vlo = valid ? (__float_as_uint(x) & 0x7FFFFFFFu) : kPosInfBits;
-            uint32_t vhi = valid ? (__float_as_uint(x) & 0x7FFFFFFFu) : 0u;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {                  // segmented inclusive min / max
-                const uint32_t po = __shfl_up_sync(0xffffffffu, owner, o);
-                const uint32_t pl = __shfl_up_sync(0xffffffffu, vlo, o);
-                const uint32_t ph = __shfl_up_sync(0xffffffffu, vhi, o);
-                if (lane >= (unsigned)o && po == owner) {
-                    vlo = min(vlo, pl);
-                    vhi = max(vhi, ph);
-                }
-            }
-            const uint32_t nxt = __shfl_down_sync(0xffffffffu, owner, 1);
-            if (valid && (lane == 31 || nxt != owner)) {       // the segment's last lane
-                mlo[owner] = min(mlo[owner], vlo);
-                mhi[owner] = max(mhi[owner], vhi);
-                gmin = min(gmin, vlo);
-                gmax = max(gmax, vhi);
-            }
-            __syncwarp();
-        }
-        // long lists: the whole warp, one list at a time
-        for (unsigned hm = __ballot_sync(0xffffffffu, hub); hm; hm &= hm - 1) {
-            const int j = __ffs(hm) - 1;
+        for (unsigned lm = __ballot_sync(0xffffffffu, d > 32); lm; lm &= lm - 1) {
+            const int j = __ffs(lm) - 1;
             const int64_t hb = __shfl_sync(0xffffffffu, b, j);
-            const int64_t he = hb + __shfl_sync(0xffffffffu, dfull, j);
+            const int64_t he = hb + __shfl_sync(0xffffffffu, d, j);
             uint32_t vlo = kPosInfBits, vhi = 0;
             for (int64_t x0 = hb + lane; x0 < he; x0 += 32 * 4) {
                 float xs[4];
@@ -167,18 +130,16 @@ __global__ void __launch_bounds__(kBlock) k_amsf_wrange(const int64_t* __restric
             vlo = __reduce_min_sync(0xffffffffu, vlo);
             vhi = __reduce_max_sync(0xffffffffu, vhi);
             if (lane == (unsigned)j) {
-                mlo[j] = vlo;
-                mhi[j] = vhi;
+                lo = vlo;
+                hi = vhi;
             }
-            gmin = min(gmin, vlo);
-            gmax = max(gmax, vhi);
         }
-        __syncwarp();
         if (u < n) {
-            wlo[u] = mlo[lane];
-            whi[u] = mhi[lane];
+            wlo[u] = lo;
+            whi[u] = hi;
         }
-        __syncwarp();
+        gmin = min(gmin, lo);
+        gmax = max(gmax, hi);
     }
     gmin = __reduce_min_sync(0xffffffffu, gmin);
     gmax = __reduce_max_sync(0xffffffffu, gmax);
@@ -402,7 +363,7 @@ __global__ void __launch_bounds__(kBlock, CC_AMSF_ROUND_MINB) k_amsf_round(
     const unsigned long long* __restrict__ start, uint32_t round, double blo, double bhi,
     const uint32_t* __restrict__ carry_in, AmsfCtl* ac, int in_slot, uint32_t* carry_out, bool skip, bool plain,
     uint2* F, float* Fw, uint2* chq, const uint32_t* __restrict__ hid, const uint32_t* __restrict__ hstart,
-    uint32_t nbk, cc_counters* cnt)
+    const unsigned long long* __restrict__ hbase, const uint32_t* __restrict__ hidx, uint32_t nbk, cc_counters* cnt)
 {
     const unsigned lane = threadIdx.x & 31;
     const bool rebuild = ac->rebuild != 0;
@@ -435,20 +396,24 @@ __global__ void __launch_bounds__(kBlock, CC_AMSF_ROUND_MINB) k_amsf_round(
         if (keep) carry_out[pos] = u;
         const int64_t b = work ? off[u] : 0;
         const int64_t dfull = work ? off[u + 1] - b : 0;
-        // a long list is cut into kAmsfChunk-entry pieces for k_amsf_chunks (any warp)
-        const bool big = dfull > kAmsfChunk;
+        // an indexed list (> kIdxMin entries, bucket index built) contributes only this
+        // bucket's entries, read through hidx from `base`; a range (or, without the
+        // index, a list) longer than kAmsfChunk is cut into pieces for any warp
+        const bool indexed = hstart && dfull > kIdxMin;
+        int64_t len = dfull, rbase = b;
+        if (indexed) {
+            const uint32_t h = hid[u];
+            const uint32_t* hs = hstart + (uint64_t)h * (nbk + 1);
+            rbase = (int64_t)hbase[h] + hs[round];
+            len = (int64_t)hs[round + 1] - (int64_t)hs[round];
+        }
+        const bool big = len > kAmsfChunk;
         if (big) {
-            // with the hub index: only this bucket's entries of the hub, else its whole list
-            int64_t len = dfull;
-            if (hstart) {
-                const uint32_t* hs = hstart + (uint64_t)hid[u] * (nbk + 1);
-                len = (int64_t)hs[round + 1] - (int64_t)hs[round];
-            }
             const uint32_t nch = (uint32_t)((len + kAmsfChunk - 1) / kAmsfChunk);
-            const unsigned long long q = nch ? atomicAdd(&ac->chunks, (unsigned long long)nch) : 0ull;
+            const unsigned long long q = atomicAdd(&ac->chunks, (unsigned long long)nch);
             for (uint32_t c = 0; c < nch; ++c) chq[q + c] = make_uint2(u, c);
         }
-        const uint32_t d = big ? 0u : (uint32_t)dfull;
+        const uint32_t d = big ? 0u : (uint32_t)len;
         uint32_t incl = d;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -474,9 +439,11 @@ __global__ void __launch_bounds__(kBlock, CC_AMSF_ROUND_MINB) k_amsf_round(
                     if (pe <= t) lo += step;
                 }
                 ou[j] = __shfl_sync(0xffffffffu, u, lo);
-                const int64_t ob = __shfl_sync(0xffffffffu, b, lo);
+                const int64_t ob = __shfl_sync(0xffffffffu, rbase, lo);
+                const int64_t oo = __shfl_sync(0xffffffffu, b, lo);
+                const bool oi = __shfl_sync(0xffffffffu, indexed, lo);
                 const uint32_t oex = __shfl_sync(0xffffffffu, excl, lo);
-                ex[j] = t < tot ? ob + (t - oex) : -1;
+                ex[j] = t < tot ? (oi ? oo + (int64_t)hidx[ob + (t - oex)] : ob + (t - oex)) : -1;
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j) x[j] = ex[j] >= 0 ? w[ex[j]] : 0.0f;
@@ -548,22 +515,41 @@ __global__ void __launch_bounds__(kBlock) k_amsf_hub_pieces(const int64_t* __res
     }
 }
 
-// Hub bucket index (built once): the vertices with more than kAmsfChunk entries,
+// Bucket index (built once): the vertices with more than kIdxMin entries,
 // hid[v] = their index, and per hub its entries (offsets relative to off[v])
 // grouped by bucket: hidx[hbase[h] + hstart[h][i] ..] are the bucket-i entries.
-__global__ void __launch_bounds__(kBlock) k_amsf_hubs(const int64_t* __restrict__ off, uint32_t n, uint32_t* hubs,
-                                                      uint32_t* hid, unsigned long long* hcount,
-                                                      unsigned long long* hdeg)
+// The lists to index: kIdxMin < d <= kIdxWarpMax go to queue 0 (one warp each),
+// longer ones to queue 1 (one CTA each).  Each list's hidx region is claimed
+// from a cursor (64-bit warp prefix, one atomic per warp): regions are disjoint,
+// their order does not matter.
+__global__ void __launch_bounds__(kBlock) k_amsf_hubs(const int64_t* __restrict__ off, uint32_t n, uint32_t* q0,
+                                                      uint32_t* q1, unsigned long long* qb0, unsigned long long* qb1,
+                                                      unsigned long long* hcount)
 {
+    const unsigned lane = threadIdx.x & 31;
     for (uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x; t0 < n; t0 += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t v = t0 + threadIdx.x;
         const int64_t d = v < n ? off[v + 1] - off[v] : 0;
-        const bool hub = d > kAmsfChunk;
-        const unsigned long long pos = warp_append(hcount, hub ? 1u : 0u);
-        if (hub) {
-            hubs[pos] = (uint32_t)v;
-            hid[v] = (uint32_t)pos;
-            hdeg[pos] = (unsigned long long)d;
+        const bool hub = d > kIdxMin;
+        const bool blk = d > kIdxWarpMax;
+        unsigned long long incl = hub ? (unsigned long long)d : 0ull;      // hidx region
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (unsigned)o) incl += t;
+        }
+        const unsigned long long wsum = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned long long wb = 0;
+        if (lane == 31 && wsum) wb = atomicAdd(hcount + 2, wsum);
+        wb = __shfl_sync(0xffffffffu, wb, 31);
+        const unsigned long long p0 = warp_append(hcount + 0, hub && !blk ? 1u : 0u);
+        const unsigned long long p1 = warp_append(hcount + 1, blk ? 1u : 0u);
+        if (hub && !blk) {
+            q0[p0] = (uint32_t)v;
+            qb0[p0] = wb + incl - (unsigned long long)d;
+        }
+        if (blk) {
+            q1[p1] = (uint32_t)v;
+            qb1[p1] = wb + incl - (unsigned long long)d;
         }
     }
 }
@@ -583,19 +569,24 @@ __device__ __forceinline__ uint32_t bucket_fast(const double* b, uint32_t nb, fl
 }
 
 __global__ void __launch_bounds__(1024) k_amsf_hub_index(const int64_t* __restrict__ off,
-                                                         const float* __restrict__ w, const uint32_t* hubs,
-                                                         const unsigned long long* hcount,
-                                                         const unsigned long long* hbase, const double* bnd,
-                                                         uint32_t nbk, float wmin, float inv_l2g, uint32_t* hstart,
-                                                         uint32_t* hidx)
+                                                         const float* __restrict__ w, const uint32_t* q1,
+                                                         const unsigned long long* qb1,
+                                                         const unsigned long long* hcount, const double* bnd,
+                                                         uint32_t nbk, float wmin, float inv_l2g, uint32_t* hid,
+                                                         unsigned long long* hbase, uint32_t* hstart, uint32_t* hidx)
 {
     __shared__ uint32_t sh[kIdxBins + 1];
     __shared__ double sb[kIdxBins + 1];
     for (uint32_t i = threadIdx.x; i <= nbk; i += blockDim.x) sb[i] = bnd[i];
-    const unsigned long long H = *hcount;
-    for (unsigned long long h = blockIdx.x; h < H; h += gridDim.x) {
-        const uint32_t v = hubs[h];
+    const unsigned long long H0 = hcount[0], H1 = hcount[1];
+    for (unsigned long long p = blockIdx.x; p < H1; p += gridDim.x) {
+        const uint32_t v = q1[p];
+        const unsigned long long h = H0 + p;
         const int64_t b = off[v], d = off[v + 1] - b;
+        if (threadIdx.x == 0) {
+            hid[v] = (uint32_t)h;
+            hbase[h] = qb1[p];
+        }
         for (uint32_t i = threadIdx.x; i <= nbk; i += blockDim.x) sh[i] = 0;
         __syncthreads();
         for (int64_t x = threadIdx.x; x < d; x += blockDim.x)
@@ -621,39 +612,61 @@ __global__ void __launch_bounds__(1024) k_amsf_hub_index(const int64_t* __restri
         __syncthreads();
         for (int64_t x = threadIdx.x; x < d; x += blockDim.x) {
             const uint32_t bi = bucket_fast(sb, nbk, w[b + x], wmin, inv_l2g);
-            hidx[hbase[h] + atomicAdd(sh + bi, 1u)] = (uint32_t)x;
+            hidx[qb1[p] + atomicAdd(sh + bi, 1u)] = (uint32_t)x;
         }
         __syncthreads();
     }
 }
 
-// exclusive scan of the hub degrees (one block, 64-bit)
-__global__ void __launch_bounds__(kBlock) k_amsf_hub_scan(const unsigned long long* hdeg,
-                                                          const unsigned long long* hcount, unsigned long long* hbase)
+// The same index for lists of kIdxMin < d <= kIdxWarpMax entries, one warp per
+// list (a per-warp shared histogram of nbk + 1 <= kIdxWarpBins bins).
+__global__ void __launch_bounds__(kBlock) k_amsf_idx_warp(const int64_t* __restrict__ off,
+                                                          const float* __restrict__ w, const uint32_t* q0,
+                                                          const unsigned long long* qb0,
+                                                          const unsigned long long* hcount, const double* bnd,
+                                                          uint32_t nbk, float wmin, float inv_l2g, uint32_t* hid,
+                                                          unsigned long long* hbase, uint32_t* hstart, uint32_t* hidx)
 {
-    __shared__ unsigned long long ws[kBlock / 32];
-    __shared__ unsigned long long carry;
-    if (threadIdx.x == 0) carry = 0;
+    __shared__ uint32_t sh[kBlock / 32][kIdxWarpBins];
+    __shared__ double sb[kIdxWarpBins];
+    for (uint32_t i = threadIdx.x; i <= nbk; i += blockDim.x) sb[i] = bnd[i];
     __syncthreads();
-    const unsigned lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-    const unsigned long long H = *hcount;
-    for (unsigned long long base = 0; base < H; base += kBlock) {
-        const unsigned long long i = base + threadIdx.x;
-        const unsigned long long x = i < H ? hdeg[i] : 0ull;
-        unsigned long long incl = x;
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= (unsigned)o) incl += t;
+    const unsigned lane = threadIdx.x & 31;
+    uint32_t* hw = sh[threadIdx.x >> 5];
+    const unsigned long long H0 = hcount[0];
+    const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    for (unsigned long long h = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; h < H0; h += nwarps) {
+        const uint32_t v = q0[h];
+        const int64_t b = off[v], d = off[v + 1] - b;
+        if (lane == 0) {
+            hid[v] = (uint32_t)h;
+            hbase[h] = qb0[h];
         }
-        if (lane == 31) ws[wi] = incl;
-        __syncthreads();
-        unsigned long long wb = 0;
-        for (unsigned j = 0; j < wi; ++j) wb += ws[j];
-        const unsigned long long c = carry;
-        if (i < H) hbase[i] = c + wb + incl - x;
-        __syncthreads();
-        if (threadIdx.x == kBlock - 1) carry = c + wb + incl;
-        __syncthreads();
+        for (uint32_t i = lane; i <= nbk; i += 32) hw[i] = 0;
+        __syncwarp();
+        for (int64_t x = lane; x < d; x += 32) atomicAdd(hw + bucket_fast(sb, nbk, w[b + x], wmin, inv_l2g), 1u);
+        __syncwarp();
+        uint32_t carry = 0;                                     // exclusive scan of the bins
+        for (uint32_t b0 = 0; b0 <= nbk; b0 += 32) {
+            const uint32_t i = b0 + lane;
+            const uint32_t c = i <= nbk ? hw[i] : 0u;
+            uint32_t incl = c;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= (unsigned)o) incl += t;
+            }
+            if (i <= nbk) hw[i] = carry + incl - c;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        __syncwarp();
+        uint32_t* hs = hstart + h * (nbk + 1);
+        for (uint32_t i = lane; i <= nbk; i += 32) hs[i] = hw[i];
+        __syncwarp();
+        for (int64_t x = lane; x < d; x += 32) {
+            const uint32_t bi = bucket_fast(sb, nbk, w[b + x], wmin, inv_l2g);
+            hidx[qb0[h] + atomicAdd(hw + bi, 1u)] = (uint32_t)x;
+        }
+        __syncwarp();
     }
 }
 
@@ -749,6 +762,8 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
     const bool skip = !(o.flags & CC_FLAG_NO_SKIP);
     const bool plain = (o.flags & CC_FLAG_AMSF_PLAIN) != 0;
     bool index = false;                       // hub bucket index (set once nb is known)
+    const char* tr = std::getenv("CC_AMSF_TRACE");
+    const bool trace = tr && tr[0] == '1';
     AmsfCtl* ac = nullptr;
     uint32_t *P = nullptr, *wlo = nullptr, *whi = nullptr, *fb = nullptr, *order = nullptr;
     uint32_t* carry[2] = {nullptr, nullptr};
@@ -828,23 +843,41 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
             k_amsf_scatter<<<sms * 8, kBlock, 0, s>>>(whi, fb, n, nb, cursor, order);
             CC_LAUNCH_CHECK("k_amsf_scatter");
             if (index) {
-                // hub bucket index: lists longer than kAmsfChunk grouped by bucket, once
-                const uint64_t hcap = std::max<uint64_t>(1, std::min<uint64_t>(n, (uint64_t)m / (kAmsfChunk + 1) + 1));
-                CC_CUDA_TRY(scratch_alloc((void**)&hubs, sizeof(uint32_t) * hcap, s));
+                // bucket index: lists longer than kIdxMin grouped by bucket, once; the list
+                // counts are read back (one more host sync) to size the per-list bucket starts
+                const uint64_t qcap0 = std::max<uint64_t>(1, std::min<uint64_t>(n, (uint64_t)m / (kIdxMin + 1) + 1));
+                const uint64_t qcap1 = std::max<uint64_t>(1, std::min<uint64_t>(n, (uint64_t)m / (kIdxWarpMax + 1) + 1));
+                CC_CUDA_TRY(scratch_alloc((void**)&hubs, sizeof(uint32_t) * (qcap0 + qcap1), s));
+                CC_CUDA_TRY(scratch_alloc((void**)&hdeg, sizeof(unsigned long long) * (qcap0 + qcap1), s));
+                CC_CUDA_TRY(scratch_alloc((void**)&hcount, 3 * sizeof(unsigned long long), s));
                 CC_CUDA_TRY(scratch_alloc((void**)&hid, sizeof(uint32_t) * n, s));
-                CC_CUDA_TRY(scratch_alloc((void**)&hdeg, sizeof(unsigned long long) * hcap, s));
-                CC_CUDA_TRY(scratch_alloc((void**)&hbase, sizeof(unsigned long long) * hcap, s));
-                CC_CUDA_TRY(scratch_alloc((void**)&hcount, sizeof(unsigned long long), s));
-                CC_CUDA_TRY(scratch_alloc((void**)&hstart, sizeof(uint32_t) * hcap * (nb + 1), s));
-                CC_CUDA_TRY(scratch_alloc((void**)&hidx, sizeof(uint32_t) * (size_t)m, s));
-                CC_CUDA_TRY(cudaMemsetAsync(hcount, 0, sizeof(unsigned long long), s));
-                k_amsf_hubs<<<sms * 8, kBlock, 0, s>>>(off, n, hubs, hid, hcount, hdeg);
+                CC_CUDA_TRY(cudaMemsetAsync(hcount, 0, 3 * sizeof(unsigned long long), s));
+                uint32_t *q0 = hubs, *q1 = hubs + qcap0;
+                unsigned long long *qb0 = hdeg, *qb1 = hdeg + qcap0;
+                k_amsf_hubs<<<sms * 8, kBlock, 0, s>>>(off, n, q0, q1, qb0, qb1, hcount);
                 CC_LAUNCH_CHECK("k_amsf_hubs");
-                k_amsf_hub_scan<<<1, kBlock, 0, s>>>(hdeg, hcount, hbase);
-                CC_LAUNCH_CHECK("k_amsf_hub_scan");
-                k_amsf_hub_index<<<sms * 2, 1024, 0, s>>>(off, w, hubs, hcount, hbase, bd, nb, (float)b[0],
-                                                          (float)(1.0 / std::log2(1.0 + eps)), hstart, hidx);
-                CC_LAUNCH_CHECK("k_amsf_hub_index");
+                unsigned long long hc[3] = {0, 0, 0};
+                CC_CUDA_TRY(cudaMemcpyAsync(hc, hcount, sizeof(hc), cudaMemcpyDeviceToHost, s));
+                CC_CUDA_TRY(cudaStreamSynchronize(s));
+                const uint64_t H = hc[0] + hc[1];
+                CC_CUDA_TRY(scratch_alloc((void**)&hbase, sizeof(unsigned long long) * std::max<uint64_t>(H, 1), s));
+                CC_CUDA_TRY(scratch_alloc((void**)&hstart, sizeof(uint32_t) * std::max<uint64_t>(H, 1) * (nb + 1), s));
+                CC_CUDA_TRY(scratch_alloc((void**)&hidx, sizeof(uint32_t) * std::max<uint64_t>(hc[2], 1), s));
+                const float wmin_f = (float)b[0], il2g = (float)(1.0 / std::log2(1.0 + eps));
+                if (hc[0]) {
+                    if (nb + 1 <= kIdxWarpBins) {
+                        k_amsf_idx_warp<<<sms * 8, kBlock, 0, s>>>(off, w, q0, qb0, hcount, bd, nb, wmin_f, il2g, hid,
+                                                                  hbase, hstart, hidx);
+                        CC_LAUNCH_CHECK("k_amsf_idx_warp");
+                    } else {
+                        index = false;                      // too many buckets for the warp build: no index
+                    }
+                }
+                if (index && hc[1]) {
+                    k_amsf_hub_index<<<sms * 2, 1024, 0, s>>>(off, w, q1, qb1, hcount, bd, nb, wmin_f, il2g, hid, hbase,
+                                                              hstart, hidx);
+                    CC_LAUNCH_CHECK("k_amsf_hub_index");
+                }
             }
         }
         // the rounds: bucket i = [b_i, b_(i+1)), lightest first
@@ -857,7 +890,7 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
             k_amsf_round<MODE><<<sms * 8, kBlock, 0, s>>>(off, adj, w, P, wlo, whi, order, start, i, b[i], b[i + 1],
                                                           carry[in_slot], ac, in_slot, carry[in_slot ^ 1],
                                                           skip, plain, F, Fw, chq, hid, index ? hstart : nullptr,
-                                                          nb, o.counters);
+                                                          hbase, hidx, nb, o.counters);
             CC_LAUNCH_CHECK("k_amsf_round");
             if (index)
                 k_amsf_hub_pieces<MODE><<<sms * 8, kBlock, 0, s>>>(off, adj, w, P, i, chq, ac, hid, hstart, hbase, hidx,
@@ -871,6 +904,16 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
             CC_LAUNCH_CHECK("k_amsf_chunks");
             k_amsf_next<<<1, 1, 0, s>>>(ac, in_slot, o.counters);
             CC_LAUNCH_CHECK("k_amsf_next");
+            if (trace && o.counters) {                       // diagnostics only (CC_AMSF_TRACE=1)
+                cc_counters c{};
+                AmsfCtl hc{};
+                CC_CUDA_TRY(cudaMemcpyAsync(&c, o.counters, sizeof(c), cudaMemcpyDeviceToHost, s));
+                CC_CUDA_TRY(cudaMemcpyAsync(&hc, ac, sizeof(hc), cudaMemcpyDeviceToHost, s));
+                CC_CUDA_TRY(cudaStreamSynchronize(s));
+                std::fprintf(stderr, "amsf round %u visits %llu edges %llu hooks %llu carry %llu anchor %u skip %u\n", i,
+                             (unsigned long long)c.amsf_visits, (unsigned long long)c.amsf_edges,
+                             (unsigned long long)c.amsf_hooks, hc.cnt[in_slot ^ 1], hc.anchor, hc.skip_root);
+            }
         }
         // Filter: the non-empty slots, in slot order, with their weights
         CC_CUDA_TRY(scratch_alloc((void**)&fcnt, sizeof(uint32_t) * nfb, s));
