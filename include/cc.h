@@ -285,7 +285,8 @@ const char* cc_status_str(cc_status s);
 const char* cc_last_error(void);
 
 /* Upper bound of the transient device scratch a call allocates (informational).
- * op: 0 = cc_labels, 1 = cc_spanning_forest, 2 = cc_incr_create. */
+ * op: 0 = cc_labels, 1 = cc_spanning_forest, 2 = cc_incr_create, 3 = cc_amsf
+ * (eps = 0.25-like bucket counts). */
 size_t cc_workspace_bytes(uint32_t n, int64_t m, uint32_t kout_k, int op);
 
 /* Library version string. */

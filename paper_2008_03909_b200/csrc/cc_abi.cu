@@ -175,6 +175,13 @@ size_t cc_workspace_bytes(uint32_t n, int64_t m, uint32_t kout_k, int op)
 {
     const size_t N = n, M = m < 0 ? 0 : (size_t)m;
     if (op == 2) return 4 * N;
+    if (op == 3) {
+        // cc_amsf: P, weight range x2, activation bucket, order, 2 carry lists, index ids (4 B each),
+        // forest slots (8 B) + weights (4 B), long-list pieces, the bucket index (<= 4 B per
+        // entry + per-list starts, bounded for eps = 0.25 by 128 buckets), bucket starts
+        return 64 + 4 * N * 8 + 12 * N + 8 * (M / 2048 + std::min<size_t>(N, M / 2048 + 1) + 1) + 4 * M +
+               4 * 129 * (M / 257 + 1) + 16 * (M / 257 + 1) + 8 * 4096;
+    }
     size_t b = 64 + 4 * N /*worklist*/ + 8 * std::min(N * kout_k, std::max(M, N) * kout_k) + 4 * (M / 4096 + 1);
     if (op == 1) b += 8 * N + 4 * N + 12 * (N / 4096 + 1);
     return b;
