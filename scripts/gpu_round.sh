@@ -9,5 +9,5 @@ timeout 600 python bench.py --config 5 --steps 5 --warmup 3 > gpurun_out/bench_c
 P="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
 timeout 300 $P > gpurun_out/plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $P > gpurun_out/ncu_l.log 2>&1 && \
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_link_refill|k_sample_init|k_finish|k_compress|k_identify|k_probe" -c 8 -o gpurun_out/prof_full $P > gpurun_out/ncu_f.log 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_link_refill|k_sample_init|k_finish|k_compress|k_identify|k_probe" -c 10 -o gpurun_out/prof_full $P > gpurun_out/ncu_f.log 2>&1
 echo done
