@@ -674,7 +674,7 @@ def run_ours_incr(a, rank, ws, cfg):
 
     # ---- cpu_baseline: the oracle (sequential DSU, 1 thread) on the first batches of the
     # same stream (the generator's bytes), answers checked against the GPU's
-    if not a.no_cpu_baseline and rank == 0:
+    if not a.no_cpu_baseline and rank == 0 and ws == 1:
         import numpy as np
 
         import oracle
