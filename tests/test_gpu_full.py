@@ -161,3 +161,34 @@ def test_maximum_n_labels_and_forest():
     assert E.shape[0] == sum(1 for v in verts if comp[v] != v)
     for a, b in E.tolist():
         assert b in adjl[a] and find(a) == find(b)
+
+
+def test_more_than_2_32_adjacency_entries():
+    """m > 2^32 (64-bit adjacency indexing everywhere): 256 disjoint cliques of 4101
+    vertices, 4,304,409,600 entries (17.2 GB); every list exceeds the CTA-per-list
+    threshold, so the finish's long-list path is exercised too.  Labels must be the
+    first vertex of each clique."""
+    B, nb = 4101, 256
+    n = B * nb
+    d = B - 1
+    m = n * d
+    assert m > (1 << 32)
+    off = torch.arange(0, n + 1, dtype=torch.int64, device="cuda") * d
+    adj = torch.empty(m, dtype=torch.int32, device="cuda")
+    j = torch.arange(d, dtype=torch.int64, device="cuda")
+    step = 8192
+    for v0 in range(0, n, step):
+        v = torch.arange(v0, min(n, v0 + step), dtype=torch.int64, device="cuda")
+        b = (v // B) * B
+        r = (v - b).unsqueeze(1)
+        vals = b.unsqueeze(1) + j.unsqueeze(0) + (j.unsqueeze(0) >= r).to(torch.int64)
+        adj[v0 * d:(v0 + v.numel()) * d] = vals.reshape(-1).to(torch.int32)
+        del vals
+    torch.cuda.synchronize()
+    want = (torch.arange(n, device="cuda", dtype=torch.int64) // B) * B
+    for kw in (dict(), dict(k=0)):
+        lab = pkg.connected_components(off, adj, **kw)
+        torch.cuda.synchronize()
+        assert torch.equal(lab.to(torch.int64), want), kw
+    del adj
+    torch.cuda.empty_cache()
