@@ -916,18 +916,16 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
             }
         }
         // Filter: the non-empty slots, in slot order, with their weights
-        CC_CUDA_TRY(scratch_alloc((void**)&fcnt, sizeof(uint32_t) * nfb, s));
+        CC_CUDA_TRY(scratch_alloc((void**)&fcnt, sizeof(uint32_t), s));
         CC_CUDA_TRY(scratch_alloc((void**)&foff, sizeof(unsigned long long) * nfb, s));
-        k_forest_count<<<nfb, kBlock, 0, s>>>(F, n, fcnt);
-        CC_LAUNCH_CHECK("k_forest_count");
-        k_forest_scan<<<1, kBlock, 0, s>>>(fcnt, nfb, foff, num_edges);
-        CC_LAUNCH_CHECK("k_forest_scan");
+        CC_CUDA_TRY(cudaMemsetAsync(fcnt, 0, sizeof(uint32_t), s));
+        CC_CUDA_TRY(cudaMemsetAsync(foff, 0, sizeof(unsigned long long) * nfb, s));
         float* ew = edge_w;
         if (!ew && total) {
             CC_CUDA_TRY(scratch_alloc((void**)&ew, sizeof(float) * n, s));
         }
-        k_forest_write<<<nfb, kBlock, 0, s>>>(F, n, foff, edges, Fw, ew);
-        CC_LAUNCH_CHECK("k_forest_write");
+        k_forest_filter<<<nfb, kBlock, 0, s>>>(F, n, nfb, foff, fcnt, edges, num_edges, Fw, ew);
+        CC_LAUNCH_CHECK("k_forest_filter");
         if (total) {
             CC_CUDA_TRY(cudaMemsetAsync(total, 0, sizeof(double), s));
             k_amsf_total<<<sms * 4, kBlock, 0, s>>>(ew, num_edges, total);

@@ -76,19 +76,8 @@ static __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t*
 // ---------------------------------------------------------------------------
 // K7: Filter -- stable compaction of the non-sentinel forest slots.
 
-static __global__ void __launch_bounds__(kBlock) k_forest_count(const uint2* F, uint32_t n, uint32_t* block_cnt)
-{
-    uint32_t tot;
-    const uint64_t base = (uint64_t)blockIdx.x * kFTile + (uint64_t)threadIdx.x * kFItems;
-    uint32_t c = 0;
-#pragma unroll
-    for (int j = 0; j < kFItems; ++j)
-        if (base + j < n && F[base + j].x != kSentinel) ++c;
-    block_excl_scan(c, &tot);
-    if (threadIdx.x == 0) block_cnt[blockIdx.x] = tot;
-}
-
-// single CTA: exclusive scan of the per-block counts (64-bit running total)
+// single CTA: exclusive scan of per-block counts (64-bit running total); used by
+// the contracted link's rank scan
 static __global__ void __launch_bounds__(kBlock) k_forest_scan(const uint32_t* block_cnt, uint32_t nb,
                                                         unsigned long long* block_off, int64_t* num_edges)
 {
@@ -105,31 +94,6 @@ static __global__ void __launch_bounds__(kBlock) k_forest_scan(const uint32_t* b
     if (threadIdx.x == 0) *num_edges = (int64_t)carry;
 }
 
-// Fw / out_w (optional, AMSF): the weight stored with each slot, compacted alongside
-static __global__ void __launch_bounds__(kBlock) k_forest_write(const uint2* F, uint32_t n,
-                                                                const unsigned long long* block_off,
-                                                                uint32_t* edges, const float* Fw = nullptr,
-                                                                float* out_w = nullptr)
-{
-    uint32_t tot;
-    const uint64_t base = (uint64_t)blockIdx.x * kFTile + (uint64_t)threadIdx.x * kFItems;
-    uint2 f[kFItems];
-    uint32_t c = 0;
-#pragma unroll
-    for (int j = 0; j < kFItems; ++j) {
-        f[j] = (base + j < n) ? F[base + j] : make_uint2(kSentinel, kSentinel);
-        c += f[j].x != kSentinel;
-    }
-    uint32_t ex = block_excl_scan(c, &tot);
-    unsigned long long o = block_off[blockIdx.x] + ex;
-#pragma unroll
-    for (int j = 0; j < kFItems; ++j)
-        if (f[j].x != kSentinel) {
-            reinterpret_cast<uint2*>(edges)[o] = f[j];
-            if (out_w) out_w[o] = Fw[base + j];
-            ++o;
-        }
-}
 
 // ---------------------------------------------------------------------------
 // K1': UF-Rem-CAS + SplitAtomicOne links with lane refill (the static k-out link
@@ -237,6 +201,87 @@ static __global__ void __launch_bounds__(kBlock, CC_REFILL_MINB) k_link_refill(
         warp_count(&cnt->sample_hooks, hooked);
         warp_count(&cnt->link_steps, steps);
         warp_count(&cnt->cas_failures, fails);
+    }
+}
+
+
+// Filter in ONE pass (decoupled look-back): a block takes the next tile of kFTile
+// slots by ticket; each warp owns kFTile/8 consecutive slots and counts them with
+// ballots; the block publishes its count, adds up its predecessors' published
+// counts / prefixes, publishes its inclusive prefix, and each warp writes its
+// slots in order (re-reading them, still in L2) at ballot-ranked positions.  F is
+// read from DRAM once, and a tile needs three block barriers, not one per slot
+// round.  status[] (one word per tile) and *ticket start at zero; the last tile
+// stores the total in *num_edges.
+static __global__ void __launch_bounds__(kBlock) k_forest_filter(const uint2* F, uint32_t n, uint32_t ntiles,
+                                                                 unsigned long long* status, unsigned int* ticket,
+                                                                 uint32_t* edges, int64_t* num_edges,
+                                                                 const float* Fw = nullptr, float* out_w = nullptr)
+{
+    constexpr unsigned long long kAgg = 1ull << 62, kPre = 2ull << 62, kVal = (1ull << 62) - 1;
+    constexpr int NW = kBlock / 32, SEG = kFTile / NW;      // slots per warp
+    __shared__ uint32_t s_tile;
+    __shared__ uint32_t s_wc[NW];
+    __shared__ unsigned long long s_wo[NW];
+    const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint64_t seg = (uint64_t)tile * kFTile + (uint64_t)w * SEG;
+    uint32_t c = 0;
+#pragma unroll 4
+    for (int r = 0; r < SEG / 32; ++r) {
+        const uint64_t i = seg + (uint64_t)r * 32 + lane;
+        c += __popc(__ballot_sync(0xffffffffu, i < n && F[i].x != kSentinel));
+    }
+    if (lane == 0) s_wc[w] = c;
+    __syncthreads();
+    if (w == 0) {                                            // warp 0: publish + look back 32 tiles at a time
+        unsigned long long agg = 0;
+        for (int k = 0; k < NW; ++k) agg += s_wc[k];
+        if (lane == 0) atomicExch(status + tile, (tile == 0 ? kPre : kAgg) | agg);
+        unsigned long long excl = 0;
+        int64_t p = (int64_t)tile - 1;
+        while (p >= 0) {
+            const int64_t q = p - lane;
+            unsigned long long st = q >= 0 ? atomicAdd(status + q, 0ull) : kPre;   // before tile 0: prefix 0
+            const unsigned pre = __ballot_sync(0xffffffffu, (st & kPre) != 0);
+            const unsigned none = __ballot_sync(0xffffffffu, (st & ~kVal) == 0);
+            // lanes up to the first published prefix (lane order = descending tile)
+            const int lim = pre ? __ffs(pre) - 1 : 31;
+            const unsigned upto = lim == 31 ? 0xffffffffu : ((2u << lim) - 1u);
+            if (none & upto) continue;                       // a tile in the window has not published: re-read
+            unsigned long long v = (lane <= (unsigned)lim && q >= 0) ? (st & kVal) : 0ull;
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);   // 64-bit sum
+            excl += v;
+            if (pre) break;
+            p -= 32;
+        }
+        if (lane == 0) {
+            if (tile) atomicExch(status + tile, kPre | (excl + agg));
+            unsigned long long acc = excl;
+            for (int k = 0; k < NW; ++k) {
+                s_wo[k] = acc;
+                acc += s_wc[k];
+            }
+            if (tile == ntiles - 1) *num_edges = (int64_t)(excl + agg);
+        }
+    }
+    __syncthreads();
+    unsigned long long o = s_wo[w];
+#pragma unroll 4
+    for (int r = 0; r < SEG / 32; ++r) {
+        const uint64_t i = seg + (uint64_t)r * 32 + lane;
+        const uint2 f = i < n ? F[i] : make_uint2(kSentinel, kSentinel);
+        const bool keep = f.x != kSentinel;
+        const unsigned mk = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+            const unsigned long long pos = o + __popc(mk & lt);
+            reinterpret_cast<uint2*>(edges)[pos] = f;
+            if (out_w) out_w[pos] = Fw[i];
+        }
+        o += __popc(mk);
     }
 }
 

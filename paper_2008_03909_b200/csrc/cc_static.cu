@@ -156,11 +156,11 @@ __global__ void __launch_bounds__(kBlock, 3) k_sample_init(
         const uint64_t u = wbase + 32 * j + lane;
         if (u < n) {
             uint32_t p = (uint32_t)u;
-            if (v0[j] < (uint32_t)u) {
-                p = v0[j];                              // Union(u, v0): hook singleton root u
-                if (SF) F[u] = make_uint2((uint32_t)u, v0[j]);   // forest edge at the hooked root
-            }
+            if (v0[j] < (uint32_t)u) p = v0[j];        // Union(u, v0): hook singleton root u
             P[u] = p;
+            // forest slots: the round-0 edge at the hooked root, else empty --
+            // every slot is written here, so F needs no separate initialisation
+            if (SF) F[u] = p != (uint32_t)u ? make_uint2((uint32_t)u, p) : make_uint2(kSentinel, kSentinel);
         }
     }
     // exclusive positions in vertex order: warp scans per j, then block, then one atomic
@@ -1334,7 +1334,7 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
             CC_CUDA_TRY(scratch_alloc((void**)&F, sizeof(uint2) * (size_t)n, s));
             CC_CUDA_TRY(scratch_alloc((void**)&fcnt, sizeof(uint32_t) * nfb, s));
             CC_CUDA_TRY(scratch_alloc((void**)&foff, sizeof(unsigned long long) * nfb, s));
-            CC_CUDA_TRY(cudaMemsetAsync(F, 0xFF, sizeof(uint2) * (size_t)n, s));
+            // (F is initialised by k_sample_init, which writes every slot)
         }
         if (contract) {
             // R <= number of non-isolated vertices <= min(n, m); sized for the worst case
@@ -1469,12 +1469,11 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
         CC_CUDA_TRY(mark(CC_MARK_COMPRESS));
         // H7
         if (SF) {
-            k_forest_count<<<nfb, kBlock, 0, s>>>(F, n, fcnt);
-            CC_LAUNCH_CHECK("k_forest_count");
-            k_forest_scan<<<1, kBlock, 0, s>>>(fcnt, nfb, foff, num_edges);
-            CC_LAUNCH_CHECK("k_forest_scan");
-            k_forest_write<<<nfb, kBlock, 0, s>>>(F, n, foff, edges);
-            CC_LAUNCH_CHECK("k_forest_write");
+            // one-pass Filter: status words (foff) and the ticket (fcnt[0]) start at zero
+            CC_CUDA_TRY(cudaMemsetAsync(foff, 0, sizeof(unsigned long long) * nfb, s));
+            CC_CUDA_TRY(cudaMemsetAsync(fcnt, 0, sizeof(uint32_t), s));
+            k_forest_filter<<<nfb, kBlock, 0, s>>>(F, n, nfb, foff, fcnt, edges, num_edges);
+            CC_LAUNCH_CHECK("k_forest_filter");
         }
         CC_CUDA_TRY(mark(CC_MARK_FOREST));
         if (o.timings) {
