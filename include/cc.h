@@ -213,7 +213,7 @@ cc_status cc_spanning_forest(const int64_t* offsets, const uint32_t* adj, uint32
 
 /* Approximate minimum spanning forest, AMSF-NF-S (Sec. 5.1):
  * W(F_OPT) <= W(F) <= (1+eps) W(F_OPT).  The folklore algorithm:
- * W_min = min w(e); bucket i holds the edges with b_i <= w < b_(i+1), b_0 =
+ * W_min = min w(e) over every adjacency entry, self-loops included; bucket i holds the edges with b_i <= w < b_(i+1), b_0 =
  * W_min, b_(i+1) = b_i * (1+eps) in fp64 (reading R25); buckets are
  * processed from light to heavy, each one's edges unioned with UF-Rem-CAS +
  * SplitAtomicOne on one persistent parent array, recording the

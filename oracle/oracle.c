@@ -59,6 +59,7 @@
  * uint32; vertex ids are uint32 < n.  Return 0 on success, a negative value on
  * malformed input or allocation failure.
  */
+#include <float.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -304,12 +305,15 @@ int oracle_amsf(uint32_t n, const int64_t* off, const uint32_t* adj, const float
     int64_t ne = collect_edges(n, off, adj, w, &E);
     if (ne < 0) return -1;
     if (ne == 0) { free(E); return 0; }
-    /* W_min and the boundaries b_i = W_min (1+eps)^i (reading R25) */
-    float wmin = E[0].w, wmax = E[0].w;
-    for (int64_t i = 0; i < ne; ++i) {
-        if (!(E[i].w > 0.0f)) { free(E); return -2; }
-        if (E[i].w < wmin) wmin = E[i].w;
-        if (E[i].w > wmax) wmax = E[i].w;
+    /* W_min and the boundaries b_i = W_min (1+eps)^i (reading R25).  W_min / W_max
+     * range over every adjacency entry as given, self-loops included (a self-loop never
+     * joins the forest, but it is an element of the input edge set; reading R25) */
+    const int64_t m_all = off[n];
+    float wmin = w[0], wmax = w[0];
+    for (int64_t i = 0; i < m_all; ++i) {
+        if (!(w[i] > 0.0f) || !(w[i] <= FLT_MAX)) { free(E); return -2; }
+        if (w[i] < wmin) wmin = w[i];
+        if (w[i] > wmax) wmax = w[i];
     }
     const double g = 1.0 + eps;
     int64_t nb = 1;

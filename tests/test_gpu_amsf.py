@@ -232,3 +232,27 @@ def test_amsf_host_buffers():
     cc.cc_amsf(p_off, p_adj, p_w, n, m, 0.25, d_e, None, d_num, None)
     torch.cuda.synchronize()
     assert int(d_num.item()) == k
+
+
+def test_amsf_self_loops_extreme_weights():
+    """Self-loops carrying the smallest and the largest weight: they set W_min / W_max and
+    so the bucket boundaries on both sides (reading R25) but never join the forest."""
+    rng = np.random.default_rng(21)
+    off, adj = gen.er(seed=11, n0=20000, pairs=30000, isolated=5)
+    n = off.size - 1
+    loops = rng.choice(n, 300, replace=False)
+    pairs = np.concatenate([np.stack([np.repeat(np.arange(n), np.diff(off)), adj.astype(np.int64)], 1),
+                            np.stack([loops, loops], 1)])
+    off, adj = oracle.csr_from_pairs(n, pairs)
+    w = gen.exp_weights(off, adj, 5)
+    src = np.repeat(np.arange(n), np.diff(off))
+    is_loop = np.nonzero(src == adj)[0]
+    assert is_loop.size >= 300
+    w[is_loop[0]] = np.float32(w.min() / 1000)
+    w[is_loop[1]] = np.float32(w.max() * 1000)
+    for eps in (0.05, 0.25):
+        want = oracle.amsf(off, adj, w, eps)
+        for opt in OPTS:
+            E, W, tot = run(off, adj, w, eps, **opt)
+            assert not np.any(E[:, 0] == E[:, 1])
+            check(off, adj, w, eps, E, W, tot, want=want)

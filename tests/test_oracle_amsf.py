@@ -156,6 +156,13 @@ def test_amsf_closed_forms():
     off, adj, w = weighted(3, [(0, 1, 1.0), (1, 2, 2.0), (0, 2, 3.9)])
     r, wopt = check_amsf(off, adj, w, 1.0)
     assert wopt == 3.0 and r["total"] == pytest.approx(4.9, abs=1e-6) and r["buckets"].tolist() == [0, 1]
+    # self-loops are entries of the input: a loop of weight 0.001 sets W_min (reading R25),
+    # eps = 1 gives b_i = 0.001 * 2^i, so w = 1.0 is in bucket 9 ([0.512, 1.024)), w = 1.5
+    # in bucket 10 and nb = 11 (b_11 = 2.048 > W_max); a loop never joins the forest
+    off, adj = csr(3, [(0, 1), (1, 2), (2, 2)], keep_loops=True)
+    w = np.array([1.0, 1.0, 1.5, 1.5, 0.001], dtype=np.float32)        # CSR: 0:[1] 1:[0,2] 2:[1,2]
+    r = oracle.amsf(off, adj, w, 1.0)
+    assert r["nbuckets"] == 11 and r["buckets"].tolist() == [9, 10] and r["total"] == 2.5
     off, adj = csr(4, [])
     r = oracle.amsf(off, adj, np.zeros(0, np.float32), 0.25)
     assert r["total"] == 0.0 and r["pairs"].shape == (0, 2)
