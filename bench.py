@@ -257,6 +257,13 @@ def byte_model(off_h_deg_pos, n, m, k, ctr, sampled, final, mid_ran, f0=None):
         B["k_compress_mid"] = 3 * (n // 8) + 8 * R + 4 * n + 4 * f0_nonroots + 4 * f0_deep
         B["k_link_pending"] = 16 * pend + 8 * R
         B["k_finish"] = 4 * n + n // 8 + 12 * ctr["finish_gathers"] + 4 * ctr["compress_writes"] + 4 * fin_v
+    if ctr.get("fused_link"):
+        # k_sample_link (DESIGN.md §6 item 1b): P initialised first (4n write), offsets + first-k
+        # adj entries, the round-0 CAS on P[u] (4n read), finish bitmap, and the links queued in
+        # shared memory: P[u], P[v] gathers + hook CAS -- no pending list through HBM
+        B["k_sample_init"] = 8 * (n + 1) + 4 * sum_mink + 4 * n + 4 * n + n // 8 + 8 * pend + 4 * ctr["sample_hooks"]
+        B["k_compress_mid"] = 1024 * 8 * 12
+        B["k_link_pending"] = 0
     B["finish_phase"] = B["k_finish"] + B["k_finish_proc"] + B["k_compress_H6"]
     B["sampling_phase"] = B["k_sample_init"] + B["k_compress_mid"] + B["k_link_pending"]
     return B, {"relabelled": relab, "sampled_nonroots": nonroot, "mid_nonroots_bound": npos}
@@ -402,6 +409,8 @@ def run_ours(a, rank, ws):
             gbs = B[kname] / (t * 1e-3) / 1e9
             kernels[kname] = {"ms": round(t, 5), "bytes": int(B[kname]), "GB/s": round(gbs, 1),
                               "frac": round(gbs / peak, 4), "share": round(t / mean_ms, 4)}
+    if ctr.get("fused_link") and "k_sample_init" in kernels:
+        kernels["k_sample_link"] = kernels.pop("k_sample_init")      # sampling + k-out links, one kernel
     dom = max(kernels, key=lambda k: kernels[k]["ms"])
     dk = kernels[dom]
     roofline = {"bound": "hbm", "kernel": dom, "achieved": dk["GB/s"], "peak": peak, "unit": "GB/s",
@@ -461,7 +470,7 @@ def run_ours(a, rank, ws):
     # CAS) against the uniform random-gather rate measured just above on an
     # array of the same size.
     rg = line["floors"]["random_gather"]["Gloads_per_s"]
-    lk = kernels.get("k_link_pending")
+    lk = kernels.get("k_sample_link" if ctr.get("fused_link") else "k_link_pending")
     if lk and contract:
         # contracted: the HBM random accesses are the P[v] gathers (one per pending
         # link); the Rem walk and CAS run in the L2-resident compact array
@@ -480,7 +489,8 @@ def run_ours(a, rank, ws):
         acc = ctr["pending_links"] + ctr["link_steps"] + (ctr["cas_failures"] if refill else ctr["sample_hooks"])
         ach = acc / (lk["ms"] * 1e-3) / 1e9
         line["roofline"]["random_access_view"] = {
-            "kernel": "k_link_pending", "random_accesses_per_launch": int(acc),
+            "kernel": "k_sample_link" if ctr.get("fused_link") else "k_link_pending",
+            "random_accesses_per_launch": int(acc),
             "achieved_Gaccess_per_s": round(ach, 2), "uniform_random_gather_Gloads_per_s": rg,
             "frac_of_random_gather_rate": round(ach / rg, 3)}
 

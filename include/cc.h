@@ -97,6 +97,10 @@ typedef int cc_status;
                                           on C3/C4                               */
 #define CC_FLAG_NO_REFILL   (1u << 11) /* k-out links: one warp step per slowest lane (the
                                           round-1 kernel) instead of lane refill           */
+#define CC_FLAG_FUSED_LINK  (1u << 16) /* run k-out sampling and its CAS links in one kernel
+                                          (links queued in shared memory, P initialised first);
+                                          UF-Rem-CAS + SplitAtomicOne with k <= 2 only, else
+                                          ignored.  Measured, not the default     */
 #define CC_FLAG_FINISH_CRFA (1u << 13) /* finish with the Liu-Tarjan CRFA rounds (Connect,
                                           RootUp, FullShortcut, Alter)
                                           instead of UF-Rem-CAS; one host sync per round.
@@ -151,6 +155,7 @@ typedef struct {
     uint64_t amsf_edges;       /* cc_amsf: adjacency weights inspected over all rounds */
     uint64_t amsf_hooks;       /* cc_amsf: successful root hooks (= forest edges)      */
     uint64_t amsf_rebuilds;    /* cc_amsf: rounds whose L_max left the skipped component*/
+    uint64_t fused_link;       /* 1 if the k-out links ran inside k_sample_link         */
 } cc_counters;
 
 typedef struct {

@@ -36,6 +36,7 @@ FLAG_NO_REFILL = 1 << 11
 FLAG_AMSF_PLAIN = 1 << 12
 FLAG_FINISH_CRFA = 1 << 13
 FLAG_AMSF_NO_INDEX = 1 << 14
+FLAG_FUSED_LINK = 1 << 16
 FLAG_FIND_NAIVE = 1 << 15
 
 # every symbol include/cc.h and include/cc_bench.h declare
@@ -61,7 +62,7 @@ COUNTER_FIELDS = ["pending_links", "worklist", "finish_vertices", "finish_edges"
                   "big_vertices", "compress_writes",
                   "link_steps", "cas_failures", "probe_deep", "finish_gathers", "h6_writes", "h6_gathers",
                   "sv_rounds", "contract_roots", "amsf_rounds", "amsf_visits", "amsf_edges", "amsf_hooks",
-                  "amsf_rebuilds"]
+                  "amsf_rebuilds", "fused_link"]
 
 
 class Opts(ctypes.Structure):

@@ -214,6 +214,233 @@ __global__ void __launch_bounds__(kBlock, 3) k_sample_init(
 }
 
 // ---------------------------------------------------------------------------
+// K0' + K1' fused (CC_FLAG_FUSED_LINK; UF-Rem-CAS + SplitAtomicOne, k <= 2).
+//
+// k_sample_init streams the CSR heads (HBM-bandwidth work) and k_link_refill
+// then makes the random parent accesses of the links (DRAM row-activation
+// bound): run back to back, neither overlaps the other.  Here one kernel does
+// both per block: it samples its 2048 vertices, queues their links in SHARED
+// memory (no pending list through HBM) and links them with the lane-refill
+// loop, while the other resident blocks are in their streaming part.
+// k_init_pf initialises P (and F) first, so any P[v] a link reads is valid; the
+// round-0 hook Union(u, v0), v0 < u, is then a CAS from u to v0 (another
+// block's link may already have hooked the root u: the CAS fails and (u, v0)
+// is queued as an ordinary link).  Every sampled edge is unioned exactly as in
+// Alg. 4; only the order of the unions differs, which does not
+// change the partition (P:4259-4280 is linearizable).
+// Measured (profiles/r1_fused_link_ab.txt): no overlap gain.  With P in HBM (C4)
+// both halves are DRAM-bound and their DRAM times add (3.10-3.18 ms vs 2.89 ms
+// split); with P in L2 (C3) it ties the split kernels; C1 gains 7 % (launches);
+// a row-major grid (C2) loses the mid compress (45M vs 17M Rem steps).  Kept as
+// an option, tested in the option grid.
+__global__ void __launch_bounds__(kBlock) k_init_pf(uint32_t* __restrict__ P, uint32_t n, uint2* __restrict__ F)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; 4 * i < n; i += stride) {
+        const uint32_t b = (uint32_t)(4 * i);
+        if (b + 4 <= n && ((uintptr_t)P & 15u) == 0) {
+            reinterpret_cast<uint4*>(P)[i] = make_uint4(b, b + 1, b + 2, b + 3);
+        } else {
+            for (uint32_t t = b; t < n && t < b + 4; ++t) P[t] = t;
+        }
+        if (F)
+            for (uint32_t t = b; t < n && t < b + 4; ++t) F[t] = make_uint2(kSentinel, kSentinel);
+    }
+}
+
+#ifndef CC_SL_MINB
+#define CC_SL_MINB 3
+#endif
+template <int VAR, bool SF>
+__global__ void __launch_bounds__(kBlock, CC_SL_MINB) k_sample_link(
+    const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, uint32_t n, int64_t m, uint32_t k,
+    uint64_t seed, uint32_t full_deg, uint32_t* __restrict__ P, uint2* __restrict__ F,
+    uint32_t* __restrict__ bm, cc_counters* cnt)
+{
+    constexpr int NW = kBlock / 32;
+    __shared__ uint2 s_q[2 * kBlockTile];                    // the block's links (k <= 2)
+    __shared__ uint32_t s_wtot[NW], s_wbase[NW], s_total;
+    const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint64_t wbase = (uint64_t)blockIdx.x * kBlockTile + (uint64_t)w * kWarpTile;
+
+    int64_t o[kV];
+    uint32_t d[kV];
+#pragma unroll
+    for (int j = 0; j < kV; ++j) {
+        const uint64_t u = wbase + 32 * j + lane;
+        o[j] = ld_stream_i64(off + (u < n ? u : n));
+    }
+    const int64_t last = ld_stream_i64(off + (wbase + kWarpTile < n ? wbase + kWarpTile : n));
+#pragma unroll
+    for (int j = 0; j < kV; ++j) {
+        const int64_t nx = __shfl_down_sync(0xffffffffu, o[j], 1);
+        const int64_t first_next = __shfl_sync(0xffffffffu, j + 1 < kV ? o[(j + 1) % kV] : last, 0);
+        const int64_t e = lane == 31 ? (j + 1 < kV ? first_next : last) : nx;
+        const uint64_t u = wbase + 32 * j + lane;
+        d[j] = u < n ? (uint32_t)min(e - o[j], (int64_t)0xFFFFFFFF) : 0u;
+    }
+    uint32_t v0[kV], v1[kV];
+#pragma unroll
+    for (int j = 0; j < kV; ++j) {
+        const uint64_t u = wbase + 32 * j + lane;
+        uint32_t i0 = 0, i1 = 1;
+        if (VAR == 2 && d[j] > 0) i0 = uniform_below(mix(seed, KOUT_STREAM, u * 64 + 0), d[j]);
+        if (VAR >= 1 && d[j] > 0) i1 = uniform_below(mix(seed, KOUT_STREAM, u * 64 + 1), d[j]);
+        const bool need0 = d[j] > 0 && k > 0;
+        const bool need1 = k > 1 && (VAR >= 1 ? d[j] > 0 : d[j] > 1);
+        v0[j] = need0 ? __ldg(adj + o[j] + i0) : kSentinel;
+        v1[j] = need1 ? __ldg(adj + o[j] + i1) : kSentinel;
+    }
+    // round 0: hook the (normally still singleton) root u under v0 < u; queue the rest
+    uint32_t bits = 0, nwl = 0, q0 = 0, c[kV];
+#pragma unroll
+    for (int j = 0; j < kV; ++j) {
+        const uint64_t u = wbase + 32 * j + lane;
+        bool p0 = false;
+        if (v0[j] != kSentinel) {
+            if (v0[j] < (uint32_t)u) {
+                if (cas(P + u, (uint32_t)u, v0[j]) == (uint32_t)u) {
+                    if (SF) F[u] = make_uint2((uint32_t)u, v0[j]);
+                } else {
+                    p0 = true;
+                }
+            } else {
+                p0 = v0[j] != (uint32_t)u;
+            }
+        }
+        q0 |= (uint32_t)p0 << j;
+        c[j] = (uint32_t)p0 + (v1[j] != kSentinel ? 1u : 0u);
+        const bool mark = u < n && d[j] > full_deg;
+        nwl += mark;
+        const uint32_t word = __ballot_sync(0xffffffffu, mark);
+        if (lane == (unsigned)j) bits = word;
+    }
+    if (lane < (unsigned)kV && wbase + 32 * lane < n) bm[(wbase >> 5) + lane] = bits;
+    // queue positions: warp scans per j, then block
+    uint32_t ex[kV];
+    uint32_t run = 0;
+#pragma unroll
+    for (int j = 0; j < kV; ++j) {
+        uint32_t incl = c[j];
+#pragma unroll
+        for (int o2 = 1; o2 < 32; o2 <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o2);
+            if (lane >= (unsigned)o2) incl += t;
+        }
+        ex[j] = run + incl - c[j];
+        run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) s_wtot[w] = run;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t acc = 0;
+        for (int i = 0; i < NW; ++i) {
+            s_wbase[i] = acc;
+            acc += s_wtot[i];
+        }
+        s_total = acc;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kV; ++j) {
+        const uint32_t u = (uint32_t)(wbase + 32 * j + lane);
+        uint32_t pos = s_wbase[w] + ex[j];
+        if ((q0 >> j) & 1u) s_q[pos++] = make_uint2(u, v0[j]);
+        if (v1[j] != kSentinel) s_q[pos] = make_uint2(u, v1[j]);
+    }
+    __syncthreads();
+    const uint32_t total = s_total;
+    if (cnt) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) cnt->fused_link = 1;
+        uint32_t np = 0;
+#pragma unroll
+        for (int j = 0; j < kV; ++j) np += c[j];
+        warp_count(&cnt->pending_links, np);
+        warp_count(&cnt->worklist, nwl);
+    }
+
+    // lane-refill link loop over the block's queue (k_link_refill's step, R1/R6);
+    // warp w takes the 32-entry chunks w, w + NW, ...
+    const unsigned lt_mask = (1u << lane) - 1u;
+    uint32_t chunk = w;
+    uint2 nb = make_uint2(0u, 0u);
+    uint32_t npu = 0, npv = 0, navail = 0;
+    auto fetch = [&]() {
+        const uint32_t b0 = chunk * 32;
+        navail = b0 < total ? min(32u, total - b0) : 0u;
+        const bool ok = lane < navail;
+        nb = ok ? s_q[b0 + lane] : make_uint2(0u, 0u);
+        npu = ok ? ld_relaxed(P + nb.x) : 0u;
+        npv = ok ? ld_relaxed(P + nb.y) : 0u;
+        chunk += NW;
+    };
+    fetch();
+    uint2 cb = nb;
+    uint32_t cpu = npu, cpv = npv, cavail = navail, cpos = 0;
+    if (cavail) fetch();
+    bool act = false;
+    uint32_t u = 0, v = 0, ru = 0, rv = 0, pu = 0, pv = 0;
+    uint32_t hooked = 0, steps = 0, fails = 0;
+    while (true) {
+        unsigned need = __ballot_sync(0xffffffffu, !act);
+        while (need && cavail) {
+            const uint32_t src = cpos + __popc(need & lt_mask);
+            const uint32_t sl = src & 31;
+            const uint32_t xu = __shfl_sync(0xffffffffu, cb.x, sl), xv = __shfl_sync(0xffffffffu, cb.y, sl);
+            const uint32_t xpu = __shfl_sync(0xffffffffu, cpu, sl), xpv = __shfl_sync(0xffffffffu, cpv, sl);
+            if (!act && src < cavail && xpu != xpv) {
+                act = true;
+                u = ru = xu;
+                v = rv = xv;
+                pu = xpu;
+                pv = xpv;
+            }
+            cpos = min(cavail, cpos + (uint32_t)__popc(need));
+            if (cpos == cavail) {
+                cb = nb;
+                cpu = npu;
+                cpv = npv;
+                cavail = navail;
+                cpos = 0;
+                if (cavail) fetch();
+            }
+            need = __ballot_sync(0xffffffffu, !act);
+        }
+        if (!__any_sync(0xffffffffu, act)) break;
+        if (act) {
+            ++steps;
+            if (pu < pv) {
+                uint32_t t = ru; ru = rv; rv = t;
+                t = pu; pu = pv; pv = t;
+            }
+            if (ru == pu) {
+                const uint32_t old = cas(P + ru, ru, pv);
+                if (old == ru) {
+                    if (SF) F[ru] = make_uint2(u, v);
+                    ++hooked;
+                    act = false;
+                } else {
+                    ++fails;
+                    pu = old;
+                    pv = ld_relaxed(P + rv);
+                }
+            } else {
+                const uint32_t wg = ld_relaxed(P + pu);
+                if (wg != pu) cas(P + ru, pu, wg);
+                ru = pu;
+                pu = wg;
+            }
+            if (act && pu == pv) act = false;
+        }
+    }
+    if (cnt) {
+        warp_count(&cnt->sample_hooks, hooked);
+        warp_count(&cnt->link_steps, steps);
+        warp_count(&cnt->cas_failures, fails);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Kc: pointer-jumping compress.  Within this kernel no hook happens, so every
 // value read is an ancestor-or-self on the path to the (fixed) root, stale or
 // not; plain (L1-cacheable) loads are therefore safe and let the hot giant
@@ -1280,6 +1507,8 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
     const bool no_skip = (o.flags & CC_FLAG_NO_SKIP) != 0;
     // contracted k-out link (opt-in; needs the symmetric-graph precondition of the skip)
     const bool contract = k > 0 && !no_skip && (o.flags & CC_FLAG_CONTRACT);
+    // sampling and link in one kernel (UF-Rem-CAS + SplitAtomicOne, k <= 2, in-place)
+    const bool fused = MODE == 0 && k > 0 && k <= 2 && !contract && (o.flags & CC_FLAG_FUSED_LINK);
     const int sms = num_sms();
     const uint32_t nw = (uint32_t)(((uint64_t)n + 31) / 32);
     const uint32_t nrb = (uint32_t)(((uint64_t)nw + kFTile - 1) / kFTile);
@@ -1328,7 +1557,7 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
         CC_CUDA_TRY(scratch_alloc((void**)&ctl, sizeof(Ctl), s));
         CC_CUDA_TRY(scratch_alloc((void**)&bm, sizeof(uint32_t) * bm_words, s));
         CC_CUDA_TRY(scratch_alloc((void**)&cq, sizeof(uint32_t) * (size_t)n, s));
-        if (k > 0) CC_CUDA_TRY(scratch_alloc((void**)&pend, sizeof(uint2) * pend_cap, s));
+        if (k > 0 && !fused) CC_CUDA_TRY(scratch_alloc((void**)&pend, sizeof(uint2) * pend_cap, s));
         CC_CUDA_TRY(scratch_alloc((void**)&big, sizeof(uint32_t) * big_cap, s));
         if (SF) {
             CC_CUDA_TRY(scratch_alloc((void**)&F, sizeof(uint2) * (size_t)n, s));
@@ -1359,7 +1588,13 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
         // 16-byte list-head windows pay off when adj is read over PCIe (pinned host,
         // zero-copy); from HBM two 4-byte loads of the same sector are cheaper
         const bool win = aligned16(adj) && mem_kind(adj, nullptr) == MEM_PINNED;
-        if (contract && win)
+        if (fused) {
+            k_init_pf<<<sms * 16, kBlock, 0, s>>>(P, n, SF ? F : nullptr);
+            CC_LAUNCH_CHECK("k_init_pf");
+            k_sample_link<VAR, SF><<<nblk0, kBlock, 0, s>>>(off, adj, n, m, k, o.seed, full_deg, P, F, bm,
+                                                            o.counters);
+            CC_LAUNCH_CHECK("k_sample_link");
+        } else if (contract && win)
             k_sample_init<VAR, SF, true, true><<<nblk0, kBlock, 0, s>>>(off, adj, n, m, k, o.seed, full_deg, P, F,
                                                                           pend, bm, rbw, ctl, o.counters);
         else if (contract)
@@ -1371,7 +1606,7 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
         else
             k_sample_init<VAR, SF, false, false><<<nblk0, kBlock, 0, s>>>(off, adj, n, m, k, o.seed, full_deg, P, F,
                                                                             pend, bm, nullptr, ctl, o.counters);
-        CC_LAUNCH_CHECK("k_sample_init");
+        if (!fused) CC_LAUNCH_CHECK("k_sample_init");
         CC_CUDA_TRY(mark(CC_MARK_INIT));
         if (contract) {
             // rank words -> compact ids (rid, C[c] = c), then P[u] = root_F0(u)
@@ -1385,7 +1620,7 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
                 CC_CUDA_TRY(cudaMemcpyAsync(&o.counters->contract_roots, Rtot, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
             cc_status r = launch_compress(P, n, nullptr, nullptr, s, "k_compress(F0)");
             if (r) return r;
-        } else if (k > 0 && !(o.flags & CC_FLAG_NO_MIDCOMPRESS)) {
+        } else if (k > 0 && !fused && !(o.flags & CC_FLAG_NO_MIDCOMPRESS)) {
             // shorten the first-round chains before the CAS links when they are long
             // (grid-like inputs); k_probe decides on the device unless a flag forces it
             const bool force = (o.flags & CC_FLAG_MIDCOMPRESS) != 0;
@@ -1398,7 +1633,8 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
         }
         CC_CUDA_TRY(mark(CC_MARK_MIDCOMPRESS));
         // H2: the remaining sampled edges
-        if (contract) {
+        if (fused) {
+        } else if (contract) {
             k_link_contract<MODE, SF><<<sms * 8, kBlock, 0, s>>>(P, pend, ctl, rbw, Cc, rid, F, o.counters);
             CC_LAUNCH_CHECK("k_link_contract");
             k_contract_final<<<sms * 8, kBlock, 0, s>>>(Cc, rid, Rtot);

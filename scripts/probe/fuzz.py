@@ -17,7 +17,7 @@ from paper_2008_03909_b200 import cc  # noqa: E402
 secs = float(sys.argv[1]) if len(sys.argv) > 1 else 60
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
 FLAGS = [0, cc.FLAG_HALVE, cc.FLAG_UF_ASYNC, cc.FLAG_NO_SKIP, cc.FLAG_NO_MIDCOMPRESS, cc.FLAG_MIDCOMPRESS,
-         cc.FLAG_NO_DEGSKIP, cc.FLAG_FINISH_SV, cc.FLAG_FINISH_CRFA, cc.FLAG_CONTRACT, cc.FLAG_NO_REFILL]
+         cc.FLAG_NO_DEGSKIP, cc.FLAG_FINISH_SV, cc.FLAG_FINISH_CRFA, cc.FLAG_CONTRACT, cc.FLAG_NO_REFILL, cc.FLAG_FUSED_LINK]
 
 
 def random_graph():

@@ -72,3 +72,13 @@ def test_product_has_no_cpu_fallback(monkeypatch, tmp_path):
     monkeypatch.setattr(cc, "LIB_PATH", str(tmp_path / "missing.so"))
     with pytest.raises(cc.CCError):
         cc.load()
+
+
+def test_binding_structs_mirror_header():
+    """cc.py's ctypes mirrors of cc_counters / cc_opts / CC_FLAG_* follow include/cc.h."""
+    src = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", "cc.h")).read(), flags=re.S)
+    body = re.search(r"typedef struct\s*\{([^}]*)\}\s*cc_counters;", src).group(1)
+    fields = re.findall(r"uint64_t\s+(\w+);", body)
+    assert fields == list(cc.COUNTER_FIELDS)
+    for name, val in re.findall(r"#define\s+CC_FLAG_(\w+)\s+\(1u\s*<<\s*(\d+)\)", src):
+        assert getattr(cc, "FLAG_" + name) == 1 << int(val), name

@@ -47,6 +47,11 @@ OPTION_GRID = [
     dict(k=2, variant="pure", flags=cc.FLAG_CONTRACT | cc.FLAG_UF_ASYNC, seed=9),
     dict(k=2, variant="afforest", flags=cc.FLAG_NO_REFILL),
     dict(k=3, variant="hybrid", flags=cc.FLAG_NO_REFILL, seed=3),
+    # sampling and k-out links in one kernel
+    dict(k=2, variant="afforest", flags=cc.FLAG_FUSED_LINK),
+    dict(k=1, variant="afforest", flags=cc.FLAG_FUSED_LINK),
+    dict(k=2, variant="hybrid", flags=cc.FLAG_FUSED_LINK, seed=4),
+    dict(k=2, variant="pure", flags=cc.FLAG_FUSED_LINK | cc.FLAG_NO_DEGSKIP, seed=8),
     # Liu-Tarjan CRFA finish (NEXT-3)
     dict(k=2, variant="afforest", flags=cc.FLAG_FINISH_CRFA),
     dict(k=0, variant="afforest", flags=cc.FLAG_FINISH_CRFA),
@@ -105,7 +110,8 @@ def test_sampled_labels_are_cc_of_the_sampled_edges():
         n = off.size - 1
         for (k, variant, seed), fl in itertools.product(
                 [(1, "afforest", 0), (2, "afforest", 0), (3, "afforest", 0), (2, "hybrid", 5),
-                 (4, "hybrid", 99), (1, "pure", 4), (3, "pure", 8)], [0, cc.FLAG_CONTRACT, cc.FLAG_NO_REFILL]):
+                 (4, "hybrid", 99), (1, "pure", 4), (3, "pure", 8)],
+                [0, cc.FLAG_CONTRACT, cc.FLAG_NO_REFILL, cc.FLAG_FUSED_LINK]):
             d_off, d_adj = to_dev(off, adj)
             sampled = torch.empty(n, dtype=torch.int32, device="cuda")
             lmax = torch.empty(1, dtype=torch.int32, device="cuda")
@@ -209,6 +215,8 @@ def test_empty_and_degenerate_abi():
                                  dict(k=2, variant="afforest", flags=cc.FLAG_CONTRACT),
                                  dict(k=3, variant="pure", flags=cc.FLAG_CONTRACT | cc.FLAG_HALVE, seed=4),
                                  dict(k=2, variant="afforest", flags=cc.FLAG_NO_REFILL),
+                                 dict(k=2, variant="afforest", flags=cc.FLAG_FUSED_LINK),
+                                 dict(k=2, variant="hybrid", flags=cc.FLAG_FUSED_LINK, seed=3),
                                  dict(k=2, variant="afforest", flags=cc.FLAG_FINISH_CRFA),
                                  dict(k=0, variant="afforest", flags=cc.FLAG_FINISH_CRFA),
                                  dict(k=1, variant="hybrid", flags=0, seed=6)],
@@ -248,7 +256,7 @@ def test_repeat_stress_random_options():
     d_off, d_adj = to_dev(off, adj)
     flags_pool = [0, cc.FLAG_HALVE, cc.FLAG_UF_ASYNC, cc.FLAG_NO_SKIP, cc.FLAG_NO_MIDCOMPRESS, cc.FLAG_NO_DEGSKIP,
                   cc.FLAG_MIDCOMPRESS, cc.FLAG_FINISH_SV, cc.FLAG_CONTRACT, cc.FLAG_NO_REFILL,
-                  cc.FLAG_FINISH_CRFA]
+                  cc.FLAG_FINISH_CRFA, cc.FLAG_FUSED_LINK]
     for it in range(200):
         k = int(rng.integers(0, 5))
         variant = ["afforest", "hybrid", "pure"][int(rng.integers(0, 3))]
