@@ -319,3 +319,72 @@ def test_identify_frequent_and_canon():
     assert np.array_equal(oracle.canon(np.arange(9)), np.arange(9))
     # splitmix64 published test vector (seed 0 -> first output), pins the shared generator form
     assert int(oracle.splitmix64(np.array([0], dtype=np.uint64))[0]) == 0xE220A8397B1DCDAF
+
+
+def test_kout_sample_edges_pins():
+    """Pins of the k-out sample beyond its own definition (R7): afforest with k >= max degree
+    samples every edge (its CC is scipy's); hybrid/pure picks are uniform over the list
+    positions and independent across j (chi-square, "uniformly at random")."""
+    from scipy import stats
+    from scipy.sparse import csr_matrix
+    from scipy.sparse.csgraph import connected_components
+    off, adj = gen.er(seed=13, n0=3000, pairs=4000, isolated=7)
+    n = off.size - 1
+    deg = np.diff(off)
+    E = oracle.kout_sample_edges(off, adj, int(deg.max()), "afforest")
+    src = np.repeat(np.arange(n), deg)
+    assert set(zip(E[:, 0].tolist(), E[:, 1].tolist())) == set(zip(src.tolist(), adj.tolist()))
+    g = csr_matrix((np.ones(E.shape[0]), (E[:, 0], E[:, 1])), shape=(n, n))
+    nc, lab = connected_components(g, directed=False)
+    assert nc == int(np.sum(oracle.cc_bfs(off, adj) == np.arange(n)))
+    # circulant graph: every list is the same 12 offsets, so the position of a pick is its rank
+    n, d = 20000, 12
+    ring = [(u, (u + s) % n) for u in range(n) for s in range(1, d // 2 + 1)]
+    off, adj = oracle.csr_from_pairs(n, np.array(ring))
+    assert np.all(np.diff(off) == d)
+    for var, k in (("hybrid", 3), ("pure", 2)):
+        E = oracle.kout_sample_edges(off, adj, k, var, seed=7)
+        assert E.shape[0] == k * n
+        u = E[:, 0].astype(np.int64)
+        pos = np.array([np.searchsorted(adj[off[a]:off[a + 1]], b) for a, b in zip(u, E[:, 1])])
+        # picks are in u's list (searchsorted found them) and grouped by j in blocks of n
+        assert np.all(adj[off[u] + pos] == E[:, 1])
+        first = 1 if var == "hybrid" else 0
+        if var == "hybrid":
+            assert np.all(pos[:n] == 0)
+        picks = pos[first * n:].reshape(k - first, n)
+        for j in range(picks.shape[0]):
+            assert stats.chisquare(np.bincount(picks[j], minlength=d)).pvalue > 1e-4
+        if picks.shape[0] >= 2:
+            pairs = picks[0] * d + picks[1]
+            assert stats.chisquare(np.bincount(pairs, minlength=d * d)).pvalue > 1e-4
+
+
+def test_uniform_below_and_identify_frequent_pins():
+    """uniform_below is the multiply-shift map: value x has preimage [ceil(x 2^32 / b),
+    ceil((x+1) 2^32 / b)) of the low 32 bits (sizes differ by <= 1); IdentifyFrequent is the
+    mode of the sampled labels with ties to the smaller label (R9), i.e. scipy.stats.mode."""
+    from scipy import stats
+    for b in (1, 2, 3, 7, 1000, 4096, 134217728, 0xFFFFFFFF):
+        for x in {x for x in (0, 1, b // 2, b - 1) if x < b}:
+            lo = -(-(x * (1 << 32)) // b)                         # ceil(x 2^32 / b)
+            assert int(oracle.uniform_below(np.array([lo], dtype=np.uint64), b)[0]) == x
+            if lo > 0:
+                assert int(oracle.uniform_below(np.array([lo - 1], dtype=np.uint64), b)[0]) == x - 1
+        hi = np.array([(1 << 64) - 1], dtype=np.uint64)           # high bits are ignored
+        assert int(oracle.uniform_below(hi, b)[0]) == b - 1
+    # sample positions: in range, uniform (chi-square), distinct seeds give distinct draws
+    pos = oracle.sample_positions(1000, 200000, 3)
+    assert pos.min() >= 0 and pos.max() < 1000
+    assert stats.chisquare(np.bincount(pos, minlength=1000)).pvalue > 1e-4
+    assert not np.array_equal(oracle.sample_positions(1000, 1024, 3), oracle.sample_positions(1000, 1024, 4))
+    rng = np.random.default_rng(5)
+    for t in range(200):
+        n = int(rng.integers(1, 300))
+        lab = rng.integers(0, int(rng.integers(1, 6)), n).astype(np.uint32)   # few labels: many ties
+        s = int(rng.integers(1, 64))
+        vals = lab[oracle.sample_positions(n, s, t)]
+        assert oracle.identify_frequent(lab, s, t) == int(stats.mode(vals, keepdims=False).mode)
+    # a 60 % giant is the mode of 1024 samples for every seed (a 40 % rival would need > 512 hits)
+    lab = np.where(np.arange(100000) % 5 < 3, 3, 8).astype(np.uint32)
+    assert all(oracle.identify_frequent(lab, 1024, s) == 3 for s in range(50))
