@@ -84,62 +84,151 @@ struct ForestW {
 
 __device__ __forceinline__ bool good_weight(float x) { return x > 0.0f && x < __int_as_float((int)kPosInfBits); }
 
-// Per-vertex lightest / heaviest edge weight and the global range.  A thread per
-// vertex walks a list of up to 32 entries (consecutive vertices' lists are
-// adjacent, so the warp's loads stay within a few lines); longer lists are then
-// reduced by the whole warp, coalesced, one at a time.  No atomics except the
-// global range.
+// Per-vertex lightest / heaviest edge weight and the global range, streamed in
+// ENTRY tiles: block t reads the kWrTile weights [t*kWrTile, (t+1)*kWrTile)
+// coalesced (16 per thread, float4 loads), whatever the list lengths.  tile_vs[t]
+// (written by k_amsf_init) is the vertex owning the tile's first entry; a thread
+// finds the owner of its first entry by a binary search of the offsets within the
+// tile's vertex range (staged in shared memory), then walks the list boundaries
+// forward.  Per
+// vertex min / max are combined in shared memory; a vertex wholly inside the tile
+// is stored plainly, one that straddles a tile boundary is combined by global
+// atomics into wlo / whi (initialised to +inf / 0 by k_amsf_init).  (The thread-
+// per-vertex version walked each short list serially: 12.7 ms on C4, latency-bound.)
+#ifndef CC_AMSF_WR_STAGE
+#define CC_AMSF_WR_STAGE 0
+#endif
+#ifndef CC_AMSF_WR_ITEMS
+#define CC_AMSF_WR_ITEMS 16
+#endif
+constexpr int kWrItems = CC_AMSF_WR_ITEMS;
+constexpr int64_t kWrTile = (int64_t)kBlock * kWrItems;
+constexpr uint32_t kWrCap = 2048;          // vertices per tile combined in shared memory
 __global__ void __launch_bounds__(kBlock) k_amsf_wrange(const int64_t* __restrict__ off, const float* __restrict__ w,
-                                                        uint32_t n, int64_t m, uint32_t* wlo, uint32_t* whi,
-                                                        AmsfCtl* ac)
+                                                        uint32_t n, int64_t m, const uint32_t* __restrict__ tile_vs,
+                                                        uint32_t* wlo, uint32_t* whi, AmsfCtl* ac)
 {
+    __shared__ uint32_t s_lo[kWrCap], s_hi[kWrCap];
+#if CC_AMSF_WR_STAGE
+    __shared__ int64_t s_off[kWrCap + 1];
+#endif
     const unsigned lane = threadIdx.x & 31;
+    const uint64_t ntiles = (uint64_t)((m + kWrTile - 1) / kWrTile);
+    const bool vec = ((uintptr_t)w & 15u) == 0;
     uint32_t gmin = kPosInfBits, gmax = 0, bad = 0;
-    for (uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x; t0 < n; t0 += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t u = t0 + threadIdx.x;
-        const int64_t b = u < n ? off[u] : 0;
-        const int64_t d = u < n ? off[u + 1] - b : 0;
-        uint32_t lo = kPosInfBits, hi = 0;
-        if (d <= 32) {
-            for (int64_t x = 0; x < d; ++x) {
-                const float f = w[b + x];
-                if (!good_weight(f)) bad = 1;
-                const uint32_t bits = __float_as_uint(f) & 0x7FFFFFFFu;
-                lo = min(lo, bits);
-                hi = max(hi, bits);
-            }
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t E0 = (int64_t)t * kWrTile, E1 = min(E0 + kWrTile, m);
+        const uint32_t vs = tile_vs[t];
+        const uint32_t ve = t + 1 < ntiles ? tile_vs[t + 1] : n - 1;     // owner of entry E1 (or the last)
+        const uint32_t nv = min(ve - vs + 1, kWrCap);
+        const uint32_t no = min(ve - vs + 2, kWrCap + 1);          // offsets staged: off[vs .. vs + no)
+        for (uint32_t j = threadIdx.x; j < nv; j += blockDim.x) {
+            s_lo[j] = kPosInfBits;
+            s_hi[j] = 0;
         }
-        for (unsigned lm = __ballot_sync(0xffffffffu, d > 32); lm; lm &= lm - 1) {
-            const int j = __ffs(lm) - 1;
-            const int64_t hb = __shfl_sync(0xffffffffu, b, j);
-            const int64_t he = hb + __shfl_sync(0xffffffffu, d, j);
+#if CC_AMSF_WR_STAGE
+        for (uint32_t j = threadIdx.x; j < no; j += blockDim.x) s_off[j] = off[vs + j];
+        __syncthreads();
+        auto offat = [&](uint32_t v) -> int64_t { return v - vs < no ? s_off[v - vs] : off[v]; };
+#else
+        __syncthreads();
+        auto offat = [&](uint32_t v) -> int64_t { return off[v]; };
+        (void)no;
+#endif
+        const int64_t e0 = E0 + (int64_t)threadIdx.x * kWrItems;
+        if (e0 < E1) {
+            // owner of e0: the largest v in [vs, ve] with off[v] <= e0
+            uint32_t lo = vs, hi = ve;
+            while (lo < hi) {
+                const uint32_t mid = lo + (hi - lo + 1) / 2;
+                if (offat(mid) <= e0) lo = mid; else hi = mid - 1;
+            }
+            uint32_t owner = lo;
+            int64_t nxt = offat(owner + 1);
+            float x[kWrItems];
+            if (vec && e0 + kWrItems <= E1) {
+#pragma unroll
+                for (int q = 0; q < kWrItems / 4; ++q) {
+                    const float4 f = __ldg(reinterpret_cast<const float4*>(w + e0) + q);
+                    x[4 * q] = f.x; x[4 * q + 1] = f.y; x[4 * q + 2] = f.z; x[4 * q + 3] = f.w;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < kWrItems; ++q) x[q] = e0 + q < E1 ? __ldg(w + e0 + q) : 1.0f;
+            }
             uint32_t vlo = kPosInfBits, vhi = 0;
-            for (int64_t x0 = hb + lane; x0 < he; x0 += 32 * 4) {
-                float xs[4];
+            bool any = false;
+            auto flush = [&]() {
+                if (!any) return;
+                const uint32_t j = owner - vs;
+                if (j < kWrCap) {
+                    atomicMin(s_lo + j, vlo);
+                    atomicMax(s_hi + j, vhi);
+                } else {
+                    atomicMin(wlo + owner, vlo);
+                    atomicMax(whi + owner, vhi);
+                }
+                gmin = min(gmin, vlo);
+                gmax = max(gmax, vhi);
+            };
+            if (e0 + kWrItems <= E1 && nxt >= e0 + kWrItems) {
+                // fast path (inside one list, the common case for the long lists that hold
+                // most entries): no boundary tests; a weight is good iff 0 < bits < +inf bits
 #pragma unroll
-                for (int q = 0; q < 4; ++q) xs[q] = x0 + 32 * q < he ? w[x0 + 32 * q] : 1.0f;
+                for (int q = 0; q < kWrItems; ++q) {
+                    const uint32_t bits = __float_as_uint(x[q]);
+                    bad |= (bits - 1u) >= (kPosInfBits - 1u) ? 1u : 0u;
+                    vlo = min(vlo, bits & 0x7FFFFFFFu);
+                    vhi = max(vhi, bits & 0x7FFFFFFFu);
+                }
+                any = true;
+            } else
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    if (x0 + 32 * q >= he) continue;
-                    if (!good_weight(xs[q])) bad = 1;
-                    const uint32_t bits = __float_as_uint(xs[q]) & 0x7FFFFFFFu;
+            for (int q = 0; q < kWrItems; ++q) {
+                const int64_t e = e0 + q;
+                if (e < E1) {
+                    while (e >= nxt) {                   // next list (zero-length lists skipped)
+                        flush();
+                        ++owner;
+                        nxt = offat(owner + 1);
+                        vlo = kPosInfBits;
+                        vhi = 0;
+                        any = false;
+                    }
+                    if (!good_weight(x[q])) bad = 1;
+                    const uint32_t bits = __float_as_uint(x[q]) & 0x7FFFFFFFu;
                     vlo = min(vlo, bits);
                     vhi = max(vhi, bits);
+                    any = true;
                 }
             }
-            vlo = __reduce_min_sync(0xffffffffu, vlo);
-            vhi = __reduce_max_sync(0xffffffffu, vhi);
-            if (lane == (unsigned)j) {
-                lo = vlo;
-                hi = vhi;
+            // the last segment: inside a long list every lane of the warp has the same
+            // owner -- reduce it in the warp first (one shared atomic, not 32)
+            const unsigned am = __activemask();
+            const uint32_t o0 = __shfl_sync(am, owner, __ffs(am) - 1);
+            if (__all_sync(am, any && owner == o0)) {
+                vlo = __reduce_min_sync(am, vlo);
+                vhi = __reduce_max_sync(am, vhi);
+                if (lane == (unsigned)(__ffs(am) - 1)) flush();
+                gmin = min(gmin, vlo);
+                gmax = max(gmax, vhi);
+            } else {
+                flush();
             }
         }
-        if (u < n) {
-            wlo[u] = lo;
-            whi[u] = hi;
+        __syncthreads();
+        for (uint32_t j = threadIdx.x; j < nv; j += blockDim.x) {
+            if (s_lo[j] == kPosInfBits && s_hi[j] == 0) continue;          // no entry in this tile
+            const uint32_t v = vs + j;
+            if (offat(v) >= E0 && offat(v + 1) <= E1) {
+                wlo[v] = s_lo[j];
+                whi[v] = s_hi[j];
+            } else {
+                atomicMin(wlo + v, s_lo[j]);
+                atomicMax(whi + v, s_hi[j]);
+            }
         }
-        gmin = min(gmin, lo);
-        gmax = max(gmax, hi);
+        __syncthreads();
     }
     gmin = __reduce_min_sync(0xffffffffu, gmin);
     gmax = __reduce_max_sync(0xffffffffu, gmax);
@@ -151,13 +240,20 @@ __global__ void __launch_bounds__(kBlock) k_amsf_wrange(const int64_t* __restric
     }
 }
 
-__global__ void k_amsf_init(uint32_t* P, uint32_t* wlo, uint32_t* whi, uint2* F, uint32_t n)
+// P, the weight ranges and the forest slots; and tile_vs[t] = the vertex whose list
+// holds entry t * kWrTile (the first entry of wrange tile t).
+__global__ void k_amsf_init(const int64_t* __restrict__ off, uint32_t* P, uint32_t* wlo, uint32_t* whi, uint2* F,
+                            uint32_t n, uint32_t* tile_vs)
 {
     for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
         P[v] = (uint32_t)v;
         wlo[v] = kPosInfBits;
         whi[v] = 0u;
         F[v] = make_uint2(kSentinel, kSentinel);
+        if (tile_vs) {
+            const int64_t b = off[v], e = off[v + 1];
+            for (int64_t t = (b + kWrTile - 1) / kWrTile; t * kWrTile < e; ++t) tile_vs[t] = (uint32_t)v;
+        }
     }
 }
 
@@ -375,7 +471,7 @@ __global__ void __launch_bounds__(kBlock, CC_AMSF_ROUND_MINB) k_amsf_round(
     const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
     const unsigned cpw = (unsigned)max(1ull, min(32ull, (total + nwarps - 1) / nwarps));
-    uint32_t visits = 0, hooks = 0;
+    uint32_t visits = 0, hooks = 0, links = 0;
     unsigned long long scanned = 0;
     for (unsigned long long base = warp * cpw; base < total; base += nwarps * cpw) {
         const unsigned long long i = base + lane;
@@ -440,8 +536,8 @@ __global__ void __launch_bounds__(kBlock, CC_AMSF_ROUND_MINB) k_amsf_round(
                 }
                 ou[j] = __shfl_sync(0xffffffffu, u, lo);
                 const int64_t ob = __shfl_sync(0xffffffffu, rbase, lo);
-                const int64_t oo = __shfl_sync(0xffffffffu, b, lo);
                 const bool oi = __shfl_sync(0xffffffffu, indexed, lo);
+                const int64_t oo = __shfl_sync(0xffffffffu, b, lo);
                 const uint32_t oex = __shfl_sync(0xffffffffu, excl, lo);
                 ex[j] = t < tot ? (oi ? oo + (int64_t)hidx[ob + (t - oex)] : ob + (t - oex)) : -1;
             }
@@ -450,7 +546,10 @@ __global__ void __launch_bounds__(kBlock, CC_AMSF_ROUND_MINB) k_amsf_round(
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const double xd = (double)x[j];
-                if (ex[j] >= 0 && xd >= blo && xd < bhi) hooks += link<MODE>(P, ou[j], adj[ex[j]], ForestW{F, Fw, x[j]});
+                if (ex[j] >= 0 && xd >= blo && xd < bhi) {
+                    ++links;
+                    hooks += link<MODE>(P, ou[j], adj[ex[j]], ForestW{F, Fw, x[j]});
+                }
             }
             __syncwarp();
         }
@@ -458,6 +557,7 @@ __global__ void __launch_bounds__(kBlock, CC_AMSF_ROUND_MINB) k_amsf_round(
     if (cnt) {
         warp_count(&cnt->amsf_visits, visits);
         warp_count(&cnt->amsf_hooks, hooks);
+        warp_count(&cnt->amsf_links, links);
         const unsigned long long sc = __reduce_add_sync(0xffffffffu, (uint32_t)min(scanned, 0xFFFFFFFFull));
         if (lane == 0 && sc) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt->amsf_edges), sc);
     }
@@ -482,7 +582,7 @@ __global__ void __launch_bounds__(kBlock) k_amsf_hub_pieces(const int64_t* __res
     const unsigned long long total = ac->chunks;
     const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
-    uint32_t hooks = 0;
+    uint32_t hooks = 0, links = 0;
     unsigned long long scanned = 0;
     for (unsigned long long q = warp; q < total; q += nwarps) {
         const uint2 item = chq[q];
@@ -505,11 +605,15 @@ __global__ void __launch_bounds__(kBlock) k_amsf_hub_pieces(const int64_t* __res
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-                if (e[j] >= 0) hooks += link<MODE>(P, item.x, vx[j], ForestW{F, Fw, wx[j]});
+                if (e[j] >= 0) {
+                    ++links;
+                    hooks += link<MODE>(P, item.x, vx[j], ForestW{F, Fw, wx[j]});
+                }
         }
     }
     if (cnt) {
         warp_count(&cnt->amsf_hooks, hooks);
+        warp_count(&cnt->amsf_links, links);
         const unsigned long long sc = __reduce_add_sync(0xffffffffu, (uint32_t)min(scanned, 0xFFFFFFFFull));
         if (lane == 0 && sc) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt->amsf_edges), sc);
     }
@@ -518,38 +622,94 @@ __global__ void __launch_bounds__(kBlock) k_amsf_hub_pieces(const int64_t* __res
 // Bucket index (built once): the vertices with more than kIdxMin entries,
 // hid[v] = their index, and per hub its entries (offsets relative to off[v])
 // grouped by bucket: hidx[hbase[h] + hstart[h][i] ..] are the bucket-i entries.
+// (Storing (neighbour, weight) pairs instead, so that a round reads its edges
+// contiguously, was measured: the rounds stay bound by the links' P gathers
+// (32.0 vs 29.9 ms on C4) and the build moves 8 B more per entry.)
 // The lists to index: kIdxMin < d <= kIdxWarpMax go to queue 0 (one warp each),
 // longer ones to queue 1 (one CTA each).  Each list's hidx region is claimed
-// from a cursor (64-bit warp prefix, one atomic per warp): regions are disjoint,
-// their order does not matter.
+// from a cursor (64-bit block prefix, one atomic per block): regions are
+// disjoint, their order does not matter.
+// Block-wide exclusive scan of three per-thread counts at once (two 32-bit queue
+// counts, one 64-bit region size), with ONE global atomic per counter and block:
+// per-warp atomics on three hot addresses made k_amsf_hubs atomic-bound (2.9 ms
+// on C4 for a 1 GB offsets read).
+struct Append3 {
+    unsigned long long p0, p1, r;
+};
+__device__ __forceinline__ Append3 block_append3(uint32_t c0, uint32_t c1, unsigned long long r,
+                                                 unsigned long long* hcount)
+{
+    constexpr int NW = kBlock / 32;
+    __shared__ unsigned long long s_w[3][NW];
+    __shared__ unsigned long long s_base[3];
+    const unsigned lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    unsigned long long i0 = c0, i1 = c1, ir = r;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long a = __shfl_up_sync(0xffffffffu, i0, o);
+        const unsigned long long b = __shfl_up_sync(0xffffffffu, i1, o);
+        const unsigned long long c = __shfl_up_sync(0xffffffffu, ir, o);
+        if (lane >= (unsigned)o) {
+            i0 += a;
+            i1 += b;
+            ir += c;
+        }
+    }
+    if (lane == 31) {
+        s_w[0][wi] = i0;
+        s_w[1][wi] = i1;
+        s_w[2][wi] = ir;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        unsigned long long acc = 0;
+        for (int k = 0; k < NW; ++k) {
+            const unsigned long long x = s_w[threadIdx.x][k];
+            s_w[threadIdx.x][k] = acc;
+            acc += x;
+        }
+        s_base[threadIdx.x] = acc ? atomicAdd(hcount + threadIdx.x, acc) : 0ull;
+    }
+    __syncthreads();
+    Append3 a;
+    a.p0 = s_base[0] + s_w[0][wi] + i0 - c0;
+    a.p1 = s_base[1] + s_w[1][wi] + i1 - c1;
+    a.r = s_base[2] + s_w[2][wi] + ir - r;
+    __syncthreads();
+    return a;
+}
+
+constexpr int kHubV = 8;                  // vertices per thread in k_amsf_hubs
 __global__ void __launch_bounds__(kBlock) k_amsf_hubs(const int64_t* __restrict__ off, uint32_t n, uint32_t* q0,
                                                       uint32_t* q1, unsigned long long* qb0, unsigned long long* qb1,
                                                       unsigned long long* hcount)
 {
-    const unsigned lane = threadIdx.x & 31;
-    for (uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x; t0 < n; t0 += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t v = t0 + threadIdx.x;
-        const int64_t d = v < n ? off[v + 1] - off[v] : 0;
-        const bool hub = d > kIdxMin;
-        const bool blk = d > kIdxWarpMax;
-        unsigned long long incl = hub ? (unsigned long long)d : 0ull;      // hidx region
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= (unsigned)o) incl += t;
+    constexpr uint64_t T = (uint64_t)kBlock * kHubV;
+    for (uint64_t t0 = (uint64_t)blockIdx.x * T; t0 < n; t0 += (uint64_t)gridDim.x * T) {
+        int64_t d[kHubV];
+        uint32_t c0 = 0, c1 = 0;
+        unsigned long long r = 0;
+#pragma unroll
+        for (int j = 0; j < kHubV; ++j) {
+            const uint64_t v = t0 + (uint64_t)j * kBlock + threadIdx.x;
+            d[j] = v < n ? off[v + 1] - off[v] : 0;
+            c0 += d[j] > kIdxMin && d[j] <= kIdxWarpMax;
+            c1 += d[j] > kIdxWarpMax;
+            r += d[j] > kIdxMin ? (unsigned long long)d[j] : 0ull;
         }
-        const unsigned long long wsum = __shfl_sync(0xffffffffu, incl, 31);
-        unsigned long long wb = 0;
-        if (lane == 31 && wsum) wb = atomicAdd(hcount + 2, wsum);
-        wb = __shfl_sync(0xffffffffu, wb, 31);
-        const unsigned long long p0 = warp_append(hcount + 0, hub && !blk ? 1u : 0u);
-        const unsigned long long p1 = warp_append(hcount + 1, blk ? 1u : 0u);
-        if (hub && !blk) {
-            q0[p0] = (uint32_t)v;
-            qb0[p0] = wb + incl - (unsigned long long)d;
-        }
-        if (blk) {
-            q1[p1] = (uint32_t)v;
-            qb1[p1] = wb + incl - (unsigned long long)d;
+        Append3 a = block_append3(c0, c1, r, hcount);
+#pragma unroll
+        for (int j = 0; j < kHubV; ++j) {
+            const uint64_t v = t0 + (uint64_t)j * kBlock + threadIdx.x;
+            if (d[j] <= kIdxMin) continue;
+            if (d[j] <= kIdxWarpMax) {
+                q0[a.p0] = (uint32_t)v;
+                qb0[a.p0++] = a.r;
+            } else {
+                q1[a.p1] = (uint32_t)v;
+                qb1[a.p1++] = a.r;
+            }
+            a.r += (unsigned long long)d[j];
         }
     }
 }
@@ -558,25 +718,59 @@ __global__ void __launch_bounds__(kBlock) k_amsf_hubs(const int64_t* __restrict_
 // entries placed by a shared cursor (order within a bucket is arbitrary).  The
 // bucket of a weight is estimated from log2(x / W_min) / log2(1 + eps) and then
 // settled by the exact fp64 comparisons b_i <= x < b_(i+1) (reading R25).
-__device__ __forceinline__ uint32_t bucket_fast(const double* b, uint32_t nb, float x, float wmin, float inv_l2g)
+__device__ __forceinline__ uint32_t bucket_fast(const float* fb, uint32_t nb, float x, float wmin, float inv_l2g)
 {
+    // fb[i] = the smallest float >= b_i, so for a float weight x the exact rule
+    // b_i <= (double)x (reading R25) is the float compare fb[i] <= x
     int i = (int)(__log2f(x / wmin) * inv_l2g);
     i = max(0, min((int)nb - 1, i));
-    const double d = (double)x;
-    while (i + 1 < (int)nb && b[i + 1] <= d) ++i;
-    while (i > 0 && b[i] > d) --i;
+    while (i + 1 < (int)nb && fb[i + 1] <= x) ++i;
+    while (i > 0 && fb[i] > x) --i;
     return (uint32_t)i;
 }
+
+// Warp-aggregated shared-memory bin updates: lanes with the same bin (Exp(1)
+// weights crowd a dozen buckets) are combined by __match_any_sync, so one lane
+// per distinct bin issues the atomic.  key = kSentinel for an idle lane.
+#ifndef CC_AMSF_AGG
+#define CC_AMSF_AGG 0
+#endif
+__device__ __forceinline__ void agg_count(uint32_t* hist, uint32_t key)
+{
+    if (!CC_AMSF_AGG) {
+        if (key != kSentinel) atomicAdd(hist + key, 1u);
+        return;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    if (key != kSentinel && (threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(hist + key, __popc(peers));
+}
+// ... and the slot of this lane's entry: the leader reserves popc(peers) slots,
+// each peer takes its rank among them.
+__device__ __forceinline__ uint32_t agg_slot(uint32_t* hist, uint32_t key)
+{
+    if (!CC_AMSF_AGG) return key != kSentinel ? atomicAdd(hist + key, 1u) : 0u;
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (key != kSentinel && lane == (unsigned)leader) base = atomicAdd(hist + key, __popc(peers));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    return base + __popc(peers & ((1u << lane) - 1u));
+}
+#ifndef CC_AMSF_IDX_ILP
+#define CC_AMSF_IDX_ILP 8
+#endif
+constexpr int kIdxILP = CC_AMSF_IDX_ILP;    // weights in flight per lane in the index builds
 
 __global__ void __launch_bounds__(1024) k_amsf_hub_index(const int64_t* __restrict__ off,
                                                          const float* __restrict__ w, const uint32_t* q1,
                                                          const unsigned long long* qb1,
-                                                         const unsigned long long* hcount, const double* bnd,
+                                                         const unsigned long long* hcount, const float* bnd,
                                                          uint32_t nbk, float wmin, float inv_l2g, uint32_t* hid,
                                                          unsigned long long* hbase, uint32_t* hstart, uint32_t* hidx)
 {
     __shared__ uint32_t sh[kIdxBins + 1];
-    __shared__ double sb[kIdxBins + 1];
+    __shared__ float sb[kIdxBins + 1];
     for (uint32_t i = threadIdx.x; i <= nbk; i += blockDim.x) sb[i] = bnd[i];
     const unsigned long long H0 = hcount[0], H1 = hcount[1];
     for (unsigned long long p = blockIdx.x; p < H1; p += gridDim.x) {
@@ -589,8 +783,19 @@ __global__ void __launch_bounds__(1024) k_amsf_hub_index(const int64_t* __restri
         }
         for (uint32_t i = threadIdx.x; i <= nbk; i += blockDim.x) sh[i] = 0;
         __syncthreads();
-        for (int64_t x = threadIdx.x; x < d; x += blockDim.x)
-            atomicAdd(sh + bucket_fast(sb, nbk, w[b + x], wmin, inv_l2g), 1u);
+        for (int64_t x0 = threadIdx.x; x0 - threadIdx.x < d; x0 += (int64_t)blockDim.x * kIdxILP) {
+            float f[kIdxILP];
+#pragma unroll
+            for (int q = 0; q < kIdxILP; ++q) {
+                const int64_t x = x0 + (int64_t)q * blockDim.x;
+                f[q] = x < d ? __ldg(w + b + x) : 0.0f;
+            }
+#pragma unroll
+            for (int q = 0; q < kIdxILP; ++q) {
+                const int64_t x = x0 + (int64_t)q * blockDim.x;
+                agg_count(sh, x < d ? bucket_fast(sb, nbk, f[q], wmin, inv_l2g) : kSentinel);
+            }
+        }
         __syncthreads();
         if (threadIdx.x < 32) {                               // exclusive scan (nbk <= kIdxBins), one warp
             uint32_t carry = 0;
@@ -610,9 +815,21 @@ __global__ void __launch_bounds__(1024) k_amsf_hub_index(const int64_t* __restri
         uint32_t* hs = hstart + h * (nbk + 1);
         for (uint32_t i = threadIdx.x; i <= nbk; i += blockDim.x) hs[i] = sh[i];
         __syncthreads();
-        for (int64_t x = threadIdx.x; x < d; x += blockDim.x) {
-            const uint32_t bi = bucket_fast(sb, nbk, w[b + x], wmin, inv_l2g);
-            hidx[qb1[p] + atomicAdd(sh + bi, 1u)] = (uint32_t)x;
+        const unsigned long long hb = qb1[p];
+        for (int64_t x0 = threadIdx.x; x0 - threadIdx.x < d; x0 += (int64_t)blockDim.x * kIdxILP) {
+            float f[kIdxILP];
+#pragma unroll
+            for (int q = 0; q < kIdxILP; ++q) {
+                const int64_t x = x0 + (int64_t)q * blockDim.x;
+                f[q] = x < d ? __ldg(w + b + x) : 0.0f;
+            }
+#pragma unroll
+            for (int q = 0; q < kIdxILP; ++q) {
+                const int64_t x = x0 + (int64_t)q * blockDim.x;
+                const uint32_t key = x < d ? bucket_fast(sb, nbk, f[q], wmin, inv_l2g) : kSentinel;
+                const uint32_t slot = agg_slot(sh, key);
+                if (x < d) hidx[hb + slot] = (uint32_t)x;
+            }
         }
         __syncthreads();
     }
@@ -620,15 +837,18 @@ __global__ void __launch_bounds__(1024) k_amsf_hub_index(const int64_t* __restri
 
 // The same index for lists of kIdxMin < d <= kIdxWarpMax entries, one warp per
 // list (a per-warp shared histogram of nbk + 1 <= kIdxWarpBins bins).
-__global__ void __launch_bounds__(kBlock) k_amsf_idx_warp(const int64_t* __restrict__ off,
+constexpr int kIdxWBlock = 128;           // k_amsf_idx_warp block (4 warps: per-warp keys + bins in smem)
+__global__ void __launch_bounds__(kIdxWBlock) k_amsf_idx_warp(const int64_t* __restrict__ off,
                                                           const float* __restrict__ w, const uint32_t* q0,
                                                           const unsigned long long* qb0,
-                                                          const unsigned long long* hcount, const double* bnd,
+                                                          const unsigned long long* hcount, const float* bnd,
                                                           uint32_t nbk, float wmin, float inv_l2g, uint32_t* hid,
                                                           unsigned long long* hbase, uint32_t* hstart, uint32_t* hidx)
 {
-    __shared__ uint32_t sh[kBlock / 32][kIdxWarpBins];
-    __shared__ double sb[kIdxWarpBins];
+    __shared__ uint32_t sh[kIdxWBlock / 32][kIdxWarpBins];
+    __shared__ float sb[kIdxWarpBins];
+    __shared__ uint8_t skey[kIdxWBlock / 32][kIdxWarpMax];     // pass-1 bucket keys (nbk < 256)
+    const bool stage = nbk < 256;
     for (uint32_t i = threadIdx.x; i <= nbk; i += blockDim.x) sb[i] = bnd[i];
     __syncthreads();
     const unsigned lane = threadIdx.x & 31;
@@ -644,7 +864,19 @@ __global__ void __launch_bounds__(kBlock) k_amsf_idx_warp(const int64_t* __restr
         }
         for (uint32_t i = lane; i <= nbk; i += 32) hw[i] = 0;
         __syncwarp();
-        for (int64_t x = lane; x < d; x += 32) atomicAdd(hw + bucket_fast(sb, nbk, w[b + x], wmin, inv_l2g), 1u);
+        uint8_t* kw = skey[threadIdx.x >> 5];
+        for (int64_t x0 = lane; x0 - lane < d; x0 += 32 * kIdxILP) {
+            float f[kIdxILP];
+#pragma unroll
+            for (int q = 0; q < kIdxILP; ++q) f[q] = x0 + 32 * q < d ? __ldg(w + b + x0 + 32 * q) : 0.0f;
+#pragma unroll
+            for (int q = 0; q < kIdxILP; ++q) {
+                const int64_t x = x0 + 32 * q;
+                const uint32_t key = x < d ? bucket_fast(sb, nbk, f[q], wmin, inv_l2g) : kSentinel;
+                agg_count(hw, key);
+                if (stage && x < d) kw[x] = (uint8_t)key;
+            }
+        }
         __syncwarp();
         uint32_t carry = 0;                                     // exclusive scan of the bins
         for (uint32_t b0 = 0; b0 <= nbk; b0 += 32) {
@@ -662,9 +894,26 @@ __global__ void __launch_bounds__(kBlock) k_amsf_idx_warp(const int64_t* __restr
         uint32_t* hs = hstart + h * (nbk + 1);
         for (uint32_t i = lane; i <= nbk; i += 32) hs[i] = hw[i];
         __syncwarp();
-        for (int64_t x = lane; x < d; x += 32) {
-            const uint32_t bi = bucket_fast(sb, nbk, w[b + x], wmin, inv_l2g);
-            hidx[qb0[h] + atomicAdd(hw + bi, 1u)] = (uint32_t)x;
+        const unsigned long long hb = qb0[h];
+        if (stage) {                                            // keys from pass 1: no second weight read
+            for (int64_t x = lane; x - lane < d; x += 32) {
+                const uint32_t key = x < d ? (uint32_t)kw[x] : kSentinel;
+                const uint32_t slot = agg_slot(hw, key);
+                if (x < d) hidx[hb + slot] = (uint32_t)x;
+            }
+        } else {
+            for (int64_t x0 = lane; x0 - lane < d; x0 += 32 * kIdxILP) {
+                float f[kIdxILP];
+#pragma unroll
+                for (int q = 0; q < kIdxILP; ++q) f[q] = x0 + 32 * q < d ? __ldg(w + b + x0 + 32 * q) : 0.0f;
+#pragma unroll
+                for (int q = 0; q < kIdxILP; ++q) {
+                    const int64_t x = x0 + 32 * q;
+                    const uint32_t key = x < d ? bucket_fast(sb, nbk, f[q], wmin, inv_l2g) : kSentinel;
+                    const uint32_t slot = agg_slot(hw, key);
+                    if (x < d) hidx[hb + slot] = (uint32_t)x;
+                }
+            }
         }
         __syncwarp();
     }
@@ -682,7 +931,7 @@ __global__ void __launch_bounds__(kBlock) k_amsf_chunks(const int64_t* __restric
     const unsigned long long total = ac->chunks;
     const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
-    uint32_t hooks = 0;
+    uint32_t hooks = 0, links = 0;
     unsigned long long scanned = 0;
     for (unsigned long long q = warp; q < total; q += nwarps) {
         const uint2 item = chq[q];
@@ -705,8 +954,10 @@ __global__ void __launch_bounds__(kBlock) k_amsf_chunks(const int64_t* __restric
                     for (int c = 0; c < 4; ++c) {
                         const int64_t x = (q0 + 32 * j) * 4 + c;
                         const double xd = (double)v4[c];
-                        if (x >= b && x < e && xd >= blo && xd < bhi)
+                        if (x >= b && x < e && xd >= blo && xd < bhi) {
+                            ++links;
                             hooks += link<MODE>(P, item.x, adj[x], ForestW{F, Fw, v4[c]});
+                        }
                     }
                 }
             }
@@ -719,14 +970,17 @@ __global__ void __launch_bounds__(kBlock) k_amsf_chunks(const int64_t* __restric
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const double xd = (double)wx[j];
-                    if (xd >= blo && xd < bhi)
+                    if (xd >= blo && xd < bhi) {
+                        ++links;
                         hooks += link<MODE>(P, item.x, adj[x0 + 32 * j], ForestW{F, Fw, wx[j]});
+                    }
                 }
             }
         }
     }
     if (cnt) {
         warp_count(&cnt->amsf_hooks, hooks);
+        warp_count(&cnt->amsf_links, links);
         const unsigned long long sc = __reduce_add_sync(0xffffffffu, (uint32_t)min(scanned, 0xFFFFFFFFull));
         if (lane == 0 && sc) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt->amsf_edges), sc);
     }
@@ -773,9 +1027,12 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
     unsigned long long *hdeg = nullptr, *hbase = nullptr, *hcount = nullptr;
     float* Fw = nullptr;
     double* bd = nullptr;
+    float* bfl = nullptr;
+    std::vector<float> fbv;
     unsigned long long *start = nullptr, *cursor = nullptr;
     uint32_t* fcnt = nullptr;
     unsigned long long* foff = nullptr;
+    uint32_t* tile_vs = nullptr;
     const uint32_t nfb = (uint32_t)(((uint64_t)n + kFTile - 1) / kFTile);
     auto body = [&]() -> cc_status {
         CC_CUDA_TRY(scratch_alloc((void**)&ac, sizeof(AmsfCtl), s));
@@ -789,10 +1046,12 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
         h0.anchor = kSentinel;
         h0.skip_root = kSentinel;
         CC_CUDA_TRY(cudaMemcpyAsync(ac, &h0, sizeof(h0), cudaMemcpyHostToDevice, s));
-        k_amsf_init<<<sms * 8, kBlock, 0, s>>>(P, wlo, whi, F, n);
+        const uint64_t ntiles = (uint64_t)((m + kWrTile - 1) / kWrTile);
+        if (m > 0) CC_CUDA_TRY(scratch_alloc((void**)&tile_vs, sizeof(uint32_t) * ntiles, s));
+        k_amsf_init<<<sms * 8, kBlock, 0, s>>>(off, P, wlo, whi, F, n, m > 0 ? tile_vs : nullptr);
         CC_LAUNCH_CHECK("k_amsf_init");
         if (m > 0) {
-            k_amsf_wrange<<<sms * 16, kBlock, 0, s>>>(off, w, n, m, wlo, whi, ac);
+            k_amsf_wrange<<<sms * 16, kBlock, 0, s>>>(off, w, n, m, tile_vs, wlo, whi, ac);
             CC_LAUNCH_CHECK("k_amsf_wrange");
         }
         AmsfCtl h{};
@@ -825,6 +1084,16 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
             index = !plain && nb <= kIdxBins && !(o.flags & CC_FLAG_AMSF_NO_INDEX);
             CC_CUDA_TRY(scratch_alloc((void**)&bd, sizeof(double) * b.size(), s));
             CC_CUDA_TRY(cudaMemcpyAsync(bd, b.data(), sizeof(double) * b.size(), cudaMemcpyHostToDevice, s));
+            // the same boundaries as float thresholds: fb_i = the smallest float >= b_i, so that
+            // b_i <= (double)x  <=>  fb_i <= x for every float weight x (exact, reading R25)
+            fbv.resize(b.size());
+            for (size_t k = 0; k < b.size(); ++k) {
+                float f = (float)b[k];
+                if ((double)f < b[k]) f = std::nextafter(f, INFINITY);
+                fbv[k] = f;
+            }
+            CC_CUDA_TRY(scratch_alloc((void**)&bfl, sizeof(float) * fbv.size(), s));
+            CC_CUDA_TRY(cudaMemcpyAsync(bfl, fbv.data(), sizeof(float) * fbv.size(), cudaMemcpyHostToDevice, s));
             CC_CUDA_TRY(scratch_alloc((void**)&fb, sizeof(uint32_t) * n, s));
             CC_CUDA_TRY(scratch_alloc((void**)&order, sizeof(uint32_t) * n, s));
             CC_CUDA_TRY(scratch_alloc((void**)&carry[0], sizeof(uint32_t) * n, s));
@@ -866,7 +1135,7 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
                 const float wmin_f = (float)b[0], il2g = (float)(1.0 / std::log2(1.0 + eps));
                 if (hc[0]) {
                     if (nb + 1 <= kIdxWarpBins) {
-                        k_amsf_idx_warp<<<sms * 8, kBlock, 0, s>>>(off, w, q0, qb0, hcount, bd, nb, wmin_f, il2g, hid,
+                        k_amsf_idx_warp<<<sms * 16, kIdxWBlock, 0, s>>>(off, w, q0, qb0, hcount, bfl, nb, wmin_f, il2g, hid,
                                                                   hbase, hstart, hidx);
                         CC_LAUNCH_CHECK("k_amsf_idx_warp");
                     } else {
@@ -874,7 +1143,7 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
                     }
                 }
                 if (index && hc[1]) {
-                    k_amsf_hub_index<<<sms * 2, 1024, 0, s>>>(off, w, q1, qb1, hcount, bd, nb, wmin_f, il2g, hid, hbase,
+                    k_amsf_hub_index<<<sms * 2, 1024, 0, s>>>(off, w, q1, qb1, hcount, bfl, nb, wmin_f, il2g, hid, hbase,
                                                               hstart, hidx);
                     CC_LAUNCH_CHECK("k_amsf_hub_index");
                 }
@@ -937,8 +1206,8 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
     const cc_status rc = body();
     for (void* p : {(void*)ac, (void*)P, (void*)wlo, (void*)whi, (void*)fb, (void*)order, (void*)carry[0],
                     (void*)carry[1], (void*)F, (void*)Fw, (void*)chq, (void*)hubs, (void*)hid, (void*)hstart,
-                    (void*)hidx, (void*)hdeg, (void*)hbase, (void*)hcount, (void*)bd, (void*)start, (void*)cursor, (void*)fcnt,
-                    (void*)foff})
+                    (void*)hidx, (void*)hdeg, (void*)hbase, (void*)hcount, (void*)bd, (void*)bfl, (void*)start, (void*)cursor, (void*)fcnt,
+                    (void*)foff, (void*)tile_vs})
         scratch_free(p, s);
     return rc;
 }

@@ -27,5 +27,11 @@ for _ in range(reps - 1):
     e1.synchronize()
     ts.append(e0.elapsed_time(e1))
 c = dict(zip(cc.COUNTER_FIELDS, ctr.cpu().tolist()))
+if os.environ.get("DEGSTATS"):
+    deg = (d_off[1:] - d_off[:-1])
+    m = int(d_off[-1].item())
+    for lo, hi in ((0, 0), (1, 32), (33, 256), (257, 4096), (4097, 1 << 40)):
+        sel = (deg >= lo) & (deg <= hi)
+        print(f"deg {lo}-{hi}: vertices {int(sel.sum().item())} entries {int(deg[sel].sum().item()) / m:.3f}")
 print(cfg.name, "forest", E.shape[0], "W", tot, "ms", [round(t, 2) for t in ts],
       {k: v for k, v in c.items() if k.startswith("amsf")})
