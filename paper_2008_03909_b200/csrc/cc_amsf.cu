@@ -93,7 +93,7 @@ __device__ __forceinline__ bool good_weight(float x) { return x > 0.0f && x < __
 // forward.  Per
 // vertex min / max are combined in shared memory; a vertex wholly inside the tile
 // is stored plainly, one that straddles a tile boundary is combined by global
-// atomics into wlo / whi (initialised to +inf / 0 by k_amsf_init).  (The thread-
+// atomics into vi[v].x / .y (initialised to +inf / 0 by k_amsf_init).  (The thread-
 // per-vertex version walked each short list serially: 12.7 ms on C4, latency-bound.)
 #ifndef CC_AMSF_WR_STAGE
 #define CC_AMSF_WR_STAGE 0
@@ -106,7 +106,7 @@ constexpr int64_t kWrTile = (int64_t)kBlock * kWrItems;
 constexpr uint32_t kWrCap = 2048;          // vertices per tile combined in shared memory
 __global__ void __launch_bounds__(kBlock) k_amsf_wrange(const int64_t* __restrict__ off, const float* __restrict__ w,
                                                         uint32_t n, int64_t m, const uint32_t* __restrict__ tile_vs,
-                                                        uint32_t* wlo, uint32_t* whi, AmsfCtl* ac)
+                                                        uint4* vi, AmsfCtl* ac)
 {
     __shared__ uint32_t s_lo[kWrCap], s_hi[kWrCap];
 #if CC_AMSF_WR_STAGE
@@ -165,8 +165,8 @@ __global__ void __launch_bounds__(kBlock) k_amsf_wrange(const int64_t* __restric
                     atomicMin(s_lo + j, vlo);
                     atomicMax(s_hi + j, vhi);
                 } else {
-                    atomicMin(wlo + owner, vlo);
-                    atomicMax(whi + owner, vhi);
+                    atomicMin(reinterpret_cast<uint32_t*>(vi + owner), vlo);
+                    atomicMax(reinterpret_cast<uint32_t*>(vi + owner) + 1, vhi);
                 }
                 gmin = min(gmin, vlo);
                 gmax = max(gmax, vhi);
@@ -221,11 +221,10 @@ __global__ void __launch_bounds__(kBlock) k_amsf_wrange(const int64_t* __restric
             if (s_lo[j] == kPosInfBits && s_hi[j] == 0) continue;          // no entry in this tile
             const uint32_t v = vs + j;
             if (offat(v) >= E0 && offat(v + 1) <= E1) {
-                wlo[v] = s_lo[j];
-                whi[v] = s_hi[j];
+                *reinterpret_cast<uint2*>(vi + v) = make_uint2(s_lo[j], s_hi[j]);
             } else {
-                atomicMin(wlo + v, s_lo[j]);
-                atomicMax(whi + v, s_hi[j]);
+                atomicMin(reinterpret_cast<uint32_t*>(vi + v), s_lo[j]);
+                atomicMax(reinterpret_cast<uint32_t*>(vi + v) + 1, s_hi[j]);
             }
         }
         __syncthreads();
@@ -242,13 +241,12 @@ __global__ void __launch_bounds__(kBlock) k_amsf_wrange(const int64_t* __restric
 
 // P, the weight ranges and the forest slots; and tile_vs[t] = the vertex whose list
 // holds entry t * kWrTile (the first entry of wrange tile t).
-__global__ void k_amsf_init(const int64_t* __restrict__ off, uint32_t* P, uint32_t* wlo, uint32_t* whi, uint2* F,
+__global__ void k_amsf_init(const int64_t* __restrict__ off, uint32_t* P, uint4* vi, uint2* F,
                             uint32_t n, uint32_t* tile_vs)
 {
     for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
         P[v] = (uint32_t)v;
-        wlo[v] = kPosInfBits;
-        whi[v] = 0u;
+        vi[v] = make_uint4(kPosInfBits, 0u, kSentinel, 0u);
         F[v] = make_uint2(kSentinel, kSentinel);
         if (tile_vs) {
             const int64_t b = off[v], e = off[v + 1];
@@ -274,7 +272,7 @@ __device__ __forceinline__ uint32_t bucket_of(const double* b, uint32_t nb, floa
 // memory histogram (when the buckets fit), one global atomic per non-empty bin
 constexpr uint32_t kSmemBins = 4096;
 constexpr uint32_t kIdxBins = 4000;      // the hub bucket index is built when nb <= this
-__global__ void __launch_bounds__(kBlock) k_amsf_first(const uint32_t* wlo, const uint32_t* whi, uint32_t n,
+__global__ void __launch_bounds__(kBlock) k_amsf_first(const uint4* vi, uint32_t n,
                                                        const double* b, uint32_t nb, bool plain, uint32_t* fb,
                                                        unsigned long long* hist)
 {
@@ -284,8 +282,9 @@ __global__ void __launch_bounds__(kBlock) k_amsf_first(const uint32_t* wlo, cons
         for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) sh[i] = 0;
     __syncthreads();
     for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
-        if (!whi[v]) continue;                                // isolated
-        const uint32_t f = plain ? 0u : bucket_of(b, nb, __uint_as_float(wlo[v]));
+        const uint2 r = *reinterpret_cast<const uint2*>(vi + v);
+        if (!r.y) continue;                                   // isolated
+        const uint32_t f = plain ? 0u : bucket_of(b, nb, __uint_as_float(r.x));
         fb[v] = f;
         if (local) atomicAdd(sh + f, 1u);
         else atomicAdd(hist + f, 1ull);
@@ -326,7 +325,7 @@ __global__ void __launch_bounds__(kBlock) k_amsf_scan(unsigned long long* hist, 
 
 // order[] by activation bucket: per block tile of 8 * kBlock vertices, ranks within
 // the tile from shared atomics, one global range per non-empty bin and tile
-__global__ void __launch_bounds__(kBlock) k_amsf_scatter(const uint32_t* whi, const uint32_t* fb, uint32_t n,
+__global__ void __launch_bounds__(kBlock) k_amsf_scatter(const uint4* vi, const uint32_t* fb, uint32_t n,
                                                          uint32_t nb, unsigned long long* cursor, uint32_t* order)
 {
     constexpr int V = 8;
@@ -339,7 +338,7 @@ __global__ void __launch_bounds__(kBlock) k_amsf_scatter(const uint32_t* whi, co
 #pragma unroll
         for (int k = 0; k < V; ++k) {
             const uint64_t v = t0 + (uint64_t)k * kBlock + threadIdx.x;
-            act[k] = v < n && whi[v] != 0;
+            act[k] = v < n && reinterpret_cast<const uint2*>(vi + v)->y != 0;
             f[k] = act[k] ? fb[v] : 0u;
         }
         if (!local) {
@@ -455,11 +454,11 @@ __global__ void __launch_bounds__(1024) k_amsf_lmax(uint32_t* P, uint32_t n, uin
 template <int MODE>
 __global__ void __launch_bounds__(kBlock, CC_AMSF_ROUND_MINB) k_amsf_round(
     const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, const float* __restrict__ w, uint32_t* P,
-    const uint32_t* __restrict__ wlo, const uint32_t* __restrict__ whi, const uint32_t* __restrict__ order,
+    const uint4* __restrict__ vi, const uint32_t* __restrict__ order,
     const unsigned long long* __restrict__ start, uint32_t round, double blo, double bhi,
     const uint32_t* __restrict__ carry_in, AmsfCtl* ac, int in_slot, uint32_t* carry_out, bool skip, bool plain,
-    uint2* F, float* Fw, uint2* chq, const uint32_t* __restrict__ hid, const uint32_t* __restrict__ hstart,
-    const unsigned long long* __restrict__ hbase, const uint32_t* __restrict__ hidx, uint32_t nbk, cc_counters* cnt)
+    uint2* F, float* Fw, uint2* chq, const unsigned long long* __restrict__ hstart,
+    const uint32_t* __restrict__ hidx, uint32_t nbk, cc_counters* cnt)
 {
     const unsigned lane = threadIdx.x & 31;
     const bool rebuild = ac->rebuild != 0;
@@ -478,10 +477,13 @@ __global__ void __launch_bounds__(kBlock, CC_AMSF_ROUND_MINB) k_amsf_round(
         const bool cand = lane < cpw && i < total;
         const uint32_t u = cand ? (i < n1 ? carry_in[i] : order[s0 + (i - n1)]) : 0u;
         bool keep = false, work = false;
+        uint32_t hub = kSentinel;
         if (cand) {
             ++visits;
-            const double hi_w = plain ? INFINITY : (double)__uint_as_float(whi[u]);
-            const double lo_w = plain ? 0.0 : (double)__uint_as_float(wlo[u]);
+            const uint4 vv = vi[u];                            // [lightest, heaviest] weight bits, hub id
+            hub = vv.z;
+            const double hi_w = plain ? INFINITY : (double)__uint_as_float(vv.y);
+            const double lo_w = plain ? 0.0 : (double)__uint_as_float(vv.x);
             // FindAtomicSplit (hooks run concurrently): walks stay short on chain-shaped inputs
             if (hi_w >= blo && !(skip_root != kSentinel && find_split(P, u) == skip_root)) {
                 keep = hi_w >= bhi;                            // edges left for later buckets
@@ -498,10 +500,9 @@ __global__ void __launch_bounds__(kBlock, CC_AMSF_ROUND_MINB) k_amsf_round(
         const bool indexed = hstart && dfull > kIdxMin;
         int64_t len = dfull, rbase = b;
         if (indexed) {
-            const uint32_t h = hid[u];
-            const uint32_t* hs = hstart + (uint64_t)h * (nbk + 1);
-            rbase = (int64_t)hbase[h] + hs[round];
-            len = (int64_t)hs[round + 1] - (int64_t)hs[round];
+            const unsigned long long* hs = hstart + (uint64_t)hub * (nbk + 1);
+            rbase = (int64_t)hs[round];
+            len = (int64_t)hs[round + 1] - rbase;
         }
         const bool big = len > kAmsfChunk;
         if (big) {
@@ -572,9 +573,8 @@ __global__ void __launch_bounds__(kBlock) k_amsf_hub_pieces(const int64_t* __res
                                                             const uint32_t* __restrict__ adj,
                                                             const float* __restrict__ w, uint32_t* P, uint32_t round,
                                                             const uint2* __restrict__ chq, const AmsfCtl* ac,
-                                                            const uint32_t* __restrict__ hid,
-                                                            const uint32_t* __restrict__ hstart,
-                                                            const unsigned long long* __restrict__ hbase,
+                                                            const uint4* __restrict__ vi,
+                                                            const unsigned long long* __restrict__ hstart,
                                                             const uint32_t* __restrict__ hidx, uint32_t nbk, uint2* F,
                                                             float* Fw, cc_counters* cnt)
 {
@@ -586,10 +586,9 @@ __global__ void __launch_bounds__(kBlock) k_amsf_hub_pieces(const int64_t* __res
     unsigned long long scanned = 0;
     for (unsigned long long q = warp; q < total; q += nwarps) {
         const uint2 item = chq[q];
-        const uint32_t h = hid[item.x];
-        const uint32_t* hs = hstart + (uint64_t)h * (nbk + 1);
-        const unsigned long long s0 = hbase[h] + hs[round] + (unsigned long long)item.y * kAmsfChunk;
-        const unsigned long long s1 = min(hbase[h] + hs[round + 1], s0 + kAmsfChunk);
+        const unsigned long long* hs = hstart + (uint64_t)vi[item.x].z * (nbk + 1);
+        const unsigned long long s0 = hs[round] + (unsigned long long)item.y * kAmsfChunk;
+        const unsigned long long s1 = min(hs[round + 1], s0 + kAmsfChunk);
         const int64_t o = off[item.x];
         scanned += lane == 0 ? s1 - s0 : 0ull;
         for (unsigned long long x0 = s0 + lane; x0 < s1; x0 += 32 * 4) {
@@ -620,8 +619,12 @@ __global__ void __launch_bounds__(kBlock) k_amsf_hub_pieces(const int64_t* __res
 }
 
 // Bucket index (built once): the vertices with more than kIdxMin entries,
-// hid[v] = their index, and per hub its entries (offsets relative to off[v])
-// grouped by bucket: hidx[hbase[h] + hstart[h][i] ..] are the bucket-i entries.
+// vi[v].z = their index h, and per hub its entries (offsets relative to off[v])
+// grouped by bucket: hidx[hstart[h][i] .. hstart[h][i+1]) are the bucket-i
+// entries (absolute 64-bit starts, so a visit reads one line of hstart).  A
+// visit of the round kernel reads its vertex's lightest / heaviest weight and
+// hub id in ONE 16-byte vi load (three separate arrays made it three random
+// sectors; the rounds are bound by these per-visit gathers).
 // (Storing (neighbour, weight) pairs instead, so that a round reads its edges
 // contiguously, was measured: the rounds stay bound by the links' P gathers
 // (32.0 vs 29.9 ms on C4) and the build moves 8 B more per entry.)
@@ -766,8 +769,8 @@ __global__ void __launch_bounds__(1024) k_amsf_hub_index(const int64_t* __restri
                                                          const float* __restrict__ w, const uint32_t* q1,
                                                          const unsigned long long* qb1,
                                                          const unsigned long long* hcount, const float* bnd,
-                                                         uint32_t nbk, float wmin, float inv_l2g, uint32_t* hid,
-                                                         unsigned long long* hbase, uint32_t* hstart, uint32_t* hidx)
+                                                         uint32_t nbk, float wmin, float inv_l2g, uint4* vi,
+                                                         unsigned long long* hstart, uint32_t* hidx)
 {
     __shared__ uint32_t sh[kIdxBins + 1];
     __shared__ float sb[kIdxBins + 1];
@@ -778,8 +781,7 @@ __global__ void __launch_bounds__(1024) k_amsf_hub_index(const int64_t* __restri
         const unsigned long long h = H0 + p;
         const int64_t b = off[v], d = off[v + 1] - b;
         if (threadIdx.x == 0) {
-            hid[v] = (uint32_t)h;
-            hbase[h] = qb1[p];
+            reinterpret_cast<uint32_t*>(vi + v)[2] = (uint32_t)h;
         }
         for (uint32_t i = threadIdx.x; i <= nbk; i += blockDim.x) sh[i] = 0;
         __syncthreads();
@@ -812,8 +814,8 @@ __global__ void __launch_bounds__(1024) k_amsf_hub_index(const int64_t* __restri
             }
         }
         __syncthreads();
-        uint32_t* hs = hstart + h * (nbk + 1);
-        for (uint32_t i = threadIdx.x; i <= nbk; i += blockDim.x) hs[i] = sh[i];
+        unsigned long long* hs = hstart + h * (nbk + 1);          // absolute bucket starts in hidx
+        for (uint32_t i = threadIdx.x; i <= nbk; i += blockDim.x) hs[i] = qb1[p] + sh[i];
         __syncthreads();
         const unsigned long long hb = qb1[p];
         for (int64_t x0 = threadIdx.x; x0 - threadIdx.x < d; x0 += (int64_t)blockDim.x * kIdxILP) {
@@ -842,8 +844,8 @@ __global__ void __launch_bounds__(kIdxWBlock) k_amsf_idx_warp(const int64_t* __r
                                                           const float* __restrict__ w, const uint32_t* q0,
                                                           const unsigned long long* qb0,
                                                           const unsigned long long* hcount, const float* bnd,
-                                                          uint32_t nbk, float wmin, float inv_l2g, uint32_t* hid,
-                                                          unsigned long long* hbase, uint32_t* hstart, uint32_t* hidx)
+                                                          uint32_t nbk, float wmin, float inv_l2g, uint4* vi,
+                                                          unsigned long long* hstart, uint32_t* hidx)
 {
     __shared__ uint32_t sh[kIdxWBlock / 32][kIdxWarpBins];
     __shared__ float sb[kIdxWarpBins];
@@ -859,8 +861,7 @@ __global__ void __launch_bounds__(kIdxWBlock) k_amsf_idx_warp(const int64_t* __r
         const uint32_t v = q0[h];
         const int64_t b = off[v], d = off[v + 1] - b;
         if (lane == 0) {
-            hid[v] = (uint32_t)h;
-            hbase[h] = qb0[h];
+            reinterpret_cast<uint32_t*>(vi + v)[2] = (uint32_t)h;
         }
         for (uint32_t i = lane; i <= nbk; i += 32) hw[i] = 0;
         __syncwarp();
@@ -891,8 +892,8 @@ __global__ void __launch_bounds__(kIdxWBlock) k_amsf_idx_warp(const int64_t* __r
             carry += __shfl_sync(0xffffffffu, incl, 31);
         }
         __syncwarp();
-        uint32_t* hs = hstart + h * (nbk + 1);
-        for (uint32_t i = lane; i <= nbk; i += 32) hs[i] = hw[i];
+        unsigned long long* hs = hstart + h * (nbk + 1);          // absolute bucket starts in hidx
+        for (uint32_t i = lane; i <= nbk; i += 32) hs[i] = qb0[h] + hw[i];
         __syncwarp();
         const unsigned long long hb = qb0[h];
         if (stage) {                                            // keys from pass 1: no second weight read
@@ -1019,12 +1020,13 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
     const char* tr = std::getenv("CC_AMSF_TRACE");
     const bool trace = tr && tr[0] == '1';
     AmsfCtl* ac = nullptr;
-    uint32_t *P = nullptr, *wlo = nullptr, *whi = nullptr, *fb = nullptr, *order = nullptr;
+    uint32_t *P = nullptr, *fb = nullptr, *order = nullptr;
+    uint4* vi = nullptr;                      // per vertex: lightest / heaviest weight bits, hub id
     uint32_t* carry[2] = {nullptr, nullptr};
     uint2* F = nullptr;
     uint2* chq = nullptr;
-    uint32_t *hubs = nullptr, *hid = nullptr, *hstart = nullptr, *hidx = nullptr;
-    unsigned long long *hdeg = nullptr, *hbase = nullptr, *hcount = nullptr;
+    uint32_t *hubs = nullptr, *hidx = nullptr;
+    unsigned long long *hdeg = nullptr, *hstart = nullptr, *hcount = nullptr;
     float* Fw = nullptr;
     double* bd = nullptr;
     float* bfl = nullptr;
@@ -1037,8 +1039,7 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
     auto body = [&]() -> cc_status {
         CC_CUDA_TRY(scratch_alloc((void**)&ac, sizeof(AmsfCtl), s));
         CC_CUDA_TRY(scratch_alloc((void**)&P, sizeof(uint32_t) * n, s));
-        CC_CUDA_TRY(scratch_alloc((void**)&wlo, sizeof(uint32_t) * n, s));
-        CC_CUDA_TRY(scratch_alloc((void**)&whi, sizeof(uint32_t) * n, s));
+        CC_CUDA_TRY(scratch_alloc((void**)&vi, sizeof(uint4) * n, s));
         CC_CUDA_TRY(scratch_alloc((void**)&F, sizeof(uint2) * n, s));
         CC_CUDA_TRY(scratch_alloc((void**)&Fw, sizeof(float) * n, s));
         AmsfCtl h0{};
@@ -1048,10 +1049,10 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
         CC_CUDA_TRY(cudaMemcpyAsync(ac, &h0, sizeof(h0), cudaMemcpyHostToDevice, s));
         const uint64_t ntiles = (uint64_t)((m + kWrTile - 1) / kWrTile);
         if (m > 0) CC_CUDA_TRY(scratch_alloc((void**)&tile_vs, sizeof(uint32_t) * ntiles, s));
-        k_amsf_init<<<sms * 8, kBlock, 0, s>>>(off, P, wlo, whi, F, n, m > 0 ? tile_vs : nullptr);
+        k_amsf_init<<<sms * 8, kBlock, 0, s>>>(off, P, vi, F, n, m > 0 ? tile_vs : nullptr);
         CC_LAUNCH_CHECK("k_amsf_init");
         if (m > 0) {
-            k_amsf_wrange<<<sms * 16, kBlock, 0, s>>>(off, w, n, m, tile_vs, wlo, whi, ac);
+            k_amsf_wrange<<<sms * 16, kBlock, 0, s>>>(off, w, n, m, tile_vs, vi, ac);
             CC_LAUNCH_CHECK("k_amsf_wrange");
         }
         AmsfCtl h{};
@@ -1104,12 +1105,12 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
             CC_CUDA_TRY(scratch_alloc((void**)&cursor, sizeof(unsigned long long) * (nb + 1), s));
             CC_CUDA_TRY(cudaMemsetAsync(start, 0, sizeof(unsigned long long) * (nb + 1), s));
             // activation order: non-isolated vertices by the bucket of their lightest edge
-            k_amsf_first<<<sms * 8, kBlock, 0, s>>>(wlo, whi, n, bd, nb, plain, fb, start);
+            k_amsf_first<<<sms * 8, kBlock, 0, s>>>(vi, n, bd, nb, plain, fb, start);
             CC_LAUNCH_CHECK("k_amsf_first");
             k_amsf_scan<<<1, kBlock, 0, s>>>(start, nb);
             CC_LAUNCH_CHECK("k_amsf_scan");
             CC_CUDA_TRY(cudaMemcpyAsync(cursor, start, sizeof(unsigned long long) * (nb + 1), cudaMemcpyDeviceToDevice, s));
-            k_amsf_scatter<<<sms * 8, kBlock, 0, s>>>(whi, fb, n, nb, cursor, order);
+            k_amsf_scatter<<<sms * 8, kBlock, 0, s>>>(vi, fb, n, nb, cursor, order);
             CC_LAUNCH_CHECK("k_amsf_scatter");
             if (index) {
                 // bucket index: lists longer than kIdxMin grouped by bucket, once; the list
@@ -1119,7 +1120,6 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
                 CC_CUDA_TRY(scratch_alloc((void**)&hubs, sizeof(uint32_t) * (qcap0 + qcap1), s));
                 CC_CUDA_TRY(scratch_alloc((void**)&hdeg, sizeof(unsigned long long) * (qcap0 + qcap1), s));
                 CC_CUDA_TRY(scratch_alloc((void**)&hcount, 3 * sizeof(unsigned long long), s));
-                CC_CUDA_TRY(scratch_alloc((void**)&hid, sizeof(uint32_t) * n, s));
                 CC_CUDA_TRY(cudaMemsetAsync(hcount, 0, 3 * sizeof(unsigned long long), s));
                 uint32_t *q0 = hubs, *q1 = hubs + qcap0;
                 unsigned long long *qb0 = hdeg, *qb1 = hdeg + qcap0;
@@ -1129,22 +1129,21 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
                 CC_CUDA_TRY(cudaMemcpyAsync(hc, hcount, sizeof(hc), cudaMemcpyDeviceToHost, s));
                 CC_CUDA_TRY(cudaStreamSynchronize(s));
                 const uint64_t H = hc[0] + hc[1];
-                CC_CUDA_TRY(scratch_alloc((void**)&hbase, sizeof(unsigned long long) * std::max<uint64_t>(H, 1), s));
-                CC_CUDA_TRY(scratch_alloc((void**)&hstart, sizeof(uint32_t) * std::max<uint64_t>(H, 1) * (nb + 1), s));
+                CC_CUDA_TRY(scratch_alloc((void**)&hstart, sizeof(unsigned long long) * std::max<uint64_t>(H, 1) * (nb + 1), s));
                 CC_CUDA_TRY(scratch_alloc((void**)&hidx, sizeof(uint32_t) * std::max<uint64_t>(hc[2], 1), s));
                 const float wmin_f = (float)b[0], il2g = (float)(1.0 / std::log2(1.0 + eps));
                 if (hc[0]) {
                     if (nb + 1 <= kIdxWarpBins) {
-                        k_amsf_idx_warp<<<sms * 16, kIdxWBlock, 0, s>>>(off, w, q0, qb0, hcount, bfl, nb, wmin_f, il2g, hid,
-                                                                  hbase, hstart, hidx);
+                        k_amsf_idx_warp<<<sms * 16, kIdxWBlock, 0, s>>>(off, w, q0, qb0, hcount, bfl, nb, wmin_f, il2g, vi,
+                                                                  hstart, hidx);
                         CC_LAUNCH_CHECK("k_amsf_idx_warp");
                     } else {
                         index = false;                      // too many buckets for the warp build: no index
                     }
                 }
                 if (index && hc[1]) {
-                    k_amsf_hub_index<<<sms * 2, 1024, 0, s>>>(off, w, q1, qb1, hcount, bfl, nb, wmin_f, il2g, hid, hbase,
-                                                              hstart, hidx);
+                    k_amsf_hub_index<<<sms * 2, 1024, 0, s>>>(off, w, q1, qb1, hcount, bfl, nb, wmin_f, il2g, vi, hstart,
+                                                              hidx);
                     CC_LAUNCH_CHECK("k_amsf_hub_index");
                 }
             }
@@ -1156,13 +1155,13 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
                 k_amsf_lmax<<<1, 1024, 0, s>>>(P, n, o.seed, i, o.samples, ac);
                 CC_LAUNCH_CHECK("k_amsf_lmax");
             }
-            k_amsf_round<MODE><<<sms * 8, kBlock, 0, s>>>(off, adj, w, P, wlo, whi, order, start, i, b[i], b[i + 1],
+            k_amsf_round<MODE><<<sms * 8, kBlock, 0, s>>>(off, adj, w, P, vi, order, start, i, b[i], b[i + 1],
                                                           carry[in_slot], ac, in_slot, carry[in_slot ^ 1],
-                                                          skip, plain, F, Fw, chq, hid, index ? hstart : nullptr,
-                                                          hbase, hidx, nb, o.counters);
+                                                          skip, plain, F, Fw, chq, index ? hstart : nullptr,
+                                                          hidx, nb, o.counters);
             CC_LAUNCH_CHECK("k_amsf_round");
             if (index)
-                k_amsf_hub_pieces<MODE><<<sms * 8, kBlock, 0, s>>>(off, adj, w, P, i, chq, ac, hid, hstart, hbase, hidx,
+                k_amsf_hub_pieces<MODE><<<sms * 8, kBlock, 0, s>>>(off, adj, w, P, i, chq, ac, vi, hstart, hidx,
                                                                    nb, F, Fw, o.counters);
             else if (((uintptr_t)w & 15u) == 0)
                 k_amsf_chunks<MODE, true><<<sms * 8, kBlock, 0, s>>>(off, adj, w, P, b[i], b[i + 1], chq, ac, F, Fw,
@@ -1204,9 +1203,9 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
         return CC_OK;
     };
     const cc_status rc = body();
-    for (void* p : {(void*)ac, (void*)P, (void*)wlo, (void*)whi, (void*)fb, (void*)order, (void*)carry[0],
-                    (void*)carry[1], (void*)F, (void*)Fw, (void*)chq, (void*)hubs, (void*)hid, (void*)hstart,
-                    (void*)hidx, (void*)hdeg, (void*)hbase, (void*)hcount, (void*)bd, (void*)bfl, (void*)start, (void*)cursor, (void*)fcnt,
+    for (void* p : {(void*)ac, (void*)P, (void*)vi, (void*)fb, (void*)order, (void*)carry[0],
+                    (void*)carry[1], (void*)F, (void*)Fw, (void*)chq, (void*)hubs, (void*)hstart,
+                    (void*)hidx, (void*)hdeg, (void*)hcount, (void*)bd, (void*)bfl, (void*)start, (void*)cursor, (void*)fcnt,
                     (void*)foff, (void*)tile_vs})
         scratch_free(p, s);
     return rc;
