@@ -156,7 +156,7 @@ typedef struct {
     uint64_t amsf_hooks;       /* cc_amsf: successful root hooks (= forest edges)      */
     uint64_t amsf_rebuilds;    /* cc_amsf: rounds whose L_max left the skipped component*/
     uint64_t fused_link;       /* 1 if the k-out links ran inside k_sample_link         */
-    uint64_t amsf_links;       /* cc_amsf: in-bucket edges linked (indexed and scanned)  */
+    uint64_t amsf_links;       /* cc_amsf: in-bucket edges linked (diagnostics build only)*/
 } cc_counters;
 
 typedef struct {

@@ -63,6 +63,16 @@ struct AmsfCtl {
 };
 
 constexpr int64_t kAmsfChunk = 2048;   // lists longer than this are split across warps
+// cc_counters.amsf_links (in-bucket edges linked) is counted only in a diagnostics
+// build (-DCC_AMSF_COUNT_LINKS): the counter costs the edge sweeps registers and
+// occupancy (NF-S as stated: 98 -> 118 ms on C3)
+#ifdef CC_AMSF_COUNT_LINKS
+#define CC_AMSF_LINK_INC(x) (++(x))
+#define CC_AMSF_LINK_FLUSH(cnt, x) warp_count(&(cnt)->amsf_links, (x))
+#else
+#define CC_AMSF_LINK_INC(x) ((void)0)
+#define CC_AMSF_LINK_FLUSH(cnt, x) ((void)(x))
+#endif
 #ifndef CC_AMSF_IDX_MIN
 #define CC_AMSF_IDX_MIN 256
 #endif
@@ -449,7 +459,7 @@ __global__ void __launch_bounds__(1024) k_amsf_lmax(uint32_t* P, uint32_t n, uin
 // an anchor move, order[0 .. start[i+1]).  Survivors are appended to the next
 // carry list.
 #ifndef CC_AMSF_ROUND_MINB
-#define CC_AMSF_ROUND_MINB 1
+#define CC_AMSF_ROUND_MINB 4
 #endif
 template <int MODE>
 __global__ void __launch_bounds__(kBlock, CC_AMSF_ROUND_MINB) k_amsf_round(
@@ -480,7 +490,8 @@ __global__ void __launch_bounds__(kBlock, CC_AMSF_ROUND_MINB) k_amsf_round(
         uint32_t hub = kSentinel;
         if (cand) {
             ++visits;
-            const uint4 vv = vi[u];                            // [lightest, heaviest] weight bits, hub id
+            // [lightest, heaviest] weight bits, hub id (not needed as NF-S is stated: PLAIN)
+            const uint4 vv = plain ? make_uint4(0u, 0u, kSentinel, 0u) : vi[u];
             hub = vv.z;
             const double hi_w = plain ? INFINITY : (double)__uint_as_float(vv.y);
             const double lo_w = plain ? 0.0 : (double)__uint_as_float(vv.x);
@@ -548,7 +559,7 @@ __global__ void __launch_bounds__(kBlock, CC_AMSF_ROUND_MINB) k_amsf_round(
             for (int j = 0; j < 4; ++j) {
                 const double xd = (double)x[j];
                 if (ex[j] >= 0 && xd >= blo && xd < bhi) {
-                    ++links;
+                    CC_AMSF_LINK_INC(links);
                     hooks += link<MODE>(P, ou[j], adj[ex[j]], ForestW{F, Fw, x[j]});
                 }
             }
@@ -558,7 +569,7 @@ __global__ void __launch_bounds__(kBlock, CC_AMSF_ROUND_MINB) k_amsf_round(
     if (cnt) {
         warp_count(&cnt->amsf_visits, visits);
         warp_count(&cnt->amsf_hooks, hooks);
-        warp_count(&cnt->amsf_links, links);
+        CC_AMSF_LINK_FLUSH(cnt, links);
         const unsigned long long sc = __reduce_add_sync(0xffffffffu, (uint32_t)min(scanned, 0xFFFFFFFFull));
         if (lane == 0 && sc) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt->amsf_edges), sc);
     }
@@ -605,14 +616,14 @@ __global__ void __launch_bounds__(kBlock) k_amsf_hub_pieces(const int64_t* __res
 #pragma unroll
             for (int j = 0; j < 4; ++j)
                 if (e[j] >= 0) {
-                    ++links;
+                    CC_AMSF_LINK_INC(links);
                     hooks += link<MODE>(P, item.x, vx[j], ForestW{F, Fw, wx[j]});
                 }
         }
     }
     if (cnt) {
         warp_count(&cnt->amsf_hooks, hooks);
-        warp_count(&cnt->amsf_links, links);
+        CC_AMSF_LINK_FLUSH(cnt, links);
         const unsigned long long sc = __reduce_add_sync(0xffffffffu, (uint32_t)min(scanned, 0xFFFFFFFFull));
         if (lane == 0 && sc) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt->amsf_edges), sc);
     }
@@ -956,7 +967,7 @@ __global__ void __launch_bounds__(kBlock) k_amsf_chunks(const int64_t* __restric
                         const int64_t x = (q0 + 32 * j) * 4 + c;
                         const double xd = (double)v4[c];
                         if (x >= b && x < e && xd >= blo && xd < bhi) {
-                            ++links;
+                            CC_AMSF_LINK_INC(links);
                             hooks += link<MODE>(P, item.x, adj[x], ForestW{F, Fw, v4[c]});
                         }
                     }
@@ -972,7 +983,7 @@ __global__ void __launch_bounds__(kBlock) k_amsf_chunks(const int64_t* __restric
                 for (int j = 0; j < 8; ++j) {
                     const double xd = (double)wx[j];
                     if (xd >= blo && xd < bhi) {
-                        ++links;
+                        CC_AMSF_LINK_INC(links);
                         hooks += link<MODE>(P, item.x, adj[x0 + 32 * j], ForestW{F, Fw, wx[j]});
                     }
                 }
@@ -981,7 +992,7 @@ __global__ void __launch_bounds__(kBlock) k_amsf_chunks(const int64_t* __restric
     }
     if (cnt) {
         warp_count(&cnt->amsf_hooks, hooks);
-        warp_count(&cnt->amsf_links, links);
+        CC_AMSF_LINK_FLUSH(cnt, links);
         const unsigned long long sc = __reduce_add_sync(0xffffffffu, (uint32_t)min(scanned, 0xFFFFFFFFull));
         if (lane == 0 && sc) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt->amsf_edges), sc);
     }
