@@ -1,6 +1,8 @@
 """Shared test helpers: fixture graphs (hand-built CSRs) and device transfer."""
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 
@@ -70,3 +72,26 @@ def to_dev(off, adj, device="cuda"):
 
 def u32(t):
     return t.detach().cpu().numpy().view(np.uint32)
+
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def golden_fixtures():
+    """tests/golden/*.txt: small graphs with paper-cited expected values.
+    Yields (name, off, adj, expect) with expect = {components, labels, forest_edges}."""
+    for fn in sorted(os.listdir(GOLDEN)):
+        if not fn.endswith(".txt"):
+            continue
+        kv = {}
+        for line in open(os.path.join(GOLDEN, fn)):
+            line = line.split("#", 1)[0].strip()
+            if line:
+                k, *vals = line.split()
+                kv[k] = [int(x) for x in vals]
+        n = kv["n"][0]
+        e = kv["edges"]
+        pairs = list(zip(e[0::2], e[1::2]))
+        off, adj = csr(n, pairs)
+        yield fn, off, adj, {"components": kv["components"][0], "labels": np.array(kv["labels"], dtype=np.uint32),
+                             "forest_edges": kv["forest_edges"][0]}

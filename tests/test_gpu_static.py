@@ -369,3 +369,27 @@ def test_adversarial_long_chains():
             got = run_labels(off, adj, **opt)
             assert time.time() - t0 < 5.0, opt
             assert np.array_equal(got, want), opt
+
+
+def test_golden_fixtures_gpu():
+    """tests/golden/ (paper-cited): cc_labels gives the fixed labels for every k / variant /
+    finish, cc_spanning_forest exactly n - c valid edges, and the incremental path inserting
+    the edges one batch at a time ends with the same labels."""
+    from tests.helpers import golden_fixtures
+    for name, off, adj, want in golden_fixtures():
+        n = off.size - 1
+        for opt in OPTION_GRID[:12]:
+            assert np.array_equal(run_labels(off, adj, **opt), want["labels"]), (name, opt)
+        d_off, d_adj = to_dev(off, adj)
+        edges, lab2 = pkg.spanning_forest(d_off, d_adj)
+        E = u32(edges).reshape(-1, 2)
+        assert E.shape[0] == want["forest_edges"], name
+        assert oracle.forest_check(off, adj, want["components"], E)[0] == 0, name
+        assert np.array_equal(u32(lab2), want["labels"]), name
+        src = np.repeat(np.arange(n), np.diff(off))
+        pairs = np.stack([src, adj.astype(np.int64)], 1)[src < adj].astype(np.int32)
+        inc = pkg.IncrementalCC(n)
+        for p in pairs:
+            inc.batch(torch.from_numpy(p.reshape(1, 2)).cuda(), torch.zeros((0, 2), dtype=torch.int32, device="cuda"))
+        assert np.array_equal(u32(inc.labels()), want["labels"]), name
+        inc.close()

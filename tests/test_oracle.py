@@ -388,3 +388,19 @@ def test_uniform_below_and_identify_frequent_pins():
     # a 60 % giant is the mode of 1024 samples for every seed (a 40 % rival would need > 512 hits)
     lab = np.where(np.arange(100000) % 5 < 3, 3, 8).astype(np.uint32)
     assert all(oracle.identify_frequent(lab, 1024, s) == 3 for s in range(50))
+
+
+def test_golden_fixtures():
+    """tests/golden/: the paper's worked graph (App. A.2.3) and a forest-size fixture, each
+    with the values the paper fixes for it (one component; n - c forest edges)."""
+    from tests.helpers import golden_fixtures
+    seen = 0
+    for name, off, adj, want in golden_fixtures():
+        n = off.size - 1
+        lab = oracle.cc_bfs(off, adj)
+        assert np.array_equal(lab, want["labels"]), name
+        assert int(np.sum(lab == np.arange(n))) == want["components"], name
+        assert np.array_equal(oracle.cc_dsu(off, adj), want["labels"]), name
+        assert n - want["components"] == want["forest_edges"], name
+        seen += 1
+    assert seen >= 2
