@@ -586,6 +586,7 @@ def run_ours(a, rank, ws):
 
 def run_ours_incr(a, rank, ws, cfg):
     """--config 5: 256 batches of (943,718 inserts, 104,858 queries) on n = 2^26."""
+    import numpy as np
     import torch
 
     from inputs import gpu as ggen
@@ -695,8 +696,10 @@ def run_ours_incr(a, rank, ws, cfg):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            for b in range(nb):
-                h.batch(h_ins[b], cfg.n_ins, h_qs[b], cfg.n_q, h_ans[b])
+            # the whole stream in one cc_incr_batches call: the library DMAs batch b+1's pairs
+            # while batch b computes (double-buffered), answers written to the host in place
+            h.batches(np.full(nb, cfg.n_ins, dtype=np.int64), h_ins, np.full(nb, cfg.n_q, dtype=np.int64), h_qs,
+                      h_ans, stream)
             e1.record(stream)
             e1.synchronize()
             h.close()
@@ -705,7 +708,9 @@ def run_ours_incr(a, rank, ws, cfg):
         line["e2e"] = {"value": round(ops / (e2e_ms * 1e-3) / 1e9, 4), "unit": "Gops/s",
                        "h2d_bytes_per_step": int(nb * 8 * (cfg.n_ins + cfg.n_q)), "d2h_bytes_per_step": int(nb * cfg.n_q),
                        "ms_per_step": round(e2e_ms, 3),
-                       "path": "cc_incr_batch with pinned host inserts/queries/answers (zero-copy through UVA)",
+                       "path": "one cc_incr_batches call over the 256 pinned host batches: pairs DMA'd double-buffered "
+                                       "on a copy stream (batch b+1 while batch b computes), answers written "
+                                       "to the host in place (UVA)",
                        "answers_match_device_path": bool(torch.equal(h_ans, ans.cpu()))}
         del h_ins, h_qs, h_ans
 

@@ -342,6 +342,76 @@ cc_status cc_incr_batch(cc_incr* h, const uint32_t* inserts, int64_t n_ins, cons
     return rc;
 }
 
+}  // extern "C"
+
+namespace ccb {
+// Double-buffered staging of pinned host batches (see cc_incr_batches).  The copy
+// stream waits for the compute stream to release a buffer (event `freed`), the
+// compute stream waits for its copy (event `ready`); only inserts / queries that
+// live in pinned host memory are staged.
+cc_status pipelined_batches(cc_incr* h, int64_t nb, const std::vector<int64_t>& oi, const std::vector<int64_t>& oq,
+                            const int64_t* ins_counts, const int64_t* q_counts, const uint32_t* ins, bool stage_i,
+                            const uint32_t* qs, bool stage_q, uint8_t* ans, cudaStream_t s)
+{
+    int64_t mi = 0, mq = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        mi = std::max(mi, ins_counts[b]);
+        mq = std::max(mq, q_counts[b]);
+    }
+    uint32_t* buf_i[2] = {nullptr, nullptr};
+    uint32_t* buf_q[2] = {nullptr, nullptr};
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ready[2] = {}, freed[2] = {};
+    cc_status rc = CC_OK;
+    auto body = [&]() -> cc_status {
+        CC_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        for (int k = 0; k < 2; ++k) {
+            if (stage_i && mi) CC_CUDA_TRY(scratch_alloc((void**)&buf_i[k], 8 * (size_t)mi, s));
+            if (stage_q && mq) CC_CUDA_TRY(scratch_alloc((void**)&buf_q[k], 8 * (size_t)mq, s));
+            CC_CUDA_TRY(cudaEventCreateWithFlags(&ready[k], cudaEventDisableTiming));
+            CC_CUDA_TRY(cudaEventCreateWithFlags(&freed[k], cudaEventDisableTiming));
+            CC_CUDA_TRY(cudaEventRecord(freed[k], s));   // buffers start free (after their allocation)
+        }
+        for (int64_t b = 0; b < nb; ++b) {
+            const int k = (int)(b & 1);
+            const uint32_t* pi = ins + 2 * oi[b];
+            const uint32_t* pq = qs + 2 * oq[b];
+            CC_CUDA_TRY(cudaStreamWaitEvent(cs, freed[k], 0));
+            if (stage_i && ins_counts[b]) {
+                CC_CUDA_TRY(cudaMemcpyAsync(buf_i[k], pi, 8 * (size_t)ins_counts[b], cudaMemcpyHostToDevice, cs));
+                pi = buf_i[k];
+            }
+            if (stage_q && q_counts[b]) {
+                CC_CUDA_TRY(cudaMemcpyAsync(buf_q[k], pq, 8 * (size_t)q_counts[b], cudaMemcpyHostToDevice, cs));
+                pq = buf_q[k];
+            }
+            CC_CUDA_TRY(cudaEventRecord(ready[k], cs));
+            CC_CUDA_TRY(cudaStreamWaitEvent(s, ready[k], 0));
+            cc_status r = insert_query(h, pi, ins_counts[b], pq, q_counts[b], ans + oq[b], s);
+            if (r) return r;
+            CC_CUDA_TRY(cudaEventRecord(freed[k], s));
+        }
+        return CC_OK;
+    };
+    rc = body();
+    // the staging buffers are stream-ordered on s (freed after the last kernel that reads
+    // them); the copy stream is idle once s has passed the last `ready` it waited on
+    for (int k = 0; k < 2; ++k) {
+        scratch_free(buf_i[k], s);
+        scratch_free(buf_q[k], s);
+    }
+    cudaStreamSynchronize(s);
+    for (int k = 0; k < 2; ++k) {
+        if (ready[k]) cudaEventDestroy(ready[k]);
+        if (freed[k]) cudaEventDestroy(freed[k]);
+    }
+    if (cs) cudaStreamDestroy(cs);
+    return rc;
+}
+}  // namespace ccb
+
+extern "C" {
+
 cc_status cc_incr_batches(cc_incr* h, int64_t nb, const int64_t* ins_counts, const uint32_t* inserts,
                           const int64_t* q_counts, const uint32_t* queries, uint8_t* answers, void* stream)
 {
@@ -425,8 +495,17 @@ cc_status cc_incr_batches(cc_incr* h, int64_t nb, const int64_t* ins_counts, con
     const uint32_t saved = h->flags;
     h->flags &= ~CC_FLAG_VALIDATE;                       // ids already checked above
     cc_status rc = CC_OK;
-    for (int64_t b = 0; b < nb && rc == CC_OK; ++b)
-        rc = insert_query(h, d_ins + 2 * oi[b], ins_counts[b], d_q + 2 * oq[b], q_counts[b], d_ans + oq[b], s);
+    if ((k_ins == MEM_PINNED || k_q == MEM_PINNED) && nb > 1) {
+        // Pinned host batches: DMA each batch's pairs into one of two device staging
+        // buffers on a copy stream while the previous batch computes (double buffering);
+        // read in place over PCIe by the kernels instead, every batch waited for its own
+        // pairs (C5: 40 GB/s effective).  Answers are still written to the host in place.
+        rc = pipelined_batches(h, nb, oi, oq, ins_counts, q_counts, d_ins, k_ins == MEM_PINNED, d_q,
+                               k_q == MEM_PINNED, d_ans, s);
+    } else {
+        for (int64_t b = 0; b < nb && rc == CC_OK; ++b)
+            rc = insert_query(h, d_ins + 2 * oi[b], ins_counts[b], d_q + 2 * oq[b], q_counts[b], d_ans + oq[b], s);
+    }
     h->flags = saved;
     if (rc == CC_OK && host) CC_CUDA_TRY(cudaStreamSynchronize(s));
     return rc;

@@ -223,3 +223,30 @@ def test_adversarial_chain_queries():
                              torch.from_numpy(np.ascontiguousarray(q).view(np.int32)).cuda()).cpu().numpy())
     assert np.array_equal(np.concatenate(got), want2)
     inc.close()
+
+
+@pytest.mark.parametrize("where", ["both_pinned", "ins_pinned", "q_pinned"])
+def test_multi_batch_pinned_pipelined(where):
+    """cc_incr_batches over pinned HOST batches (the double-buffered DMA staging path):
+    ragged batch sizes (incl. empty inserts / queries and batches above the single-CTA
+    threshold), answers written to pinned host memory -- bit-exact vs the oracle."""
+    n = 1 << 16
+    rng = np.random.default_rng(8)
+    sizes = [(20000, 3000), (0, 500), (9000, 0), (30000, 7000), (1, 1), (50000, 12000), (17, 9000)]
+    batches = []
+    for b, (ni, nq) in enumerate(sizes):
+        ins, qs = gen.incr_batch(seed=21, scale=16, b=b, n_ins=max(ni, 1), n_q=max(nq, 1))
+        batches.append((ins[:ni], qs[:nq]))
+    want, want_lab = oracle.incr_run(n, batches, want_labels=True)
+    ins_all = torch.from_numpy(np.concatenate([b[0] for b in batches]).astype(np.uint32).view(np.int32))
+    qs_all = torch.from_numpy(np.concatenate([b[1] for b in batches]).astype(np.uint32).view(np.int32))
+    ins_arg = ins_all.pin_memory() if where in ("both_pinned", "ins_pinned") else ins_all.cuda()
+    qs_arg = qs_all.pin_memory() if where in ("both_pinned", "q_pinned") else qs_all.cuda()
+    ans = torch.zeros(qs_all.shape[0], dtype=torch.uint8).pin_memory()
+    h = cc.Incr(n)
+    h.batches(np.array([s[0] for s in sizes]), ins_arg, np.array([s[1] for s in sizes]), qs_arg, ans)
+    lab = torch.empty(n, dtype=torch.int32, device="cuda")
+    h.labels(lab)
+    h.close()
+    assert np.array_equal(ans.numpy(), want)
+    assert np.array_equal(u32(lab), want_lab)
