@@ -272,7 +272,12 @@ cc_status cc_incr_batch(cc_incr* h, const uint32_t* inserts, int64_t n_ins,
  * every batch has at most 8192 operations the whole sequence runs in one
  * single-CTA kernel with a block barrier between each insert and query phase
  * (the paper's small-batch regime, Table 5); otherwise one launch
- * pair per batch.  Arrays may be device or pinned host memory.  Errors as
+ * pair per batch.  Arrays may be device, pinned host or pageable host memory:
+ * pinned host inserts / queries of larger batches are copied into two device
+ * staging buffers by DMA on an internal copy stream, batch b+1 while batch b
+ * computes (scratch: 2 x 8 B per pair of the largest batch); pinned answers
+ * are written in place; pageable arrays are staged batch by batch.  A call
+ * with host arrays returns after the work is complete.  Errors as
  * cc_incr_batch (with CC_FLAG_VALIDATE, all ids are checked first). */
 cc_status cc_incr_batches(cc_incr* h, int64_t nb, const int64_t* ins_counts, const uint32_t* inserts,
                           const int64_t* q_counts, const uint32_t* queries, uint8_t* answers, void* stream);
