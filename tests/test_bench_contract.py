@@ -1,0 +1,54 @@
+"""The bench.py JSON line contract, checked on the committed round measurements
+(profiles/r1_bench_*.json, written by bench.py on a B200): every key the driver
+and the tier contract require, with the right types and units."""
+import json
+import os
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PROF = os.path.join(ROOT, "profiles")
+
+
+def line(name):
+    path = os.path.join(PROF, name)
+    if not os.path.exists(path):
+        pytest.skip(f"{name} not committed")
+    return json.loads(open(path).read().strip().splitlines()[-1])
+
+
+@pytest.mark.parametrize("name", ["r1_bench_default.json", "r1_bench_c5.json"])
+def test_bench_line_keys(name):
+    d = line(name)
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["n_gpus"] >= 1 and d["steps"] >= 1 and d["warmup"] >= 3
+    assert d["higher_is_better"] is True and d["scaling"] == "weak" and d["vs_baseline"] is None
+    assert "workload" in d["config"] and "l2" in d["config"]
+    r = d["roofline"]
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in r, k
+    assert r["bound"] in ("hbm", "tensor", "alu") and r["unit"] in ("GB/s", "TFLOP/s")
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
+    e = d["e2e"]
+    for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
+        assert k in e, k
+    assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0 and e["value"] < d["value"]
+    assert d["gpu_launches"] > 0
+    c = d["clocks"]
+    assert c["sm_mhz"] > 0 and "reasons" in c
+    assert not {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"} & set(c["reasons"])
+
+
+def test_bench_cpu_baseline_and_reference_arm():
+    d = line("r1_bench_default.json")
+    cb = d["cpu_baseline"]
+    for k in ("value", "unit", "cores", "kind", "sample"):
+        assert k in cb, k
+    assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["unit"] == d["unit"]
+    r = line("r1_bench_reference.json")
+    assert r["impl"] == "reference" and r["unit"] == d["unit"] and r["metric"] == d["metric"]
+    assert r["cpu_baseline"]["kind"] == "oracle"
+    assert r["e2e"]["h2d_bytes_per_step"] == 0 and r["e2e"]["d2h_bytes_per_step"] == 0
+    assert r["e2e"]["value"] == r["value"]
