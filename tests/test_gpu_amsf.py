@@ -256,3 +256,33 @@ def test_amsf_self_loops_extreme_weights():
             E, W, tot = run(off, adj, w, eps, **opt)
             assert not np.any(E[:, 0] == E[:, 1])
             check(off, adj, w, eps, E, W, tot, want=want)
+
+
+def test_amsf_bucket_boundaries_exact():
+    """Weights placed exactly at the bucket boundaries: for b_i = W_min (1+eps)^i (fp64 chain,
+    reading R25) the smallest float >= b_i must land in bucket i and the float just below it in
+    bucket i-1 -- through the scanned lists, the warp-built index (lists of 257..4096) and the
+    CTA-built index (longer lists), whose float thresholds must decide as b_i <= (double)w."""
+    eps = 0.1
+    b = oracle.amsf_bounds(1.0, 50.0, eps)
+    vals = [np.float32(1.0)]
+    for bi in b[1:-1]:
+        f = np.float32(bi)
+        if float(f) < bi:
+            f = np.nextafter(f, np.float32(np.inf))
+        vals += [f, np.nextafter(f, np.float32(0))]
+    vals = np.array(vals, dtype=np.float32)
+    for leaves in (40, 1000, 6000):                      # scanned / warp index / CTA index
+        n = leaves + 1 + 2
+        rng = np.random.default_rng(leaves)
+        pairs = [(0, i) for i in range(1, leaves + 1)] + [(leaves + 1, leaves + 2)]
+        off, adj = oracle.csr_from_pairs(n, np.array(pairs))
+        wmap = {}
+        for u, v in pairs:
+            wmap[(u, v)] = wmap[(v, u)] = vals[rng.integers(0, vals.size)]
+        wmap[(leaves + 1, leaves + 2)] = wmap[(leaves + 2, leaves + 1)] = np.float32(1.0)   # W_min = 1
+        src = np.repeat(np.arange(n), np.diff(off))
+        w = np.array([wmap[(int(a), int(c))] for a, c in zip(src, adj)], dtype=np.float32)
+        want = oracle.amsf(off, adj, w, eps)
+        for opt in (OPTS[0], OPTS[6], OPTS[2]):
+            check(off, adj, w, eps, *run(off, adj, w, eps, **opt), want=want)
