@@ -250,3 +250,30 @@ def test_multi_batch_pinned_pipelined(where):
     h.close()
     assert np.array_equal(ans.numpy(), want)
     assert np.array_equal(u32(lab), want_lab)
+
+
+def test_multi_batch_pinned_validate():
+    """CC_FLAG_VALIDATE on the pinned multi-batch path: ids are checked before any batch
+    is staged or applied (an out-of-range id anywhere rejects the whole call)."""
+    n = 1 << 12
+    batches = [gen.incr_batch(seed=3, scale=12, b=b, n_ins=20000, n_q=500) for b in range(3)]
+    ins = np.concatenate([b[0] for b in batches]).astype(np.uint32)
+    qs = np.concatenate([b[1] for b in batches]).astype(np.uint32)
+    want, want_lab = oracle.incr_run(n, batches, want_labels=True)
+    ans = torch.zeros(qs.shape[0], dtype=torch.uint8).pin_memory()
+    h = cc.Incr(n, cc.FLAG_VALIDATE)
+    h.batches(np.full(3, 20000), torch.from_numpy(ins.view(np.int32)).pin_memory(), np.full(3, 500),
+              torch.from_numpy(qs.view(np.int32)).pin_memory(), ans)
+    assert np.array_equal(ans.numpy(), want)
+    bad = ins.copy()
+    bad[-1, 1] = n                                        # last insert of the last batch
+    lab0 = torch.empty(n, dtype=torch.int32, device="cuda")
+    h.labels(lab0)
+    with pytest.raises(cc.CCError):
+        h.batches(np.full(3, 20000), torch.from_numpy(bad.view(np.int32)).pin_memory(), np.full(3, 500),
+                  torch.from_numpy(qs.view(np.int32)).pin_memory(), ans)
+    lab1 = torch.empty(n, dtype=torch.int32, device="cuda")
+    h.labels(lab1)
+    h.close()
+    assert torch.equal(lab0, lab1)                        # nothing applied
+    assert np.array_equal(u32(lab0), want_lab)
