@@ -30,3 +30,12 @@ clean:
 	rm -rf build paper_2008_03909_b200/libcc.so inputs/libccgen.so oracle/liboracle.so
 
 .PHONY: all clean
+
+# measurement probes (not product code; binaries are git-ignored, built on demand)
+probes: scripts/probe/randgather scripts/probe/zerocopy scripts/probe/incr_latency
+scripts/probe/incr_latency: scripts/probe/incr_latency.cu paper_2008_03909_b200/libcc.so
+	$(NVCC) $(ARCH) -O3 --cudart shared $< -o $@ -Lpaper_2008_03909_b200 -lcc -Xlinker -rpath=$(CURDIR)/paper_2008_03909_b200
+scripts/probe/%: scripts/probe/%.cu
+	$(NVCC) $(ARCH) -O3 --cudart shared $< -o $@
+
+.PHONY: probes

@@ -151,11 +151,13 @@ def peaks():
         return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(kernel: str):
-    """dram read+write bytes per launch from a committed `ncu --set full` capture, if any."""
+def ncu_traffic(workload: str, kernel: str):
+    """dram read+write bytes per launch of `kernel` from a committed `ncu --set full`
+    capture of THIS workload (profiles/ncu_traffic.json is keyed by workload, then by
+    bench mark name); None when no capture of this workload / kernel exists."""
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        return d.get(kernel)
+        return d.get(workload, {}).get(kernel)
     except Exception:
         return None
 
@@ -211,17 +213,22 @@ def run_reference(a, rank, ws):
 
 
 # ---------------------------------------------------------------------------
-def byte_model(off_h_deg_pos, n, m, k, ctr, sampled, final, mid_ran, f0=None):
-    """Algorithmic bytes per launch of each kernel.
+def byte_model(off_h_deg_pos, n, m, k, ctr, sampled, final, mid_ran, f0=None, partial_h6=True):
+    """Algorithmic bytes per launch of each kernel, SURVEY §8(d).
 
-    Counts only what the implemented design must move (SURVEY §8(d) honesty
-    rules): 4 B per uint32 read/written, 8 B per int64 offset.  f0 = (F0
-    non-roots, F0 vertices at depth >= 2) selects the contracted-link model."""
+    Counts only what the implemented design must move (§8(d) honesty rule 1):
+    4 B per uint32 read/written, 8 B per int64 offset.  First-level parent reads
+    of a traversed edge (P[v]) are counted; root checks and walks beyond the
+    first parent level (P[P[v]], k_finish's and H6's `*_gathers`) are NOT (§8(d):
+    "Path-walk reads beyond the first level ... are not counted").  f0 = (F0
+    non-roots, F0 vertices at depth >= 2) selects the contracted-link model;
+    partial_h6 selects the partial final compress (k_relabel) over the full pass."""
     import numpy as np
     npos, sum_mink = off_h_deg_pos
     pend = ctr["pending_links"]
     fin_v, fin_e = ctr["finish_vertices"], ctr["finish_edges"]
-    relab = int(np.count_nonzero(final != sampled))          # H6 label writes
+    ntiles = (n + 2047) // 2048
+    relab = int(np.count_nonzero(final != sampled))          # labels that differ from the sampled ones
     nonroot = int(np.count_nonzero(sampled != np.arange(n, dtype=np.uint32)))
     B = {
         # offsets (n+1) + first-k adj entries + P write + pending writes + finish bitmap
@@ -232,15 +239,17 @@ def byte_model(off_h_deg_pos, n, m, k, ctr, sampled, final, mid_ran, f0=None):
         # pending read + P[u], P[v] gathers + hook CAS
         "k_link_pending": 8 * pend + 8 * pend + 4 * ctr["sample_hooks"],
         "k_identify": 4 * 1024,
-        # fused H3 + H5 scan: P read + bitmap + first-level parent reads + compress writes
-        # + candidate queue writes
-        "k_finish": 4 * n + n // 8 + 4 * ctr["finish_gathers"] + 4 * ctr["compress_writes"] + 4 * fin_v,
-        # H5 edge work: queue read + offsets pair + adj + P[v] gather per edge + hook CAS
-        "k_finish_proc": 4 * fin_v + 16 * fin_v + 8 * fin_e + 4 * ctr["finish_hooks"],
-        # P read + first-level parent reads (the root check P[P[v]] of every non-root slot:
-        # reads the method makes; they land on the few root slots, i.e. mostly L2 hits, so
-        # this kernel's algorithmic rate can exceed the DRAM peak) + changed-label writes
-        "k_compress_H6": 4 * n + 4 * ctr["h6_gathers"] + 4 * ctr["h6_writes"],
+        # fused H3 + H5 scan (B_fin's "4n skip-test read"): P read + degree bitmap (replaces the
+        # 8 N_off offsets reads, §8(d) rule 1) + H3 label writes + candidate queue writes +
+        # the tile summaries of the partial H6 (16 B + a 1 B hook flag per 2048-slot tile)
+        "k_finish": 4 * n + n // 8 + 4 * ctr["compress_writes"] + 4 * fin_v + 17 * ntiles,
+        # H5 edge work: queue read + offsets pair + P[u] per candidate, adj + first-level P[v]
+        # per traversed edge (B_fin's 8 E_ng) + hook CAS (4 H)
+        "k_finish_proc": 4 * fin_v + 16 * fin_v + 4 * fin_v + 8 * fin_e + 4 * ctr["finish_hooks"],
+        # H6: partial -- tile summaries + flags read, every slot of a dirty tile re-read,
+        # changed labels written; full -- B_fin's "4n compress read" + changed labels
+        "k_compress_H6": (17 * ntiles + 8192 * ctr.get("h6_tiles", 0) + 4 * ctr["h6_writes"]) if partial_h6
+                         else 4 * n + 4 * ctr["h6_writes"],
     }
     if f0 is not None:
         # contracted link: + the F0-root bitmap words in k_sample_init;
@@ -256,7 +265,7 @@ def byte_model(off_h_deg_pos, n, m, k, ctr, sampled, final, mid_ran, f0=None):
         B["k_sample_init"] += n // 8
         B["k_compress_mid"] = 3 * (n // 8) + 8 * R + 4 * n + 4 * f0_nonroots + 4 * f0_deep
         B["k_link_pending"] = 16 * pend + 8 * R
-        B["k_finish"] = 4 * n + n // 8 + 12 * ctr["finish_gathers"] + 4 * ctr["compress_writes"] + 4 * fin_v
+        B["k_finish"] = 4 * n + n // 8 + 12 * ctr["finish_gathers"] + 4 * ctr["compress_writes"] + 4 * fin_v + 17 * ntiles
     if ctr.get("fused_link"):
         # k_sample_link (DESIGN.md §6 item 1b): P initialised first (4n write), offsets + first-k
         # adj entries, the round-0 CAS on P[u] (4n read), finish bitmap, and the links queued in
@@ -266,7 +275,14 @@ def byte_model(off_h_deg_pos, n, m, k, ctr, sampled, final, mid_ran, f0=None):
         B["k_link_pending"] = 0
     B["finish_phase"] = B["k_finish"] + B["k_finish_proc"] + B["k_compress_H6"]
     B["sampling_phase"] = B["k_sample_init"] + B["k_compress_mid"] + B["k_link_pending"]
-    return B, {"relabelled": relab, "sampled_nonroots": nonroot, "mid_nonroots_bound": npos}
+    terms = {"4n_skip_test_read": 4 * n, "bitmap_for_8N_off": n // 8, "8E_ng": 8 * fin_e,
+             "candidates_queue_offsets_Pu": 28 * fin_v,
+             "4W_label_writes": 4 * (ctr["compress_writes"] + ctr["h6_writes"]), "4H_hooks": 4 * ctr["finish_hooks"],
+             "4n_compress_read": 0 if partial_h6 else 4 * n,
+             "tile_summaries": 34 * ntiles if partial_h6 else 0,
+             "dirty_tile_rereads": 8192 * ctr.get("h6_tiles", 0) if partial_h6 else 0}
+    return B, {"relabelled": relab, "sampled_nonroots": nonroot, "mid_nonroots_bound": npos, "B_fin_terms": terms,
+               "root_check_reads_not_counted": int(ctr["finish_gathers"] + ctr["h6_gathers"])}
 
 
 def floors(cc, d_off, d_adj, n, m, x, stream, cc_ms, reps=3):
@@ -359,7 +375,9 @@ def run_ours(a, rank, ws):
             del p0
         del ids
         mid_ran = True
-    B, extra = byte_model((nonisolated, sum_mink), n, m, a.k, ctr, sampled, final, mid_ran, f0)
+    # the partial final compress runs unless an SV / CRFA finish is selected (cc_static.cu run())
+    partial_h6 = not (a.flags & (cc.FLAG_FINISH_SV | cc.FLAG_FINISH_CRFA))
+    B, extra = byte_model((nonisolated, sum_mink), n, m, a.k, ctr, sampled, final, mid_ran, f0, partial_h6)
     extra["mid_compress_ran"] = mid_ran
     extra["contracted_link"] = contract
     if f0 is not None:
@@ -400,6 +418,9 @@ def run_ours(a, rank, ws):
         kern_ms[cc.MARK_NAMES[j]] = statistics.mean(marks[i][j - 1].elapsed_time(marks[i][j]) for i in range(a.steps))
     mean_ms = statistics.mean(step_ms)
     max_ms = reduce_max(mean_ms, ws)
+    srt = sorted(step_ms)
+    t_stats = {"mean": round(mean_ms, 5), "median": round(statistics.median(step_ms), 5), "min": round(srt[0], 5),
+               "p90": round(srt[min(len(srt) - 1, int(0.9 * len(srt)))], 5), "max": round(srt[-1], 5)}
     value = aggregate_value(m, max_ms * 1e-3, ws) / 1e9
 
     peak, peak_src = peaks()
@@ -414,21 +435,46 @@ def run_ours(a, rank, ws):
     dom = max(kernels, key=lambda k: kernels[k]["ms"])
     dk = kernels[dom]
     roofline = {"bound": "hbm", "kernel": dom, "achieved": dk["GB/s"], "peak": peak, "unit": "GB/s",
-                "frac": dk["frac"], "traffic": ncu_traffic(dom), "peak_source": peak_src,
+                "frac": dk["frac"], "traffic": ncu_traffic(cfg.name, dom), "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": dk["bytes"], "launch_ms": dk["ms"]}
     fin_ms = kern_ms["k_finish"] + kern_ms["k_finish_proc"] + kern_ms["k_compress_H6"]
     fin_gbs = B["finish_phase"] / (fin_ms * 1e-3) / 1e9
     smp_ms = sum(kern_ms[x] for x in ("k_sample_init", "k_compress_mid", "k_link_pending"))
+    t_fin_ms = [sum(marks[i][j - 1].elapsed_time(marks[i][j]) for j in (6, 7, 8)) for i in range(a.steps)]
     finish = {"scope": "H3 compress fused with the H5 scan (k_finish) + H5 edge work (k_finish_proc, "
-                       "k_finish_big) + H6 (k_compress_H6)", "ms": round(fin_ms, 5), "bytes": int(B["finish_phase"]), "GB/s": round(fin_gbs, 1),
+                       "k_finish_big) + H6 (" + ("partial: k_relabel" if partial_h6 else "full: k_compress") + ")",
+              "t_fin_ms": round(fin_ms, 5), "ms": round(fin_ms, 5),
+              "t_fin_ms_stats": {"median": round(statistics.median(t_fin_ms), 5), "min": round(min(t_fin_ms), 5),
+                                 "p90": round(sorted(t_fin_ms)[min(len(t_fin_ms) - 1, int(0.9 * len(t_fin_ms)))], 5)},
+              "bytes": int(B["finish_phase"]), "GB/s": round(fin_gbs, 1),
               "frac_of_8TBs": round(fin_gbs / CONTRACT_GBS, 4), "frac_of_measured": round(fin_gbs / peak, 4),
-              "bytes_note": "algorithmic: every P read the method makes (first-level parent reads 4 B each, "
-                            "cache hits included) + writes; see dram_view for the ncu DRAM traffic"}
-    dram = [ncu_traffic(k) for k in ("k_finish", "k_finish_proc", "k_finish_big", "k_compress_H6")]
+              "byte_model": "SURVEY 8(d) B_fin of the implemented design: 4n skip-test read + n/8 degree bitmap "
+                            "(for 8 N_off) + 8 E_ng + candidates (queue, offsets, P[u]) + 4 W + 4 H + "
+                            + ("the partial H6's tile summaries and dirty-tile re-reads (no 4n compress read)"
+                               if partial_h6 else "4n compress read")
+                            + "; root checks beyond the first parent level are not counted",
+              "terms": extra["B_fin_terms"], "h6_mode": "partial" if partial_h6 else "full",
+              "h6_dirty_tiles": int(ctr.get("h6_tiles", 0)), "tiles": (n + 2047) // 2048,
+              "root_check_reads_not_counted": extra["root_check_reads_not_counted"]}
+    if partial_h6:
+        # the same t_fin against the 8(d) budget of a finish whose H6 reads all of P (4n more):
+        # what a full-compress design would have to sustain to finish as fast (context only)
+        full_b = B["finish_phase"] - B["k_compress_H6"] + 4 * n + 4 * ctr["h6_writes"]
+        finish["full_compress_budget_view"] = {
+            "bytes": int(full_b), "frac_of_8TBs_at_this_t_fin": round(full_b / (fin_ms * 1e-3) / 1e9 / CONTRACT_GBS, 4),
+            "note": "8(d)'s B_fin with the 4n compress read of a full final compress, over this t_fin; the partial "
+                    "H6 does not move those bytes (context, not the headline fraction)"}
+    dram = [ncu_traffic(cfg.name, k) for k in ("k_finish", "k_finish_proc", "k_finish_big", "k_compress_H6")]
     if all(x is not None for x in dram):
         finish["dram_view"] = {"dram_bytes": int(sum(dram)), "GB/s": round(sum(dram) / (fin_ms * 1e-3) / 1e9, 1),
                                "frac_of_8TBs": round(sum(dram) / (fin_ms * 1e-3) / 1e9 / CONTRACT_GBS, 4),
-                               "source": "profiles/ncu_traffic.json (ncu --set full, cold cache, per launch)"}
+                               "dram_over_B_fin": round(sum(dram) / max(1, B["finish_phase"]), 3),
+                               "source": f"profiles/ncu_traffic.json[{cfg.name}] (ncu --set full, cold cache, per launch)"}
+    else:
+        finish["dram_view"] = None
+    phase_ms = {"sample": round(smp_ms, 5), "identify": round(kern_ms["k_identify"], 5),
+                "finish": round(kern_ms["k_finish"] + kern_ms["k_finish_proc"], 5),
+                "compress": round(kern_ms["k_compress_H6"], 5)}
     sampling = {"ms": round(smp_ms, 5), "bytes": int(B["sampling_phase"]),
                 "GB/s": round(B["sampling_phase"] / (smp_ms * 1e-3) / 1e9, 1)}
 
@@ -442,6 +488,7 @@ def run_ours(a, rank, ws):
                              f"CSR {(8 * (n + 1) + 4 * m) / 1e9:.1f} GB > L2",
                        "parallelism": f"replicas x{ws}", "gen_s": round(gen_s, 2),
                        "l2_fetch_granularity": a.l2_fetch if a.l2_fetch >= 0 else "driver default"},
+            "t_ms": t_stats, "phase_ms": phase_ms,
             "roofline": roofline, "finish": finish, "sampling": sampling, "kernels": kernels,
             "counters": ctr, "byte_model_extra": extra, "gpu_launches": int(launches), "clocks": clocks}
 
@@ -558,13 +605,38 @@ def run_ours(a, rank, ws):
                        "ms_per_step": round(e2e_ms, 3), "steps": a.e2e_steps, "labels_match_device_path": ok}
         del h_off, h_adj, h_lab
 
-    # ---- cpu_baseline: the oracle on the host cores (rank 0, N = 1 only)
+    # ---- cpu_baseline: the oracle on the host cores (rank 0, N = 1 only).  (1) oracle.cc_bfs on
+    # the reported graph itself, in this run (one run for C4, median of 3 for
+    # the smaller configs), its labels compared with the GPU's; (2) the RMAT-24 sample the
+    # reference arm times, as a secondary number.
     if not a.no_cpu_baseline and rank == 0 and ws == 1:
         del flush
         torch.cuda.empty_cache()
+        import oracle as _oracle
+        need = 8 * (n + 1) + 4 * m + 16 * n          # host CSR copy + labels + BFS queue + GPU labels
+        try:
+            import psutil
+            avail = psutil.virtual_memory().available
+        except Exception:
+            avail = None
+        full = None
+        if avail is None or need * 1.2 < avail:
+            off_h = d_off.cpu().numpy()
+            adj_h = d_adj.cpu().numpy().view(np.uint32)
+            reps = 1 if m > 1e9 else 3
+            ts = []
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                lab_h = _oracle.cc_bfs(off_h, adj_h)
+                ts.append(time.perf_counter() - t0)
+            dt_full = statistics.median(ts)
+            full = {"value": round(m / dt_full / 1e9, 5), "unit": "GTEPS", "cores": 1, "kind": "oracle",
+                    "sample": f"oracle.cc_bfs (sequential BFS, 1 thread) on the reported workload itself "
+                              f"({cfg.name}, n={n}, m={m}), median of {reps} run(s): {dt_full:.2f} s",
+                    "seconds": round(dt_full, 3), "gpu_labels_bit_exact": bool(np.array_equal(lab_h, final))}
+            del off_h, adj_h, lab_h
         m_s, dt, off_s, adj_s, lab_s = cpu_oracle_sample(a.cpu_scale, True)
         reps, spent = 1, dt
-        import oracle as _oracle
         while spent < CPU_BASELINE_MIN_S and reps < 5:
             t0 = time.perf_counter()
             _oracle.cc_bfs(off_s, adj_s)
@@ -576,10 +648,16 @@ def run_ours(a, rank, ws):
         sl = torch.empty(off_s.size - 1, dtype=torch.int32, device=dev)
         cc.cc_labels(so, sa, off_s.size - 1, adj_s.size, sl, cc.make_opts(k=a.k, variant=variant, flags=a.flags))
         par = bool(np.array_equal(sl.cpu().numpy().view(np.uint32), lab_s))
-        line["cpu_baseline"] = {"value": round(m_s / dt / 1e9, 5), "unit": "GTEPS", "cores": 1, "kind": "oracle",
-                                "sample": f"oracle.cc_bfs (sequential BFS, 1 thread) on RMAT scale {a.cpu_scale} "
-                                          f"(C4 recipe, seed 4), m={m_s}; mean of {reps} runs, {dt:.2f} s each",
-                                "host_cores": os.cpu_count(), "gpu_labels_bit_exact_on_sample": par}
+        sample = {"value": round(m_s / dt / 1e9, 5), "unit": "GTEPS", "cores": 1, "kind": "oracle",
+                  "sample": f"oracle.cc_bfs (sequential BFS, 1 thread) on RMAT scale {a.cpu_scale} "
+                            f"(C4 recipe, seed 4), m={m_s}; mean of {reps} runs, {dt:.2f} s each",
+                  "gpu_labels_bit_exact_on_sample": par}
+        if full is not None:
+            line["cpu_baseline"] = dict(full, host_cores=os.cpu_count(), secondary_sample=sample)
+        else:
+            line["cpu_baseline"] = dict(sample, host_cores=os.cpu_count(),
+                                        full_workload_skipped=f"host RAM: need {need / 1e9:.1f} GB, "
+                                                              f"available {avail / 1e9:.1f} GB")
     if rank == 0:
         print(json.dumps(line), flush=True)
 

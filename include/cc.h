@@ -113,6 +113,9 @@ typedef int cc_status;
                                           vertex in every round, as AMSF-NF-S is stated
                                           (P:1819-1822), instead of consulting the per-
                                           vertex [min, max] weight index first          */
+#define CC_FLAG_INSERT1     (1u << 17) /* cc_incr: one insert / query per thread (the round-1
+                                          kernels) instead of 4 with their first parent
+                                          reads issued together                            */
 #define CC_FLAG_WAIT_FREE   (1u << 8)  /* cc_incr: the wait-free type (1) setting (P:973-977,
                                           P:2663-2682): a batch's inserts and queries run
                                           concurrently in ONE kernel.  Answers are then
@@ -157,6 +160,9 @@ typedef struct {
     uint64_t amsf_rebuilds;    /* cc_amsf: rounds whose L_max left the skipped component*/
     uint64_t fused_link;       /* 1 if the k-out links ran inside k_sample_link         */
     uint64_t amsf_links;       /* cc_amsf: in-bucket edges linked (diagnostics build only)*/
+    uint64_t h6_tiles;         /* tiles of kCTile = 2048 slots the partial final compress
+                                  re-resolved (dirty: a root they hold or name was
+                                  hooked by H5, L_max was hooked, or > 3 foreign roots)*/
 } cc_counters;
 
 typedef struct {
@@ -295,9 +301,13 @@ uint32_t cc_incr_num_vertices(const cc_incr* h);
 const char* cc_status_str(cc_status s);
 const char* cc_last_error(void);
 
-/* Upper bound of the transient device scratch a call allocates (informational).
- * op: 0 = cc_labels, 1 = cc_spanning_forest, 2 = cc_incr_create, 3 = cc_amsf
- * (eps = 0.25-like bucket counts). */
+/* Transient device scratch a call allocates (informational; no GPU access).
+ * op 0 = cc_labels, 1 = cc_spanning_forest: an upper bound -- the sum of every
+ * allocation any flag combination makes (pending links, queues, bitmaps, tile
+ * summaries, the parent array and staging buffers used with host arguments,
+ * the contracted-link arrays, the SV / CRFA edge lists; forest slots for op 1).
+ * op 2 = cc_incr_create: the handle's parent array.  op 3 = cc_amsf: an
+ * ESTIMATE sized for eps = 0.25-like bucket counts. */
 size_t cc_workspace_bytes(uint32_t n, int64_t m, uint32_t kout_k, int op);
 
 /* Library version string. */

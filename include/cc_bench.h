@@ -48,6 +48,13 @@ cc_status cc_bench_set_l2_fetch(int bytes, int* prev);
  * (bench evidence for "gpu_launches"; host-side counter, no GPU access). */
 uint64_t cc_bench_launch_count(void);
 
+/* Test hook: launch every grid-strided ("persistent") kernel of libcc.so with
+ * exactly `blocks` blocks (0 = the default multiple of the SM count); returns
+ * the previous setting.  Process-wide, not thread-safe against concurrent
+ * calls.  Results never depend on it (repeats with random launch
+ * configurations); the tile-per-block streaming kernels keep their grids. */
+unsigned cc_bench_set_grid(unsigned blocks);
+
 #ifdef __cplusplus
 }
 #endif

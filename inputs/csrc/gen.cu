@@ -2,7 +2,7 @@
 //
 // NOT part of the method: this builds the synthetic graphs/streams that stand
 // in for the paper's datasets, bit-identical to inputs/gen.py (numpy) for the
-// same seed (tests/test_gen_gpu.py checks byte equality).  Every draw is
+// same seed (tests/test_gpu_gen.py checks byte equality).  Every draw is
 //     mix(seed, stream, i) = splitmix64(seed*GOLD + stream*2^40 + i)  (mod 2^64)
 // so the output is independent of the launch configuration.
 //

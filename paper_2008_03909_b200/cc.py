@@ -38,6 +38,7 @@ FLAG_FINISH_CRFA = 1 << 13
 FLAG_AMSF_NO_INDEX = 1 << 14
 FLAG_FUSED_LINK = 1 << 16
 FLAG_FIND_NAIVE = 1 << 15
+FLAG_INSERT1 = 1 << 17
 
 # every symbol include/cc.h and include/cc_bench.h declare
 EXPORTS = [
@@ -46,7 +47,7 @@ EXPORTS = [
     "cc_amsf",
     "cc_workspace_bytes", "cc_version",
     "cc_bench_map_edges", "cc_bench_gather_edges", "cc_bench_random_gather", "cc_bench_copy",
-    "cc_bench_launch_count", "cc_bench_set_l2_fetch",
+    "cc_bench_launch_count", "cc_bench_set_l2_fetch", "cc_bench_set_grid",
 ]
 
 
@@ -62,7 +63,7 @@ COUNTER_FIELDS = ["pending_links", "worklist", "finish_vertices", "finish_edges"
                   "big_vertices", "compress_writes",
                   "link_steps", "cas_failures", "probe_deep", "finish_gathers", "h6_writes", "h6_gathers",
                   "sv_rounds", "contract_roots", "amsf_rounds", "amsf_visits", "amsf_edges", "amsf_hooks",
-                  "amsf_rebuilds", "fused_link", "amsf_links"]
+                  "amsf_rebuilds", "fused_link", "amsf_links", "h6_tiles"]
 
 
 class Opts(ctypes.Structure):
@@ -116,8 +117,11 @@ def load() -> ctypes.CDLL:
         "cc_bench_copy": (ctypes.c_int, [P, P, U64, P]),
         "cc_bench_launch_count": (U64, []),
         "cc_bench_set_l2_fetch": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
+        "cc_bench_set_grid": (ctypes.c_uint, [ctypes.c_uint]),
     }
     for name, (res, args) in sig.items():
+        if os.environ.get("CC_LIBCC_PATH") and not hasattr(lib, name):
+            continue                    # an older A/B build may lack a newer bench-only symbol
         f = getattr(lib, name)
         f.restype = res
         f.argtypes = args
@@ -245,6 +249,11 @@ def set_l2_fetch(nbytes: int) -> int:
     prev = ctypes.c_int()
     _check(load().cc_bench_set_l2_fetch(nbytes, ctypes.byref(prev)), "set_l2_fetch")
     return prev.value
+
+
+def set_grid(blocks: int) -> int:
+    """Test hook: grid-strided kernels launch exactly `blocks` blocks (0 = default)."""
+    return int(load().cc_bench_set_grid(blocks))
 
 
 def launch_count() -> int:

@@ -40,6 +40,42 @@ int num_sms()
     return cached[dev];
 }
 
+// Test hook (cc_bench_set_grid): when non-zero, every grid-strided
+// ("persistent") kernel launches exactly this many blocks instead of a
+// multiple of the SM count.  Results must not depend on it.
+std::atomic<unsigned> g_grid_override{0};
+
+unsigned grid_blocks(unsigned per_sm)
+{
+    const unsigned o = g_grid_override.load(std::memory_order_relaxed);
+    return o ? o : (unsigned)num_sms() * per_sm;
+}
+
+unsigned resident_blocks(const void* kernel, int block)
+{
+    const unsigned o = g_grid_override.load(std::memory_order_relaxed);
+    if (o) return o;
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<const void*, int>, int>> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const std::pair<const void*, int> key{kernel, block * 64 + dev};
+    {
+        std::lock_guard<std::mutex> g(mu);
+        for (auto& e : cache)
+            if (e.first == key) return (unsigned)e.second;
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0) != cudaSuccess || per_sm < 1) {
+        cudaGetLastError();
+        per_sm = 1;
+    }
+    const int g = per_sm * num_sms();
+    std::lock_guard<std::mutex> lk(mu);
+    cache.push_back({key, g});
+    return (unsigned)g;
+}
+
 bool is_device_ptr(const void* p)
 {
     if (!p) return true;                   // NULL: nothing to stage
@@ -173,17 +209,33 @@ const char* cc_version(void) { return "cc-b200 0.1 (sm_100a)"; }
 
 size_t cc_workspace_bytes(uint32_t n, int64_t m, uint32_t kout_k, int op)
 {
-    const size_t N = n, M = m < 0 ? 0 : (size_t)m;
-    if (op == 2) return 4 * N;
+    const size_t N = n, M = m < 0 ? 0 : (size_t)m, K = kout_k;
+    const size_t nw = (N + 31) / 32, ntile = (N + 2047) / 2048, nfb = (N + 4095) / 4096;
+    if (op == 2) return 64 + 4 * N;                             // the handle's parent array + flags
     if (op == 3) {
-        // cc_amsf: P, weight range x2, activation bucket, order, 2 carry lists, index ids (4 B each),
-        // forest slots (8 B) + weights (4 B), long-list pieces, the bucket index (<= 4 B per
-        // entry + per-list starts, bounded for eps = 0.25 by 128 buckets), bucket starts
+        // cc_amsf (an ESTIMATE: the bucket count depends on eps and the weight range; sized for
+        // eps = 0.25-like counts): P, weight range x2, activation bucket, order, 2 carry lists,
+        // index ids (4 B each), forest slots (8 B) + weights (4 B), long-list pieces, the bucket
+        // index (<= 4 B per entry + per-list starts, 128 buckets), bucket starts; plus the
+        // staging of pageable host inputs
         return 64 + 4 * N * 8 + 12 * N + 8 * (M / 2048 + std::min<size_t>(N, M / 2048 + 1) + 1) + 4 * M +
-               4 * 129 * (M / 257 + 1) + 16 * (M / 257 + 1) + 8 * 4096;
+               4 * 129 * (M / 257 + 1) + 16 * (M / 257 + 1) + 8 * 4096 + (8 * (N + 1) + 8 * M + 12 * N + 24);
     }
-    size_t b = 64 + 4 * N /*worklist*/ + 8 * std::min(N * kout_k, std::max(M, N) * kout_k) + 4 * (M / 4096 + 1);
-    if (op == 1) b += 8 * N + 4 * N + 12 * (N / 4096 + 1);
+    // cc_labels / cc_spanning_forest: an UPPER BOUND, the sum over every flag combination's
+    // allocations (cc_static.cu run(), cc_abi.cu staging):
+    size_t b = 64                                   // control block
+               + 4 * nw                             // finish bitmap
+               + 4 * N                              // finish candidate queue
+               + 8 * K * std::min(N, M)             // pending sampled links
+               + 4 * std::min(N, M / 4096 + 1)      // big-list queue
+               + 65 * ntile                         // warp summaries (8 x 8 B) + hook flag per tile
+               + 4 * N                              // parent array when labels are not device memory
+               + 8 * (N + 1) + 4 * M + 4 * N        // staging of pageable offsets / adjacency / labels
+               + 8 * nw + 8 * std::min(N, M) + 12 * (nw / 4096 + 1) + 8     // CC_FLAG_CONTRACT
+               + 4 * N + 8 * (N / 4096 + 1) + 8 + 8 * M + 4 * nw + 4        // FINISH_SV / CRFA edge list
+               + 2 * (op == 1 ? 16 : 8) * M + 16;                           // CRFA's two edge buffers
+    if (op == 1) b += 8 * N + 12 * nfb             // forest slots + Filter status words
+                      + 8 * N + 8;                  // staging of pageable edges / num_edges
     return b;
 }
 

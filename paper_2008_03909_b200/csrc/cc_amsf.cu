@@ -957,8 +957,19 @@ __global__ void __launch_bounds__(kBlock) k_amsf_chunks(const int64_t* __restric
             for (int64_t q0 = (b >> 2) + lane; q0 * 4 < e; q0 += 32 * 4) {
                 float4 wq[4];
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    wq[j] = (q0 + 32 * j) * 4 < e ? w4[q0 + 32 * j] : make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int j = 0; j < 4; ++j) {
+                    const int64_t x0 = (q0 + 32 * j) * 4;
+                    // the whole quad only when it ends inside the piece (e <= m, so never past
+                    // the end of w); a quad straddling e takes its entries below e one by one
+                    if (x0 + 4 <= e) {
+                        wq[j] = w4[q0 + 32 * j];
+                    } else {
+                        wq[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                        if (x0 < e) wq[j].x = w[x0];
+                        if (x0 + 1 < e) wq[j].y = w[x0 + 1];
+                        if (x0 + 2 < e) wq[j].z = w[x0 + 2];
+                    }
+                }
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const float v4[4] = {wq[j].x, wq[j].y, wq[j].z, wq[j].w};
@@ -1024,7 +1035,6 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
                    uint32_t* edges, float* edge_w, int64_t* num_edges, double* total, const cc_opts& o,
                    cudaStream_t s)
 {
-    const int sms = num_sms();
     const bool skip = !(o.flags & CC_FLAG_NO_SKIP);
     const bool plain = (o.flags & CC_FLAG_AMSF_PLAIN) != 0;
     bool index = false;                       // hub bucket index (set once nb is known)
@@ -1060,10 +1070,10 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
         CC_CUDA_TRY(cudaMemcpyAsync(ac, &h0, sizeof(h0), cudaMemcpyHostToDevice, s));
         const uint64_t ntiles = (uint64_t)((m + kWrTile - 1) / kWrTile);
         if (m > 0) CC_CUDA_TRY(scratch_alloc((void**)&tile_vs, sizeof(uint32_t) * ntiles, s));
-        k_amsf_init<<<sms * 8, kBlock, 0, s>>>(off, P, vi, F, n, m > 0 ? tile_vs : nullptr);
+        k_amsf_init<<<grid_blocks(8), kBlock, 0, s>>>(off, P, vi, F, n, m > 0 ? tile_vs : nullptr);
         CC_LAUNCH_CHECK("k_amsf_init");
         if (m > 0) {
-            k_amsf_wrange<<<sms * 16, kBlock, 0, s>>>(off, w, n, m, tile_vs, vi, ac);
+            k_amsf_wrange<<<grid_blocks(16), kBlock, 0, s>>>(off, w, n, m, tile_vs, vi, ac);
             CC_LAUNCH_CHECK("k_amsf_wrange");
         }
         AmsfCtl h{};
@@ -1116,12 +1126,12 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
             CC_CUDA_TRY(scratch_alloc((void**)&cursor, sizeof(unsigned long long) * (nb + 1), s));
             CC_CUDA_TRY(cudaMemsetAsync(start, 0, sizeof(unsigned long long) * (nb + 1), s));
             // activation order: non-isolated vertices by the bucket of their lightest edge
-            k_amsf_first<<<sms * 8, kBlock, 0, s>>>(vi, n, bd, nb, plain, fb, start);
+            k_amsf_first<<<grid_blocks(8), kBlock, 0, s>>>(vi, n, bd, nb, plain, fb, start);
             CC_LAUNCH_CHECK("k_amsf_first");
             k_amsf_scan<<<1, kBlock, 0, s>>>(start, nb);
             CC_LAUNCH_CHECK("k_amsf_scan");
             CC_CUDA_TRY(cudaMemcpyAsync(cursor, start, sizeof(unsigned long long) * (nb + 1), cudaMemcpyDeviceToDevice, s));
-            k_amsf_scatter<<<sms * 8, kBlock, 0, s>>>(vi, fb, n, nb, cursor, order);
+            k_amsf_scatter<<<grid_blocks(8), kBlock, 0, s>>>(vi, fb, n, nb, cursor, order);
             CC_LAUNCH_CHECK("k_amsf_scatter");
             if (index) {
                 // bucket index: lists longer than kIdxMin grouped by bucket, once; the list
@@ -1134,7 +1144,7 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
                 CC_CUDA_TRY(cudaMemsetAsync(hcount, 0, 3 * sizeof(unsigned long long), s));
                 uint32_t *q0 = hubs, *q1 = hubs + qcap0;
                 unsigned long long *qb0 = hdeg, *qb1 = hdeg + qcap0;
-                k_amsf_hubs<<<sms * 8, kBlock, 0, s>>>(off, n, q0, q1, qb0, qb1, hcount);
+                k_amsf_hubs<<<grid_blocks(8), kBlock, 0, s>>>(off, n, q0, q1, qb0, qb1, hcount);
                 CC_LAUNCH_CHECK("k_amsf_hubs");
                 unsigned long long hc[3] = {0, 0, 0};
                 CC_CUDA_TRY(cudaMemcpyAsync(hc, hcount, sizeof(hc), cudaMemcpyDeviceToHost, s));
@@ -1145,7 +1155,7 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
                 const float wmin_f = (float)b[0], il2g = (float)(1.0 / std::log2(1.0 + eps));
                 if (hc[0]) {
                     if (nb + 1 <= kIdxWarpBins) {
-                        k_amsf_idx_warp<<<sms * 16, kIdxWBlock, 0, s>>>(off, w, q0, qb0, hcount, bfl, nb, wmin_f, il2g, vi,
+                        k_amsf_idx_warp<<<grid_blocks(16), kIdxWBlock, 0, s>>>(off, w, q0, qb0, hcount, bfl, nb, wmin_f, il2g, vi,
                                                                   hstart, hidx);
                         CC_LAUNCH_CHECK("k_amsf_idx_warp");
                     } else {
@@ -1153,7 +1163,7 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
                     }
                 }
                 if (index && hc[1]) {
-                    k_amsf_hub_index<<<sms * 2, 1024, 0, s>>>(off, w, q1, qb1, hcount, bfl, nb, wmin_f, il2g, vi, hstart,
+                    k_amsf_hub_index<<<grid_blocks(2), 1024, 0, s>>>(off, w, q1, qb1, hcount, bfl, nb, wmin_f, il2g, vi, hstart,
                                                               hidx);
                     CC_LAUNCH_CHECK("k_amsf_hub_index");
                 }
@@ -1166,19 +1176,19 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
                 k_amsf_lmax<<<1, 1024, 0, s>>>(P, n, o.seed, i, o.samples, ac);
                 CC_LAUNCH_CHECK("k_amsf_lmax");
             }
-            k_amsf_round<MODE><<<sms * 8, kBlock, 0, s>>>(off, adj, w, P, vi, order, start, i, b[i], b[i + 1],
+            k_amsf_round<MODE><<<resident_grid(k_amsf_round<MODE>, kBlock), kBlock, 0, s>>>(off, adj, w, P, vi, order, start, i, b[i], b[i + 1],
                                                           carry[in_slot], ac, in_slot, carry[in_slot ^ 1],
                                                           skip, plain, F, Fw, chq, index ? hstart : nullptr,
                                                           hidx, nb, o.counters);
             CC_LAUNCH_CHECK("k_amsf_round");
             if (index)
-                k_amsf_hub_pieces<MODE><<<sms * 8, kBlock, 0, s>>>(off, adj, w, P, i, chq, ac, vi, hstart, hidx,
+                k_amsf_hub_pieces<MODE><<<resident_grid(k_amsf_hub_pieces<MODE>, kBlock), kBlock, 0, s>>>(off, adj, w, P, i, chq, ac, vi, hstart, hidx,
                                                                    nb, F, Fw, o.counters);
             else if (((uintptr_t)w & 15u) == 0)
-                k_amsf_chunks<MODE, true><<<sms * 8, kBlock, 0, s>>>(off, adj, w, P, b[i], b[i + 1], chq, ac, F, Fw,
+                k_amsf_chunks<MODE, true><<<resident_grid(k_amsf_chunks<MODE, true>, kBlock), kBlock, 0, s>>>(off, adj, w, P, b[i], b[i + 1], chq, ac, F, Fw,
                                                                      o.counters);
             else
-                k_amsf_chunks<MODE, false><<<sms * 8, kBlock, 0, s>>>(off, adj, w, P, b[i], b[i + 1], chq, ac, F,
+                k_amsf_chunks<MODE, false><<<resident_grid(k_amsf_chunks<MODE, false>, kBlock), kBlock, 0, s>>>(off, adj, w, P, b[i], b[i + 1], chq, ac, F,
                                                                       Fw, o.counters);
             CC_LAUNCH_CHECK("k_amsf_chunks");
             k_amsf_next<<<1, 1, 0, s>>>(ac, in_slot, o.counters);
@@ -1207,7 +1217,7 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
         CC_LAUNCH_CHECK("k_forest_filter");
         if (total) {
             CC_CUDA_TRY(cudaMemsetAsync(total, 0, sizeof(double), s));
-            k_amsf_total<<<sms * 4, kBlock, 0, s>>>(ew, num_edges, total);
+            k_amsf_total<<<grid_blocks(4), kBlock, 0, s>>>(ew, num_edges, total);
             CC_LAUNCH_CHECK("k_amsf_total");
         }
         if (ew != edge_w) scratch_free(ew, s);

@@ -163,4 +163,6 @@ cc_status cc_bench_set_l2_fetch(int bytes, int* prev)
 
 uint64_t cc_bench_launch_count(void) { return g_launches.load(); }
 
+unsigned cc_bench_set_grid(unsigned blocks) { return g_grid_override.exchange(blocks); }
+
 }  // extern "C"

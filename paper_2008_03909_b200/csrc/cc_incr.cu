@@ -40,6 +40,34 @@ __global__ void __launch_bounds__(kBlock) k_insert(uint32_t* P, const uint2* __r
     link<MODE>(P, e.x, e.y, NoForest{});
 }
 
+// Batched form (the default for UF-Rem-CAS): each thread takes kIB inserts spaced
+// one block apart (coalesced pair loads) and issues all 2 kIB first parent reads
+// together, then enters the Rem loop of each with them (link_rem_from) -- kIB
+// times the memory-level parallelism of one link per thread.  Same unions, same
+// partition; only the first reads move.
+constexpr int kIB = 4;
+
+template <bool HALVE>
+__global__ void __launch_bounds__(kBlock) k_insert4(uint32_t* P, const uint2* __restrict__ ins, int64_t n_ins)
+{
+    const int64_t base = (int64_t)blockIdx.x * (kBlock * kIB) + threadIdx.x;
+    uint2 e[kIB];
+    uint32_t pu[kIB], pv[kIB];
+#pragma unroll
+    for (int q = 0; q < kIB; ++q) {
+        const int64_t i = base + (int64_t)q * kBlock;
+        e[q] = i < n_ins ? ins[i] : make_uint2(0u, 0u);
+    }
+#pragma unroll
+    for (int q = 0; q < kIB; ++q) {
+        pu[q] = ld_relaxed(P + e[q].x);
+        pv[q] = ld_relaxed(P + e[q].y);
+    }
+#pragma unroll
+    for (int q = 0; q < kIB; ++q)
+        if (pu[q] != pv[q]) link_rem_from<HALVE>(P, e[q].x, e[q].y, pu[q], pv[q], NoForest{});
+}
+
 // Queries run after the insert kernel: no hook can happen concurrently, so
 // roots are fixed and FindNaive needs no L2-forced loads; with SPLIT the finds
 // also shorten paths (FindAtomicSplit) for later batches.
@@ -54,6 +82,39 @@ __device__ __forceinline__ uint32_t query_find(uint32_t* P, uint32_t x)
     if constexpr (FIND == 1) return find_split(P, x);
     else if constexpr (FIND == 2) return find_naive(P, x);
     else return find_halve_quiet(P, x);
+}
+
+// Default queries (FIND 0, path halving with plain stores) batched like
+// k_insert4: kIB queries per thread, the 2 kIB first parent reads issued
+// together; a query whose two first parents agree is answered without a walk.
+__global__ void __launch_bounds__(kBlock) k_query4(uint32_t* P, const uint2* __restrict__ q, int64_t n_q,
+                                                   uint8_t* __restrict__ ans)
+{
+    const int64_t base = (int64_t)blockIdx.x * (kBlock * kIB) + threadIdx.x;
+    uint2 e[kIB];
+    uint32_t pa[kIB], pb[kIB];
+#pragma unroll
+    for (int k = 0; k < kIB; ++k) {
+        const int64_t i = base + (int64_t)k * kBlock;
+        e[k] = i < n_q ? q[i] : make_uint2(0u, 0u);
+    }
+#pragma unroll
+    for (int k = 0; k < kIB; ++k) {
+        pa[k] = ld_relaxed(P + e[k].x);
+        pb[k] = ld_relaxed(P + e[k].y);
+    }
+#pragma unroll
+    for (int k = 0; k < kIB; ++k) {
+        const int64_t i = base + (int64_t)k * kBlock;
+        if (i >= n_q) break;
+        uint8_t a = 1;
+        if (pa[k] != pb[k]) {
+            const uint32_t ra = pa[k] == e[k].x ? pa[k] : find_halve_quiet(P, pa[k]);
+            const uint32_t rb = pb[k] == e[k].y ? pb[k] : find_halve_quiet(P, pb[k]);
+            a = ra == rb ? 1 : 0;
+        }
+        ans[i] = a;
+    }
 }
 
 template <int FIND>
@@ -179,6 +240,7 @@ __global__ void __launch_bounds__(kBlock) k_labels(uint32_t* P, uint32_t n, uint
 }
 
 static unsigned nblocks(int64_t count) { return (unsigned)((count + kBlock - 1) / kBlock); }
+static unsigned nblocks4(int64_t count) { return (unsigned)((count + kBlock * kIB - 1) / (kBlock * kIB)); }
 
 static cc_status insert_query(cc_incr* h, const uint32_t* ins, int64_t n_ins, const uint32_t* qs, int64_t n_q,
                               uint8_t* ans, cudaStream_t s)
@@ -188,11 +250,11 @@ static cc_status insert_query(cc_incr* h, const uint32_t* ins, int64_t n_ins, co
         CC_CUDA_TRY(scratch_alloc((void**)&err, sizeof(unsigned int), s));
         CC_CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(unsigned int), s));
         if (n_ins) {
-            k_check_ids<<<num_sms() * 4, kBlock, 0, s>>>(ins, 2 * n_ins, h->n, err);
+            k_check_ids<<<grid_blocks(4), kBlock, 0, s>>>(ins, 2 * n_ins, h->n, err);
             CC_LAUNCH_CHECK("k_check_ids");
         }
         if (n_q) {
-            k_check_ids<<<num_sms() * 4, kBlock, 0, s>>>(qs, 2 * n_q, h->n, err);
+            k_check_ids<<<grid_blocks(4), kBlock, 0, s>>>(qs, 2 * n_q, h->n, err);
             CC_LAUNCH_CHECK("k_check_ids");
         }
         unsigned int e = 0;
@@ -240,7 +302,8 @@ static cc_status insert_query(cc_incr* h, const uint32_t* ins, int64_t n_ins, co
         else if (h->flags & CC_FLAG_HALVE) k_insert<1><<<nblocks(n_ins), kBlock, 0, s>>>(h->P, e, n_ins);
         // (the static path's lane-refill kernel measured slower here: 26.1 vs 28.0 G ops/s
         // on C5 -- random u, and one link per thread already fills the machine)
-        else k_insert<0><<<nblocks(n_ins), kBlock, 0, s>>>(h->P, e, n_ins);
+        else if (h->flags & CC_FLAG_INSERT1) k_insert<0><<<nblocks(n_ins), kBlock, 0, s>>>(h->P, e, n_ins);
+        else k_insert4<false><<<nblocks4(n_ins), kBlock, 0, s>>>(h->P, e, n_ins);
         CC_LAUNCH_CHECK("k_insert");
     }
     // ---- kernel boundary: the insert/query barrier of type (3) ----
@@ -248,7 +311,8 @@ static cc_status insert_query(cc_incr* h, const uint32_t* ins, int64_t n_ins, co
         const uint2* q = reinterpret_cast<const uint2*>(qs);
         if (h->flags & CC_FLAG_FIND_SPLIT) k_query<1><<<nblocks(n_q), kBlock, 0, s>>>(h->P, q, n_q, ans);
         else if (h->flags & CC_FLAG_FIND_NAIVE) k_query<2><<<nblocks(n_q), kBlock, 0, s>>>(h->P, q, n_q, ans);
-        else k_query<0><<<nblocks(n_q), kBlock, 0, s>>>(h->P, q, n_q, ans);
+        else if (h->flags & CC_FLAG_INSERT1) k_query<0><<<nblocks(n_q), kBlock, 0, s>>>(h->P, q, n_q, ans);
+        else k_query4<<<nblocks4(n_q), kBlock, 0, s>>>(h->P, q, n_q, ans);
         CC_LAUNCH_CHECK("k_query");
     }
     return CC_OK;
@@ -453,8 +517,8 @@ cc_status cc_incr_batches(cc_incr* h, int64_t nb, const int64_t* ins_counts, con
         unsigned int* err = nullptr;
         CC_CUDA_TRY(scratch_alloc((void**)&err, sizeof(unsigned int), s));
         CC_CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(unsigned int), s));
-        if (tot_i) { k_check_ids<<<num_sms() * 4, kBlock, 0, s>>>(d_ins, 2 * tot_i, h->n, err); CC_LAUNCH_CHECK("k_check_ids"); }
-        if (tot_q) { k_check_ids<<<num_sms() * 4, kBlock, 0, s>>>(d_q, 2 * tot_q, h->n, err); CC_LAUNCH_CHECK("k_check_ids"); }
+        if (tot_i) { k_check_ids<<<grid_blocks(4), kBlock, 0, s>>>(d_ins, 2 * tot_i, h->n, err); CC_LAUNCH_CHECK("k_check_ids"); }
+        if (tot_q) { k_check_ids<<<grid_blocks(4), kBlock, 0, s>>>(d_q, 2 * tot_q, h->n, err); CC_LAUNCH_CHECK("k_check_ids"); }
         unsigned int e = 0;
         CC_CUDA_TRY(cudaMemcpyAsync(&e, err, sizeof(e), cudaMemcpyDeviceToHost, s));
         CC_CUDA_TRY(cudaStreamSynchronize(s));

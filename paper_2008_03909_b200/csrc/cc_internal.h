@@ -19,6 +19,19 @@ extern std::atomic<uint64_t> g_launches;
 inline void count_launch(uint64_t k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
 int num_sms();
+// Blocks of a grid-strided kernel: num_sms() * per_sm, unless a test set an
+// override (cc_bench_set_grid) -- such kernels are correct for any grid size.
+unsigned grid_blocks(unsigned per_sm);
+extern std::atomic<unsigned> g_grid_override;
+// One wave of a grid-strided kernel: num_sms() x the blocks of `block` threads
+// that fit on one SM (occupancy query, cached per kernel), so static grid-stride
+// work splits never leave a partial second wave; the test override applies.
+unsigned resident_blocks(const void* kernel, int block);
+template <class K>
+inline unsigned resident_grid(K* kernel, int block)
+{
+    return resident_blocks(reinterpret_cast<const void*>(kernel), block);
+}
 bool is_device_ptr(const void* p);
 
 // Where an array argument lives: device memory, pinned host memory (device-

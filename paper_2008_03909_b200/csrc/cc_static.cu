@@ -594,7 +594,7 @@ static cc_status launch_compress(uint32_t* P, uint32_t n, uint32_t* out, cc_coun
     // a gated (maybe skipped) compress runs as a persistent grid so that a skip
     // costs one short wave, not 65k empty blocks; otherwise one block per tile
     const uint64_t ntiles = ((uint64_t)n + kCTile - 1) / kCTile;
-    const unsigned grid = (unsigned)(gate ? std::min<uint64_t>(ntiles, (uint64_t)num_sms() * 8) : ntiles);
+    const unsigned grid = (unsigned)(gate ? std::min<uint64_t>(ntiles, (uint64_t)grid_blocks(8)) : ntiles);
     if (aligned16(P) && aligned16(out) && cnt) k_compress<true><<<grid, kBlock, 0, s>>>(P, n, out, cnt, gate);
     else if (aligned16(P) && aligned16(out)) k_compress<false><<<grid, kBlock, 0, s>>>(P, n, out, nullptr, gate);
     else
@@ -850,6 +850,17 @@ __global__ void __launch_bounds__(kBlock) k_rank_fill(uint2* rbw, uint32_t nw, c
     }
 }
 
+// Grid of the static k-out link kernel.  CC_REFILL_GRID blocks per SM (default
+// 8: 1.33 waves at its 6 resident blocks per SM), 0 = exactly one resident wave.
+#ifndef CC_REFILL_GRID
+#define CC_REFILL_GRID 8
+#endif
+template <bool SF>
+static unsigned refill_grid()
+{
+    return CC_REFILL_GRID ? grid_blocks(CC_REFILL_GRID) : resident_grid(k_link_refill<SF>, kBlock);
+}
+
 // ---------------------------------------------------------------------------
 // K4: IdentifyFrequent: the mode of root(s_i) over S samples,
 // s_i = uniform_below(mix(seed, IDENT, i), n), ties to the smaller label
@@ -940,30 +951,48 @@ __global__ void __launch_bounds__(1024) k_identify(uint32_t* P, uint32_t n, uint
 // root is skipped without a link), longer lists are queued for k_finish_big
 // (one CTA per vertex).  Keeping the edge work out of the scan keeps the scan
 // a lean streaming kernel (no spills, full occupancy).
-template <bool VEC, bool CNT, bool CONTRACT>
-__global__ void __launch_bounds__(kBlock, CC_FINISH_MINB) k_finish(uint32_t* P, const uint32_t* __restrict__ bm, uint32_t n,
-                                                   Ctl* ctl, bool no_skip, uint32_t* cq, cc_counters* cnt,
-                                                   const uint2* __restrict__ rbw, const uint32_t* __restrict__ rid)
+//
+// Warp summaries for the partial final compress (k_relabel): after this pass
+// every slot holds its sampled root, and the only labels H5 can change are
+// those of slots whose root it hooks.  Each warp records, for its 256 slots,
+// its "foreign" root -- a root other than the slot itself and L_max -- in one
+// word: kSentinel none, r the only one, kWarpOverflow two or more distinct (ids
+// are < n <= 0xFFFFFFFE, so 0xFFFFFFFE is never a root).  Warp-level only (no
+// block barrier: the scan keeps fire-and-forget blocks).  Each block clears the
+// hook flag of its 2048-slot tile (set by H5 when it hooks a root of the tile).
+constexpr uint32_t kWarpOverflow = 0xFFFFFFFEu;
+constexpr int kSumPerTile = kBlock / 32;                 // warp summaries per tile
+
+__device__ __forceinline__ uint32_t warp_foreign_summary(const uint32_t (&rr)[kCV], uint32_t fmask)
 {
-    const uint32_t lmax = no_skip ? kSentinel : ctl->lmax;
-    const uint64_t base = (uint64_t)blockIdx.x * kCTile;
+    // fmask: bit s set iff slot s of this lane holds a foreign root
+    const unsigned m1 = __ballot_sync(0xffffffffu, fmask != 0);
+    if (!m1) return kSentinel;
+    const int src = __ffs(m1) - 1;
+    uint32_t x = kSentinel;                              // the lane's first foreign root (static indexing)
+#pragma unroll
+    for (int s = kCV - 1; s >= 0; --s)
+        if (fmask >> s & 1u) x = rr[s];
+    const uint32_t a = __shfl_sync(0xffffffffu, x, src);
+    bool more = false;
+#pragma unroll
+    for (int s = 0; s < kCV; ++s) more |= (fmask >> s & 1u) && rr[s] != a;
+    return __any_sync(0xffffffffu, more) ? kWarpOverflow : a;
+}
+
+// One tile of the scan, with its P words (pp) and bitmap words already loaded.
+template <bool CNT, bool CONTRACT>
+__device__ __forceinline__ void finish_tile(uint32_t* P, uint32_t n, uint64_t tile, bool full, uint32_t (&pp)[kCV],
+                                            uint32_t w0, uint32_t w1, uint32_t lmax, Ctl* ctl, uint32_t* cq,
+                                            const uint2* __restrict__ rbw, const uint32_t* __restrict__ rid,
+                                            uint32_t* __restrict__ wsum, uint8_t* __restrict__ td, uint32_t& writes,
+                                            uint32_t& gathers)
+{
+    const uint64_t base = tile * kCTile;
     const uint64_t i0 = base + 4 * (uint64_t)threadIdx.x, i1 = i0 + 4 * kBlock;
-    const bool full = VEC && base + kCTile <= n;
-    uint32_t vv[kCV], pp[kCV], rr[kCV];
+    uint32_t vv[kCV], rr[kCV];
 #pragma unroll
     for (int s = 0; s < kCV; ++s) vv[s] = (uint32_t)((s < 4 ? i0 : i1) + (s & 3));
-    if (full) {
-        const uint4 a = reinterpret_cast<const uint4*>(P)[i0 >> 2];
-        const uint4 c = reinterpret_cast<const uint4*>(P)[i1 >> 2];
-        pp[0] = a.x; pp[1] = a.y; pp[2] = a.z; pp[3] = a.w;
-        pp[4] = c.x; pp[5] = c.y; pp[6] = c.z; pp[7] = c.w;
-    } else {
-#pragma unroll
-        for (int s = 0; s < kCV; ++s) pp[s] = (uint64_t)((s < 4 ? i0 : i1) + (s & 3)) < n ? P[vv[s]] : vv[s];
-    }
-    const uint32_t w0 = i0 < n ? bm[i0 >> 5] : 0u;
-    const uint32_t w1 = i1 < n ? bm[i1 >> 5] : 0u;
-    uint32_t writes = 0, gathers = 0;
     if constexpr (CONTRACT) {
         // P[v] is v's F0 root: its sampled root is one rank-word + one rid
         // lookup (L2-resident), no gather into P
@@ -974,13 +1003,16 @@ __global__ void __launch_bounds__(kBlock, CC_FINISH_MINB) k_finish(uint32_t* P, 
         for (int s = 0; s < kCV; ++s) {
             const bool cr = (w[s].x >> (pp[s] & 31)) & 1u;
             rr[s] = cr ? rid[cid_of(w[s], pp[s])] : pp[s];
-            gathers += cr;
+            if (CNT) gathers += cr;
         }
     } else {
-        gathers = roots8(P, vv, pp, rr, lmax);               // L_max stays a root: no hook runs here
+        const uint32_t g = roots8(P, vv, pp, rr, lmax);     // L_max stays a root: no hook runs here
+        if (CNT) gathers += g;
     }
+    if (CNT) {
 #pragma unroll
-    for (int s = 0; s < kCV; ++s) writes += rr[s] != pp[s];
+        for (int s = 0; s < kCV; ++s) writes += rr[s] != pp[s];
+    }
     if (full) {                                          // H3 compress writes
         if (rr[0] != pp[0] || rr[1] != pp[1] || rr[2] != pp[2] || rr[3] != pp[3])
             reinterpret_cast<uint4*>(P)[i0 >> 2] = make_uint4(rr[0], rr[1], rr[2], rr[3]);
@@ -991,13 +1023,22 @@ __global__ void __launch_bounds__(kBlock, CC_FINISH_MINB) k_finish(uint32_t* P, 
         for (int s = 0; s < kCV; ++s)
             if (rr[s] != pp[s]) P[vv[s]] = rr[s];           // rr != pp only for in-range slots
     }
-    uint32_t cm = 0;                                     // candidate slots of this thread
+    uint32_t cm = 0, fmask = 0;                          // candidate / foreign-root slots of this thread
 #pragma unroll
     for (int s = 0; s < kCV; ++s) {
         const uint64_t v64 = (s < 4 ? i0 : i1) + (s & 3);
         const uint32_t word = s < 4 ? w0 : w1;
         if (v64 < n && ((word >> (vv[s] & 31)) & 1u) && rr[s] != lmax) cm |= 1u << s;
+        if (v64 < n && rr[s] != vv[s] && rr[s] != lmax) fmask |= 1u << s;
     }
+    // warp summary of the foreign roots (rare outside grids)
+#ifndef CC_FINISH_NOSUM
+    const uint32_t ws = warp_foreign_summary(rr, fmask);
+#else
+    const uint32_t ws = kWarpOverflow;
+#endif
+    if ((threadIdx.x & 31) == 0) wsum[tile * kSumPerTile + (threadIdx.x >> 5)] = ws;
+    if (threadIdx.x == 0) td[tile] = 0;
     if (__any_sync(0xffffffffu, cm != 0)) {
         const unsigned long long pos = warp_append(&ctl->cand_count, __popc(cm));
         uint32_t k2 = 0;
@@ -1005,11 +1046,96 @@ __global__ void __launch_bounds__(kBlock, CC_FINISH_MINB) k_finish(uint32_t* P, 
         for (int s = 0; s < kCV; ++s)
             if (cm >> s & 1u) cq[pos + k2++] = vv[s];
     }
+}
+
+__device__ __forceinline__ void finish_load(const uint32_t* P, const uint32_t* __restrict__ bm, uint32_t n,
+                                            uint64_t tile, bool full, uint32_t (&pp)[kCV], uint32_t& w0, uint32_t& w1)
+{
+    const uint64_t base = tile * kCTile;
+    const uint64_t i0 = base + 4 * (uint64_t)threadIdx.x, i1 = i0 + 4 * kBlock;
+    if (full) {
+        const uint4 a = reinterpret_cast<const uint4*>(P)[i0 >> 2];
+        const uint4 c = reinterpret_cast<const uint4*>(P)[i1 >> 2];
+        pp[0] = a.x; pp[1] = a.y; pp[2] = a.z; pp[3] = a.w;
+        pp[4] = c.x; pp[5] = c.y; pp[6] = c.z; pp[7] = c.w;
+    } else {
+#pragma unroll
+        for (int s = 0; s < kCV; ++s) {
+            const uint64_t v = (s < 4 ? i0 : i1) + (s & 3);
+            pp[s] = v < n ? P[v] : (uint32_t)v;
+        }
+    }
+    w0 = i0 < n ? bm[i0 >> 5] : 0u;
+    w1 = i1 < n ? bm[i1 >> 5] : 0u;
+}
+
+// One tile per block (65,536 blocks on C4): fire-and-forget blocks, 8 resident per SM.
+template <bool VEC, bool CNT, bool CONTRACT>
+__global__ void __launch_bounds__(kBlock, CC_FINISH_MINB) k_finish(uint32_t* P, const uint32_t* __restrict__ bm, uint32_t n,
+                                                   Ctl* ctl, bool no_skip, uint32_t* cq, cc_counters* cnt,
+                                                   const uint2* __restrict__ rbw, const uint32_t* __restrict__ rid,
+                                                   uint32_t* __restrict__ wsum, uint8_t* __restrict__ td)
+{
+    const uint32_t lmax = no_skip ? kSentinel : ctl->lmax;
+    const uint64_t tile = blockIdx.x;
+    const bool full = VEC && (tile + 1) * kCTile <= n;
+    uint32_t pp[kCV], w0, w1, writes = 0, gathers = 0;
+    finish_load(P, bm, n, tile, full, pp, w0, w1);
+    finish_tile<CNT, CONTRACT>(P, n, tile, full, pp, w0, w1, lmax, ctl, cq, rbw, rid, wsum, td, writes, gathers);
     if (CNT) {
         warp_count(&cnt->compress_writes, writes);
         warp_count(&cnt->finish_gathers, gathers);
     }
 }
+
+// Persistent variant (CC_FINISH_PERSIST): each block walks tiles blockIdx.x,
+// + gridDim.x, ... and issues the NEXT tile's P / bitmap loads before resolving
+// the current one's roots, so a tile's streaming reads overlap the previous
+// tile's gathers (twice the bytes in flight per thread).
+#ifndef CC_FINISH_PMINB
+#define CC_FINISH_PMINB 6
+#endif
+template <bool VEC, bool CNT, bool CONTRACT>
+__global__ void __launch_bounds__(kBlock, CC_FINISH_PMINB) k_finish_persist(
+    uint32_t* P, const uint32_t* __restrict__ bm, uint32_t n, Ctl* ctl, bool no_skip, uint32_t* cq, cc_counters* cnt,
+    const uint2* __restrict__ rbw, const uint32_t* __restrict__ rid, uint32_t* __restrict__ wsum,
+    uint8_t* __restrict__ td)
+{
+    const uint32_t lmax = no_skip ? kSentinel : ctl->lmax;
+    const uint64_t ntiles = ((uint64_t)n + kCTile - 1) / kCTile;
+    uint32_t pp[kCV], w0 = 0, w1 = 0, writes = 0, gathers = 0;
+    uint64_t tile = blockIdx.x;
+    if (tile < ntiles) finish_load(P, bm, n, tile, VEC && (tile + 1) * kCTile <= n, pp, w0, w1);
+    for (; tile < ntiles; tile += gridDim.x) {
+        const bool full = VEC && (tile + 1) * kCTile <= n;
+        uint32_t cur[kCV];
+#pragma unroll
+        for (int s = 0; s < kCV; ++s) cur[s] = pp[s];
+        const uint32_t c0 = w0, c1 = w1;
+        const uint64_t nt = tile + gridDim.x;
+        if (nt < ntiles) finish_load(P, bm, n, nt, VEC && (nt + 1) * kCTile <= n, pp, w0, w1);
+        finish_tile<CNT, CONTRACT>(P, n, tile, full, cur, c0, c1, lmax, ctl, cq, rbw, rid, wsum, td, writes, gathers);
+    }
+    if (CNT) {
+        warp_count(&cnt->compress_writes, writes);
+        warp_count(&cnt->finish_gathers, gathers);
+    }
+}
+
+// H5 hook record: besides the forest slot (SF), flag the tile of the hooked
+// root for the partial final compress -- every label H5 changes is a slot of
+// that root's component (the tiles holding its other slots name it among their
+// foreign roots, see k_finish).
+template <class F>
+struct TileMarked {
+    F f;
+    uint8_t* td;
+    __device__ __forceinline__ void record(uint32_t r, uint32_t u, uint32_t v) const
+    {
+        td[r / (uint32_t)kCTile] = 1;
+        f.record(r, u, v);
+    }
+};
 
 // k_finish_proc: the H5 edge work of the queued candidates.  A warp takes 32
 // candidates, prefix-sums their list lengths (after the afforest-sampled
@@ -1022,7 +1148,7 @@ template <int MODE, bool SF>
 __global__ void __launch_bounds__(kBlock) k_finish_proc(
     const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, uint32_t* P,
     const uint32_t* __restrict__ cq, Ctl* ctl, uint32_t skip_prefix, uint32_t* big, unsigned long long big_cap,
-    uint2* F, cc_counters* cnt)
+    uint2* F, cc_counters* cnt, uint8_t* td)
 {
     const unsigned long long total = ctl->cand_count;
     const unsigned lane = threadIdx.x & 31;
@@ -1084,11 +1210,12 @@ __global__ void __launch_bounds__(kBlock) k_finish_proc(
                 const uint32_t pv = ld_relaxed(P + v);
                 if (pv != orr) {                            // enter the Rem loop with both reads done
                     if constexpr (MODE == 2) {
-                        if constexpr (SF) hooks += link_async(P, ou, v, Forest{F});
-                        else hooks += link_async(P, ou, v, NoForest{});
+                        if constexpr (SF) hooks += link_async(P, ou, v, TileMarked<Forest>{Forest{F}, td});
+                        else hooks += link_async(P, ou, v, TileMarked<NoForest>{NoForest{}, td});
                     } else {
-                        if constexpr (SF) hooks += link_rem_from<MODE == 1>(P, ou, v, orr, pv, Forest{F});
-                        else hooks += link_rem_from<MODE == 1>(P, ou, v, orr, pv, NoForest{});
+                        if constexpr (SF)
+                            hooks += link_rem_from<MODE == 1>(P, ou, v, orr, pv, TileMarked<Forest>{Forest{F}, td});
+                        else hooks += link_rem_from<MODE == 1>(P, ou, v, orr, pv, TileMarked<NoForest>{NoForest{}, td});
                     }
                 }
             }
@@ -1106,7 +1233,8 @@ template <int MODE, bool SF>
 __global__ void __launch_bounds__(512) k_finish_big(const int64_t* __restrict__ off,
                                                     const uint32_t* __restrict__ adj, uint32_t* P,
                                                     const uint32_t* __restrict__ big, unsigned long long big_cap,
-                                                    const Ctl* ctl, uint32_t skip_prefix, uint2* F, cc_counters* cnt)
+                                                    const Ctl* ctl, uint32_t skip_prefix, uint2* F, cc_counters* cnt,
+                                                    uint8_t* td)
 {
     __shared__ uint32_t s_ru;
     const unsigned long long nbig = ctl->big_count, nhuge = ctl->huge_count;
@@ -1130,12 +1258,115 @@ __global__ void __launch_bounds__(512) k_finish_big(const int64_t* __restrict__ 
             for (int64_t x = x0; x < e; x += step) {
                 const uint32_t v = adj[x];
                 if (ld_relaxed(P + v) == ru) continue;
-                if constexpr (SF) hooks += link<MODE>(P, u, v, Forest{F});
-                else hooks += link<MODE>(P, u, v, NoForest{});
+                if constexpr (SF) hooks += link<MODE>(P, u, v, TileMarked<Forest>{Forest{F}, td});
+                else hooks += link<MODE>(P, u, v, TileMarked<NoForest>{NoForest{}, td});
             }
         }
     }
     if (cnt) warp_count(&cnt->finish_hooks, hooks);
+}
+
+// ---------------------------------------------------------------------------
+// K6': the final compress (H6) as a PARTIAL pass.  After k_finish every slot
+// holds its sampled root, and H5 changes the label of exactly the slots whose
+// root it hooked: the slots of a tile whose hook flag H5 set (the hooked root
+// itself lies there) and of every tile that lists a hooked root among its
+// foreign roots -- or, if L_max itself was hooked, every slot of its component
+// (then every tile is re-resolved).  A tile with two distinct foreign
+// roots in one of its 256-slot warp summaries is always re-resolved.  Each warp
+// owns a run of consecutive tiles: one lane per tile decides (flag, 32 bytes of
+// warp summaries, a P[r] == r test per named root),
+// then the whole warp re-resolves each dirty tile (coalesced 16-byte loads,
+// first-level parents batched as in k_compress, writes only changed slots).
+// The result equals the full compress: every other slot already holds its
+// final root (the canonical min-id label, reading R13).
+template <bool CNT>
+__global__ void __launch_bounds__(kBlock) k_relabel(uint32_t* P, uint32_t n, const Ctl* ctl, bool no_skip,
+                                                    const uint32_t* __restrict__ wsum, const uint8_t* __restrict__ td,
+                                                    cc_counters* cnt)
+{
+    const unsigned lane = threadIdx.x & 31;
+    uint32_t lm = no_skip ? kSentinel : ctl->lmax;
+    if (lm >= n) lm = kSentinel;                                      // a forced out-of-range L_max skips nothing
+    // L_max no longer a root: H5 hooked it, or a forced L_max was never one -- in
+    // both cases slots holding it are not final, so every tile is re-resolved
+    const bool lmax_hooked = lm != kSentinel && P[lm] != lm;         // no hook runs in H6: plain loads
+    const uint32_t known = lmax_hooked ? kSentinel : lm;
+    const uint64_t ntiles = ((uint64_t)n + kCTile - 1) / kCTile;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t tpw = (ntiles + nwarps - 1) / nwarps < 32 ? (ntiles + nwarps - 1) / nwarps : (uint64_t)32;  // tiles per warp per sweep
+    const bool vec = ((uintptr_t)P & 15u) == 0;
+    uint32_t writes = 0, gathers = 0, tiles = 0;
+    for (uint64_t t0 = warp * tpw; t0 < ntiles; t0 += nwarps * tpw) {
+        const uint64_t t = t0 + lane;
+        bool dirty = false;
+        if (lane < tpw && t < ntiles) {
+            if (lmax_hooked || td[t]) {
+                dirty = true;
+            } else {
+                // the tile's kSumPerTile warp summaries (32 contiguous bytes)
+                const uint4* w4 = reinterpret_cast<const uint4*>(wsum + t * kSumPerTile);
+                const uint4 q0 = w4[0], q1 = w4[1];
+                const uint32_t r8[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    dirty |= r8[c] == kWarpOverflow || (r8[c] != kSentinel && P[r8[c]] != r8[c]);
+            }
+        }
+        unsigned mask = __ballot_sync(0xffffffffu, dirty);
+        if (CNT) tiles += dirty;
+        while (mask) {
+            const uint64_t base = (t0 + (unsigned)(__ffs(mask) - 1)) * kCTile;
+            mask &= mask - 1;
+            if (vec && base + kCTile <= n) {
+                // 512 uint4 per tile: 4 rounds of 4 uint4 (16 slots) per lane
+#pragma unroll 1
+                for (int j = 0; j < 16; j += 4) {
+                    uint4 q[4];
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) q[h] = reinterpret_cast<const uint4*>(P)[base / 4 + lane + 32 * (j + h)];
+#pragma unroll
+                    for (int h = 0; h < 4; h += 2) {
+                        const uint64_t i0 = base + 4 * (lane + 32 * (uint64_t)(j + h)), i1 = i0 + 128;
+                        const uint32_t pp[8] = {q[h].x, q[h].y, q[h].z, q[h].w, q[h + 1].x, q[h + 1].y, q[h + 1].z,
+                                                q[h + 1].w};
+                        uint32_t vv[8], rr[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) vv[k] = (uint32_t)((k < 4 ? i0 : i1) + (k & 3));
+                        const uint32_t g = roots8(P, vv, pp, rr, known);
+                        const uint4 r0 = make_uint4(rr[0], rr[1], rr[2], rr[3]);
+                        const uint4 r1 = make_uint4(rr[4], rr[5], rr[6], rr[7]);
+                        const uint32_t c0 = nchanged4(r0, q[h]), c1 = nchanged4(r1, q[h + 1]);
+                        if (c0) reinterpret_cast<uint4*>(P)[i0 >> 2] = r0;
+                        if (c1) reinterpret_cast<uint4*>(P)[i1 >> 2] = r1;
+                        if (CNT) {
+                            gathers += g;
+                            writes += c0 + c1;
+                        }
+                    }
+                }
+            } else {
+                const uint64_t end = (base + kCTile < n ? base + kCTile : (uint64_t)n);
+                for (uint64_t v64 = base + lane; v64 < end; v64 += 32) {
+                    const uint32_t v = (uint32_t)v64;
+                    const uint32_t p = P[v];
+                    const bool g = !(p == v || p == known);
+                    const uint32_t r = g ? root_halve(P, p) : p;
+                    if (r != p) P[v] = r;
+                    if (CNT) {
+                        gathers += g;
+                        writes += r != p;
+                    }
+                }
+            }
+        }
+    }
+    if (CNT) {
+        warp_count(&cnt->h6_writes, writes);
+        warp_count(&cnt->h6_gathers, gathers);
+        warp_count(&cnt->h6_tiles, tiles);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1363,7 +1594,6 @@ static cc_status sv_finish(const int64_t* off, const uint32_t* adj, uint32_t* P,
     CC_CUDA_TRY(cudaMemcpyAsync(&cand, &ctl->cand_count, sizeof(cand), cudaMemcpyDeviceToHost, s));
     CC_CUDA_TRY(cudaStreamSynchronize(s));
     if (cand == 0) return CC_OK;
-    const int sms = num_sms();
     const unsigned long long nbk = (cand + kFTile - 1) / kFTile;
     uint32_t *deg = nullptr, *bits = nullptr;
     unsigned long long *bsum = nullptr, *tot = nullptr;
@@ -1374,7 +1604,7 @@ static cc_status sv_finish(const int64_t* off, const uint32_t* adj, uint32_t* P,
         CC_CUDA_TRY(scratch_alloc((void**)&deg, sizeof(uint32_t) * cand, s));
         CC_CUDA_TRY(scratch_alloc((void**)&bsum, sizeof(unsigned long long) * nbk, s));
         CC_CUDA_TRY(scratch_alloc((void**)&tot, sizeof(unsigned long long), s));
-        k_sv_degree<<<sms * 8, kBlock, 0, s>>>(off, cq, ctl, skip_prefix, deg);
+        k_sv_degree<<<grid_blocks(8), kBlock, 0, s>>>(off, cq, ctl, skip_prefix, deg);
         CC_LAUNCH_CHECK("k_sv_degree");
         k_sv_blocksum<<<(unsigned)nbk, kBlock, 0, s>>>(deg, cand, bsum);
         CC_LAUNCH_CHECK("k_sv_blocksum");
@@ -1395,7 +1625,7 @@ static cc_status sv_finish(const int64_t* off, const uint32_t* adj, uint32_t* P,
             CC_CUDA_TRY(scratch_alloc((void**)&le[0], sizeof(LtEdge<SF>) * ne, s));
             CC_CUDA_TRY(scratch_alloc((void**)&le[1], sizeof(LtEdge<SF>) * ne, s));
             CC_CUDA_TRY(scratch_alloc((void**)&lcnt, 2 * sizeof(unsigned long long), s));
-            k_lt_init<SF><<<sms * 8, kBlock, 0, s>>>(edges, ne, (LtEdge<SF>*)le[0]);
+            k_lt_init<SF><<<grid_blocks(8), kBlock, 0, s>>>(edges, ne, (LtEdge<SF>*)le[0]);
             CC_LAUNCH_CHECK("k_lt_init");
             CC_CUDA_TRY(cudaMemcpyAsync(lcnt, &ne, sizeof(ne), cudaMemcpyHostToDevice, s));
             for (uint64_t round = 1;; ++round) {
@@ -1403,16 +1633,16 @@ static cc_status sv_finish(const int64_t* off, const uint32_t* adj, uint32_t* P,
                 k_sv_rootbits<<<nbv, kBlock, 0, s>>>(P, n, bits);
                 CC_LAUNCH_CHECK("k_sv_rootbits(LT)");
                 CC_CUDA_TRY(cudaMemsetAsync(changed, 0, sizeof(unsigned int), s));
-                k_lt_connect<SF><<<sms * 8, kBlock, 0, s>>>(P, (const LtEdge<SF>*)le[a], lcnt + a, bits, changed);
+                k_lt_connect<SF><<<grid_blocks(8), kBlock, 0, s>>>(P, (const LtEdge<SF>*)le[a], lcnt + a, bits, changed);
                 CC_LAUNCH_CHECK("k_lt_connect");
                 if constexpr (SF) {
-                    k_lt_record<<<sms * 8, kBlock, 0, s>>>(P, (const uint4*)le[a], lcnt + a, bits, F);
+                    k_lt_record<<<grid_blocks(8), kBlock, 0, s>>>(P, (const uint4*)le[a], lcnt + a, bits, F);
                     CC_LAUNCH_CHECK("k_lt_record");
                 }
                 cc_status r = launch_compress(P, n, nullptr, nullptr, s, "k_compress(LT FullShortcut)");
                 if (r) return r;
                 CC_CUDA_TRY(cudaMemsetAsync(lcnt + (a ^ 1), 0, sizeof(unsigned long long), s));
-                k_lt_alter<SF><<<sms * 8, kBlock, 0, s>>>(P, (const LtEdge<SF>*)le[a], lcnt + a, (LtEdge<SF>*)le[a ^ 1],
+                k_lt_alter<SF><<<grid_blocks(8), kBlock, 0, s>>>(P, (const LtEdge<SF>*)le[a], lcnt + a, (LtEdge<SF>*)le[a ^ 1],
                                                           lcnt + (a ^ 1));
                 CC_LAUNCH_CHECK("k_lt_alter");
                 unsigned long long left = 0;
@@ -1428,10 +1658,10 @@ static cc_status sv_finish(const int64_t* off, const uint32_t* adj, uint32_t* P,
             k_sv_rootbits<<<nbv, kBlock, 0, s>>>(P, n, bits);        // prev_labels[h] == h
             CC_LAUNCH_CHECK("k_sv_rootbits");
             CC_CUDA_TRY(cudaMemsetAsync(changed, 0, sizeof(unsigned int), s));
-            k_sv_hook<<<sms * 8, kBlock, 0, s>>>(P, edges, ne, bits, changed);
+            k_sv_hook<<<grid_blocks(8), kBlock, 0, s>>>(P, edges, ne, bits, changed);
             CC_LAUNCH_CHECK("k_sv_hook");
             if (SF) {
-                k_sv_record<<<sms * 8, kBlock, 0, s>>>(P, edges, ne, bits, F);
+                k_sv_record<<<grid_blocks(8), kBlock, 0, s>>>(P, edges, ne, bits, F);
                 CC_LAUNCH_CHECK("k_sv_record");
             }
             unsigned int h_changed = 0;
@@ -1478,7 +1708,7 @@ cc_status validate_csr(const int64_t* off, const uint32_t* adj, uint32_t n, int6
     unsigned int* err = nullptr;
     CC_CUDA_TRY(scratch_alloc((void**)&err, sizeof(unsigned int), s));
     CC_CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(unsigned int), s));
-    k_validate<<<num_sms() * 8, kBlock, 0, s>>>(off, adj, n, m, err);
+    k_validate<<<grid_blocks(8), kBlock, 0, s>>>(off, adj, n, m, err);
     CC_LAUNCH_CHECK("k_validate");
     unsigned int h = 0;
     CC_CUDA_TRY(cudaMemcpyAsync(&h, err, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -1495,7 +1725,7 @@ cc_status validate_csr(const int64_t* off, const uint32_t* adj, uint32_t n, int6
 // ---------------------------------------------------------------------------
 template <int MODE, bool SF, int VAR>
 static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_t m, uint32_t* P,
-                     uint32_t* edges, int64_t* num_edges, uint32_t* labels_out, const cc_opts& o,
+                     uint32_t* edges, int64_t* num_edges, uint32_t* labels_out, bool want_labels, const cc_opts& o,
                      cudaStream_t s)
 {
     const uint32_t k = o.kout_k;
@@ -1509,7 +1739,6 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
     const bool contract = k > 0 && !no_skip && (o.flags & CC_FLAG_CONTRACT);
     // sampling and link in one kernel (UF-Rem-CAS + SplitAtomicOne, k <= 2, in-place)
     const bool fused = MODE == 0 && k > 0 && k <= 2 && !contract && (o.flags & CC_FLAG_FUSED_LINK);
-    const int sms = num_sms();
     const uint32_t nw = (uint32_t)(((uint64_t)n + 31) / 32);
     const uint32_t nrb = (uint32_t)(((uint64_t)nw + kFTile - 1) / kFTile);
 
@@ -1519,12 +1748,16 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
     const uint64_t big_cap = std::max<uint64_t>(1, std::min<uint64_t>(n, (uint64_t)m / kBigDeg + 1));
     const uint64_t bm_words = ((uint64_t)n + 31) / 32;
     const uint32_t nfb = (uint32_t)(((uint64_t)n + kFTile - 1) / kFTile);
+    const uint64_t ntile = ((uint64_t)n + kCTile - 1) / kCTile;     // k_finish blocks = H6 tiles
+    const bool sv = (o.flags & (CC_FLAG_FINISH_SV | CC_FLAG_FINISH_CRFA)) != 0;
 
     Ctl* ctl = nullptr;
     uint32_t* bm = nullptr;
     uint32_t* cq = nullptr;
     uint2* pend = nullptr;
     uint32_t* big = nullptr;
+    uint32_t* wsum = nullptr;             // k_finish warp summaries + H5 tile hook flags (partial H6)
+    uint8_t* td = nullptr;
     uint2* F = nullptr;
     uint32_t* fcnt = nullptr;
     unsigned long long* foff = nullptr;
@@ -1543,6 +1776,8 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
         scratch_free(cq, s);
         scratch_free(pend, s);
         scratch_free(big, s);
+        scratch_free(wsum, s);
+        scratch_free(td, s);
         scratch_free(F, s);
         scratch_free(fcnt, s);
         scratch_free(foff, s);
@@ -1559,6 +1794,8 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
         CC_CUDA_TRY(scratch_alloc((void**)&cq, sizeof(uint32_t) * (size_t)n, s));
         if (k > 0 && !fused) CC_CUDA_TRY(scratch_alloc((void**)&pend, sizeof(uint2) * pend_cap, s));
         CC_CUDA_TRY(scratch_alloc((void**)&big, sizeof(uint32_t) * big_cap, s));
+        CC_CUDA_TRY(scratch_alloc((void**)&wsum, sizeof(uint32_t) * kSumPerTile * ntile, s));
+        CC_CUDA_TRY(scratch_alloc((void**)&td, ntile, s));
         if (SF) {
             CC_CUDA_TRY(scratch_alloc((void**)&F, sizeof(uint2) * (size_t)n, s));
             CC_CUDA_TRY(scratch_alloc((void**)&fcnt, sizeof(uint32_t) * nfb, s));
@@ -1589,7 +1826,7 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
         // zero-copy); from HBM two 4-byte loads of the same sector are cheaper
         const bool win = aligned16(adj) && mem_kind(adj, nullptr) == MEM_PINNED;
         if (fused) {
-            k_init_pf<<<sms * 16, kBlock, 0, s>>>(P, n, SF ? F : nullptr);
+            k_init_pf<<<grid_blocks(16), kBlock, 0, s>>>(P, n, SF ? F : nullptr);
             CC_LAUNCH_CHECK("k_init_pf");
             k_sample_link<VAR, SF><<<nblk0, kBlock, 0, s>>>(off, adj, n, m, k, o.seed, full_deg, P, F, bm,
                                                             o.counters);
@@ -1635,15 +1872,15 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
         // H2: the remaining sampled edges
         if (fused) {
         } else if (contract) {
-            k_link_contract<MODE, SF><<<sms * 8, kBlock, 0, s>>>(P, pend, ctl, rbw, Cc, rid, F, o.counters);
+            k_link_contract<MODE, SF><<<resident_grid(k_link_contract<MODE, SF>, kBlock), kBlock, 0, s>>>(P, pend, ctl, rbw, Cc, rid, F, o.counters);
             CC_LAUNCH_CHECK("k_link_contract");
-            k_contract_final<<<sms * 8, kBlock, 0, s>>>(Cc, rid, Rtot);
+            k_contract_final<<<grid_blocks(8), kBlock, 0, s>>>(Cc, rid, Rtot);
             CC_LAUNCH_CHECK("k_contract_final");
         } else if (k > 0 && MODE == 0 && !(o.flags & CC_FLAG_NO_REFILL)) {
-            k_link_refill<SF><<<sms * 8, kBlock, 0, s>>>(P, pend, &ctl->pend_count, 0, F, o.counters);
+            k_link_refill<SF><<<refill_grid<SF>(), kBlock, 0, s>>>(P, pend, &ctl->pend_count, 0, F, o.counters);
             CC_LAUNCH_CHECK("k_link_refill");
         } else if (k > 0) {
-            k_link_pending<MODE, SF><<<sms * 8, kBlock, 0, s>>>(P, pend, ctl, F, o.counters);
+            k_link_pending<MODE, SF><<<resident_grid(k_link_pending<MODE, SF>, kBlock), kBlock, 0, s>>>(P, pend, ctl, F, o.counters);
             CC_LAUNCH_CHECK("k_link_pending");
         }
         CC_CUDA_TRY(mark(CC_MARK_LINK));
@@ -1668,39 +1905,58 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
         if (o.timings) CC_CUDA_TRY(cudaEventRecord(ev[2], s));
         // H3 + H5
         {
-            const unsigned nb = (unsigned)(((uint64_t)n + kCTile - 1) / kCTile);
+#ifdef CC_FINISH_PERSIST
+#define K_FINISH k_finish_persist
+            const unsigned nb = std::min<unsigned>((unsigned)ntile, resident_grid(k_finish_persist<true, false, false>, kBlock));
+#else
+#define K_FINISH k_finish
+            const unsigned nb = (unsigned)ntile;
+#endif
             if (contract && aligned16(P) && o.counters)
-                k_finish<true, true, true><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters, rbw, rid);
+                K_FINISH<true, true, true><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters, rbw, rid, wsum, td);
             else if (contract && aligned16(P))
-                k_finish<true, false, true><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, nullptr, rbw, rid);
+                K_FINISH<true, false, true><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, nullptr, rbw, rid, wsum, td);
             else if (contract)
-                k_finish<false, true, true><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters, rbw, rid);
+                K_FINISH<false, true, true><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters, rbw, rid, wsum, td);
             else if (aligned16(P) && o.counters)
-                k_finish<true, true, false><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters, nullptr, nullptr);
+                K_FINISH<true, true, false><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters, nullptr, nullptr, wsum, td);
             else if (aligned16(P))
-                k_finish<true, false, false><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, nullptr, nullptr, nullptr);
+                K_FINISH<true, false, false><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, nullptr, nullptr, nullptr, wsum, td);
             else
-                k_finish<false, true, false><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters, nullptr, nullptr);
+                K_FINISH<false, true, false><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters, nullptr, nullptr, wsum, td);
+#undef K_FINISH
             CC_LAUNCH_CHECK("k_finish");
         }
         CC_CUDA_TRY(mark(CC_MARK_FINISH));
-        if (o.flags & (CC_FLAG_FINISH_SV | CC_FLAG_FINISH_CRFA)) {
+        if (sv) {
             cc_status r = sv_finish<SF>(off, adj, P, n, cq, ctl, skip_prefix, F, o.counters, s,
                                         (o.flags & CC_FLAG_FINISH_CRFA) != 0);
             if (r) return r;
         } else {
-            k_finish_proc<MODE, SF><<<sms * 8, kBlock, 0, s>>>(off, adj, P, cq, ctl, skip_prefix, big, big_cap, F,
-                                                               o.counters);
+            k_finish_proc<MODE, SF><<<resident_grid(k_finish_proc<MODE, SF>, kBlock), kBlock, 0, s>>>(
+                off, adj, P, cq, ctl, skip_prefix, big, big_cap, F, o.counters, td);
             CC_LAUNCH_CHECK("k_finish_proc");
-            k_finish_big<MODE, SF><<<sms * 2, 512, 0, s>>>(off, adj, P, big, big_cap, ctl, skip_prefix, F, o.counters);
+            k_finish_big<MODE, SF><<<resident_grid(k_finish_big<MODE, SF>, 512), 512, 0, s>>>(
+                off, adj, P, big, big_cap, ctl, skip_prefix, F, o.counters, td);
             CC_LAUNCH_CHECK("k_finish_big");
         }
         CC_CUDA_TRY(mark(CC_MARK_FINISH_BIG));
         if (o.timings) CC_CUDA_TRY(cudaEventRecord(ev[3], s));
-        // H6
-        {
+        // H6: the partial pass when the labels are P itself (k_relabel: only the tiles
+        // whose labels H5 changed), nothing when no labels are wanted (a spanning
+        // forest without labels), the full pass when they go to another buffer or
+        // after an SV / CRFA finish (whose rounds do not keep the tile summaries)
+        if (labels_out || sv) {
             cc_status r = launch_compress(P, n, labels_out, o.counters, s, "k_compress(H6)");
             if (r) return r;
+        } else if (want_labels) {
+            if (o.counters)
+                k_relabel<true><<<resident_grid(k_relabel<true>, kBlock), kBlock, 0, s>>>(P, n, ctl, no_skip, wsum, td,
+                                                                                          o.counters);
+            else
+                k_relabel<false><<<resident_grid(k_relabel<false>, kBlock), kBlock, 0, s>>>(P, n, ctl, no_skip, wsum,
+                                                                                            td, nullptr);
+            CC_LAUNCH_CHECK("k_relabel(H6)");
         }
         CC_CUDA_TRY(mark(CC_MARK_COMPRESS));
         // H7
@@ -1734,24 +1990,24 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
 
 template <bool SF, int VAR>
 static cc_status dispatch_mode(const int64_t* off, const uint32_t* adj, uint32_t n, int64_t m, uint32_t* P,
-                               uint32_t* edges, int64_t* num_edges, uint32_t* labels_out, const cc_opts& o,
+                               uint32_t* edges, int64_t* num_edges, uint32_t* labels_out, bool want, const cc_opts& o,
                                cudaStream_t s)
 {
-    if (o.flags & CC_FLAG_UF_ASYNC) return run<2, SF, VAR>(off, adj, n, m, P, edges, num_edges, labels_out, o, s);
-    if (o.flags & CC_FLAG_HALVE) return run<1, SF, VAR>(off, adj, n, m, P, edges, num_edges, labels_out, o, s);
-    return run<0, SF, VAR>(off, adj, n, m, P, edges, num_edges, labels_out, o, s);
+    if (o.flags & CC_FLAG_UF_ASYNC) return run<2, SF, VAR>(off, adj, n, m, P, edges, num_edges, labels_out, want, o, s);
+    if (o.flags & CC_FLAG_HALVE) return run<1, SF, VAR>(off, adj, n, m, P, edges, num_edges, labels_out, want, o, s);
+    return run<0, SF, VAR>(off, adj, n, m, P, edges, num_edges, labels_out, want, o, s);
 }
 
 template <bool SF>
 static cc_status dispatch_variant(const int64_t* off, const uint32_t* adj, uint32_t n, int64_t m, uint32_t* P,
-                                  uint32_t* edges, int64_t* num_edges, uint32_t* labels_out, const cc_opts& o,
-                                  cudaStream_t s)
+                                  uint32_t* edges, int64_t* num_edges, uint32_t* labels_out, bool want,
+                                  const cc_opts& o, cudaStream_t s)
 {
     if (o.kout_variant == CC_VARIANT_HYBRID)
-        return dispatch_mode<SF, 1>(off, adj, n, m, P, edges, num_edges, labels_out, o, s);
+        return dispatch_mode<SF, 1>(off, adj, n, m, P, edges, num_edges, labels_out, want, o, s);
     if (o.kout_variant == CC_VARIANT_PURE)
-        return dispatch_mode<SF, 2>(off, adj, n, m, P, edges, num_edges, labels_out, o, s);
-    return dispatch_mode<SF, 0>(off, adj, n, m, P, edges, num_edges, labels_out, o, s);
+        return dispatch_mode<SF, 2>(off, adj, n, m, P, edges, num_edges, labels_out, want, o, s);
+    return dispatch_mode<SF, 0>(off, adj, n, m, P, edges, num_edges, labels_out, want, o, s);
 }
 
 cc_status static_pipeline(const int64_t* off, const uint32_t* adj, uint32_t n, int64_t m, uint32_t* P,
@@ -1762,13 +2018,14 @@ cc_status static_pipeline(const int64_t* off, const uint32_t* adj, uint32_t n, i
     // in-place cc_labels).  NULL: library scratch.  labels_out: where H6 writes
     // the labels when that is not P itself (NULL: nowhere).
     uint32_t* scratch = nullptr;
+    const bool want = P != nullptr || labels_out != nullptr;   // else: a forest without labels, no H6
     if (!P) {
         CC_CUDA_TRY(scratch_alloc((void**)&scratch, sizeof(uint32_t) * (size_t)n, s));
         P = scratch;
     }
     uint32_t* out = labels_out == P ? nullptr : labels_out;
-    const cc_status rc = sf ? dispatch_variant<true>(off, adj, n, m, P, edges, num_edges, out, o, s)
-                            : dispatch_variant<false>(off, adj, n, m, P, edges, num_edges, out, o, s);
+    const cc_status rc = sf ? dispatch_variant<true>(off, adj, n, m, P, edges, num_edges, out, want, o, s)
+                            : dispatch_variant<false>(off, adj, n, m, P, edges, num_edges, out, want, o, s);
     scratch_free(scratch, s);
     return rc;
 }

@@ -249,21 +249,39 @@ def test_spanning_forest_without_labels():
 
 
 def test_repeat_stress_random_options():
-    """Races must never change the answer: repeat with random k, variant, seed, flags."""
-    off, adj = gen.er(seed=21, n0=30000, pairs=45000, isolated=11)
-    want = oracle.cc_bfs(off, adj)
+    """Races must never change the answer: 1,000 repeats (SURVEY 8(c) test matrix)
+    with random k, variant, seed, flags AND random launch configurations (every
+    grid-strided kernel launched with a random block count, 1 .. 4x the default),
+    on fixtures, an ER graph spanning many tiles and C1 (BASELINE configs[0])."""
+    import inputs
+    graphs = [("er", *gen.er(seed=21, n0=30000, pairs=45000, isolated=11)), ("C1", *gen.er(seed=inputs.C1.seed))]
+    graphs += [(nm, o, a) for nm, o, a in fixtures() if nm in ("lmax_merges_smaller", "two_giants", "hubs",
+                                                                 "path_decreasing", "dups_and_loops")]
+    dev = [(nm, *to_dev(o, a), oracle.cc_bfs(o, a), o, a) for nm, o, a in graphs]
     rng = np.random.default_rng(1)
-    d_off, d_adj = to_dev(off, adj)
     flags_pool = [0, cc.FLAG_HALVE, cc.FLAG_UF_ASYNC, cc.FLAG_NO_SKIP, cc.FLAG_NO_MIDCOMPRESS, cc.FLAG_NO_DEGSKIP,
                   cc.FLAG_MIDCOMPRESS, cc.FLAG_FINISH_SV, cc.FLAG_CONTRACT, cc.FLAG_NO_REFILL,
                   cc.FLAG_FINISH_CRFA, cc.FLAG_FUSED_LINK]
-    for it in range(200):
-        k = int(rng.integers(0, 5))
-        variant = ["afforest", "hybrid", "pure"][int(rng.integers(0, 3))]
-        fl = int(rng.choice(flags_pool)) | int(rng.choice(flags_pool))
-        lab = pkg.connected_components(d_off, d_adj, k=k, variant=variant, seed=int(rng.integers(0, 1 << 30)),
-                                       flags=fl)
-        assert np.array_equal(u32(lab), want), (it, k, variant, fl)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    try:
+        for it in range(1000):
+            name, d_off, d_adj, want, off, adj = dev[it % len(dev)]
+            k = int(rng.integers(0, 5))
+            variant = ["afforest", "hybrid", "pure"][int(rng.integers(0, 3))]
+            fl = int(rng.choice(flags_pool)) | int(rng.choice(flags_pool))
+            grid = 0 if it % 7 == 0 else int(rng.integers(1, 4 * 8 * sms + 1))
+            cc.set_grid(grid)
+            seed = int(rng.integers(0, 1 << 30))
+            if it % 5 == 4:
+                edges, lab = pkg.spanning_forest(d_off, d_adj, k=k, variant=variant, seed=seed, flags=fl)
+                c = int(np.sum(want == np.arange(want.size)))
+                rc, bad = oracle.forest_check(off, adj, c, u32(edges).reshape(-1, 2))
+                assert rc == 0, (it, name, k, variant, fl, grid, oracle.FOREST_ERRORS[rc])
+            else:
+                lab = pkg.connected_components(d_off, d_adj, k=k, variant=variant, seed=seed, flags=fl)
+            assert np.array_equal(u32(lab), want), (it, name, k, variant, fl, grid)
+    finally:
+        cc.set_grid(0)
 
 
 def test_counters_and_timings():
@@ -393,3 +411,49 @@ def test_golden_fixtures_gpu():
             inc.batch(torch.from_numpy(p.reshape(1, 2)).cuda(), torch.zeros((0, 2), dtype=torch.int32, device="cuda"))
         assert np.array_equal(u32(inc.labels()), want["labels"]), name
         inc.close()
+
+
+# ---------------------------------------------------------------------------
+def _huge_graphs():
+    """Lists longer than kHugeDeg = 2^20 entries (the all-CTA slice bin of the
+    finish, cc_static.cu k_finish_big pass 1), P:4091-4100 over hub lists.
+    star: one centre (id 3) with 2^20 + 50 leaves, plus a few isolated ids.
+    two_hubs: hub 5 with 1.2M leaves and hub 7 with 1.3M leaves (the larger,
+    sampled L_max component at k = 1), joined only through vertex x, which is
+    the LAST entry of hub 5's list and adjacent to both hubs; and an extra
+    path 0-1-2 attached to hub 5's leaf 10 (so the final labels are 0)."""
+    n = (1 << 20) + 60
+    star = [(3, i) for i in range(4, n - 6)]
+    G = [("star", *oracle.csr_from_pairs(n, np.array(star, dtype=np.uint64)))]
+    a0, a1 = 10, 10 + 1_200_000
+    b0, b1 = a1, a1 + 1_300_000
+    x = b1 + 5
+    pairs = [(5, i) for i in range(a0, a1)] + [(7, i) for i in range(b0, b1)]
+    pairs += [(5, x), (7, x), (0, 1), (1, 2), (2, a0)]
+    G.append(("two_hubs", *oracle.csr_from_pairs(x + 3, np.array(pairs, dtype=np.uint64))))
+    return G
+
+
+@pytest.mark.parametrize("opt", [dict(k=0), dict(k=1), dict(k=1, flags=cc.FLAG_NO_SKIP), dict(k=2),
+                                 dict(k=0, flags=cc.FLAG_UF_ASYNC), dict(k=1, variant="hybrid", seed=3)],
+                         ids=lambda o: "-".join(f"{k}{v}" for k, v in o.items()))
+def test_huge_list_bin_labels_and_forest(opt):
+    """>2^20-entry lists: labels bit-exact and forests valid for k in {0, 1} (the
+    'No Sampling' regime of Table 3) and with the skip off."""
+    for name, off, adj in _huge_graphs():
+        n = off.size - 1
+        assert int(np.diff(off).max()) > (1 << 20) + 1, name
+        want = oracle.cc_bfs(off, adj)
+        c = int(np.sum(want == np.arange(n)))
+        d_off, d_adj = to_dev(off, adj)
+        ctr = torch.zeros(len(cc.COUNTER_FIELDS), dtype=torch.int64, device="cuda")
+        lab = pkg.connected_components(d_off, d_adj, counters=ctr, **opt)
+        assert np.array_equal(u32(lab), want), (name, opt)
+        edges, lab2 = pkg.spanning_forest(d_off, d_adj, **opt)
+        rc, bad = oracle.forest_check(off, adj, c, u32(edges).reshape(-1, 2))
+        assert rc == 0, (name, opt, oracle.FOREST_ERRORS[rc], bad)
+        assert np.array_equal(u32(lab2), want), (name, opt)
+        cnt = dict(zip(cc.COUNTER_FIELDS, ctr.cpu().tolist()))
+        if opt["k"] == 0 or opt.get("flags") == cc.FLAG_NO_SKIP or (name == "two_hubs" and opt["k"] == 1):
+            # the hub list went through the finish (the huge bin) -- not skipped
+            assert cnt["finish_edges"] > (1 << 20), (name, opt, cnt["finish_edges"])
