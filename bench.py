@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--amsf", action="store_true", help="NEXT-4 AMSF-NF-S study on C3/C4 with Exp(1) weights")
     p.add_argument("--table4", action="store_true", help="NEXT-2(b): Table 4 insert-only protocol, RM stream")
     p.add_argument("--eps", type=float, default=0.25)
+    p.add_argument("--graph", action="store_true",
+                   help="time cc_labels captured once into a CUDA graph and replayed (launch-bound configs: C1)")
     return p.parse_args()
 
 
@@ -389,6 +391,23 @@ def run_ours(a, rank, ws):
         flush.zero_()
         call()
     torch.cuda.synchronize()
+    step = call
+    if a.graph:
+        # one cc_labels call captured into a CUDA graph (kernels, stream-ordered scratch
+        # allocations, programmatic-dependent launches), replayed per step
+        gs = torch.cuda.Stream()
+        gs.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        lc0 = cc.launch_count()
+        with torch.cuda.graph(graph, stream=gs, capture_error_mode="thread_local"):
+            cc.cc_labels(d_off, d_adj, n, m, labels, cc.make_opts(k=a.k, variant=variant, flags=a.flags), gs)
+        torch.cuda.synchronize()
+        graph_kernels = cc.launch_count() - lc0        # libcc kernels in the captured graph
+        step = graph.replay
+        for _ in range(a.warmup):
+            flush.zero_()
+            step()
+        torch.cuda.synchronize()
 
     # ---- timed region: K steps, each bracketed by its own events; L2 flushed between steps
     clk = Clocks(torch.cuda.current_device())
@@ -405,14 +424,24 @@ def run_ours(a, rank, ws):
     for i in range(a.steps):
         flush.zero_()
         outer[i][0].record(stream)
-        call(marks=[e.cuda_event for e in marks[i]])
+        step()
         outer[i][1].record(stream)
     torch.cuda.synchronize()
     barrier(ws)
     torch.cuda.synchronize()
     launches = cc.launch_count() - l0
+    if a.graph:
+        launches = graph_kernels * a.steps          # replays launch the captured kernels on the device
     clocks = clk.stop()
+    # per-kernel breakdown: the same K steps again with an event at every kernel boundary
+    # (cc_opts.marks; the events serialise the launches, so the step time above is taken
+    # without them)
+    for i in range(a.steps):
+        flush.zero_()
+        call(marks=[e.cuda_event for e in marks[i]])
+    torch.cuda.synchronize()
     step_ms = [outer[i][0].elapsed_time(outer[i][1]) for i in range(a.steps)]
+    marked_ms = [marks[i][0].elapsed_time(marks[i][cc.NUM_MARKS - 1]) for i in range(a.steps)]
     kern_ms = {}
     for j in range(1, cc.NUM_MARKS):
         kern_ms[cc.MARK_NAMES[j]] = statistics.mean(marks[i][j - 1].elapsed_time(marks[i][j]) for i in range(a.steps))
@@ -487,8 +516,9 @@ def run_ours(a, rank, ws):
                        "l2": f"flushed between steps (write {flush.numel() * 4 >> 20} MiB > L2 {l2 >> 20} MiB); "
                              f"CSR {(8 * (n + 1) + 4 * m) / 1e9:.1f} GB > L2",
                        "parallelism": f"replicas x{ws}", "gen_s": round(gen_s, 2),
+                       "cuda_graph": bool(a.graph),
                        "l2_fetch_granularity": a.l2_fetch if a.l2_fetch >= 0 else "driver default"},
-            "t_ms": t_stats, "phase_ms": phase_ms,
+            "t_ms": t_stats, "phase_ms": phase_ms, "ms_per_step_with_kernel_marks": round(statistics.mean(marked_ms), 5),
             "roofline": roofline, "finish": finish, "sampling": sampling, "kernels": kernels,
             "counters": ctr, "byte_model_extra": extra, "gpu_launches": int(launches), "clocks": clocks}
 
@@ -678,14 +708,21 @@ def run_ours_incr(a, rank, ws, cfg):
     ans = torch.empty((nb, cfg.n_q), dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
 
-    def stream_once(ev=None):
+    sh = stream.cuda_stream
+
+    def stream_once(ev=None, outer=None):
         h = cc.Incr(n, flags=a.flags)
+        torch.cuda.synchronize()
+        if outer is not None:
+            outer[0].record(stream)
         for b in range(nb):
             if ev is not None:
                 ev[b][0].record(stream)
-            h.batch(ins[b], cfg.n_ins, qs[b], cfg.n_q, ans[b])
+            h.batch(ins[b], cfg.n_ins, qs[b], cfg.n_q, ans[b], sh)
             if ev is not None:
                 ev[b][1].record(stream)
+        if outer is not None:
+            outer[1].record(stream)
         torch.cuda.synchronize()
         h.close()
 
@@ -693,16 +730,21 @@ def run_ours_incr(a, rank, ws, cfg):
         stream_once()
     clk = Clocks(torch.cuda.current_device())
     clk.start()
-    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(nb)] for _ in range(a.steps)]
+    outer = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(a.steps)]
     barrier(ws)
     torch.cuda.synchronize()
     l0 = cc.launch_count()
     for s in range(a.steps):
-        stream_once(evs[s])
+        stream_once(outer=outer[s])           # one step = the whole 256-batch stream, events around it
     barrier(ws)
     launches = cc.launch_count() - l0
     clocks = clk.stop()
-    per_stream = [sum(evs[s][b][0].elapsed_time(evs[s][b][1]) for b in range(nb)) for s in range(a.steps)]
+    per_stream = [outer[s][0].elapsed_time(outer[s][1]) for s in range(a.steps)]
+    # per-batch latency: the same streams again with an event pair around every batch (the
+    # events serialise the batches, so the throughput above is taken without them)
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(nb)] for _ in range(a.steps)]
+    for s in range(a.steps):
+        stream_once(evs[s])
     batch_ms = sorted(evs[s][b][0].elapsed_time(evs[s][b][1]) for s in range(a.steps) for b in range(nb))
     mean_ms = reduce_max(statistics.mean(per_stream), ws)
     ops = nb * (cfg.n_ins + cfg.n_q)

@@ -113,9 +113,6 @@ typedef int cc_status;
                                           vertex in every round, as AMSF-NF-S is stated
                                           (P:1819-1822), instead of consulting the per-
                                           vertex [min, max] weight index first          */
-#define CC_FLAG_INSERT1     (1u << 17) /* cc_incr: one insert / query per thread (the round-1
-                                          kernels) instead of 4 with their first parent
-                                          reads issued together                            */
 #define CC_FLAG_WAIT_FREE   (1u << 8)  /* cc_incr: the wait-free type (1) setting (P:973-977,
                                           P:2663-2682): a batch's inserts and queries run
                                           concurrently in ONE kernel.  Answers are then

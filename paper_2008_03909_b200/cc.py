@@ -38,7 +38,6 @@ FLAG_FINISH_CRFA = 1 << 13
 FLAG_AMSF_NO_INDEX = 1 << 14
 FLAG_FUSED_LINK = 1 << 16
 FLAG_FIND_NAIVE = 1 << 15
-FLAG_INSERT1 = 1 << 17
 
 # every symbol include/cc.h and include/cc_bench.h declare
 EXPORTS = [

@@ -120,6 +120,8 @@ static __global__ void __launch_bounds__(kBlock, CC_REFILL_MINB) k_link_refill(
     uint32_t* P, const uint2* __restrict__ pend, const unsigned long long* count_dev, unsigned long long count_host,
     uint2* F, cc_counters* cnt)
 {
+    pdl_trigger();
+    pdl_wait();
     const unsigned lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     const unsigned long long total = count_dev ? *count_dev : count_host;
@@ -133,8 +135,8 @@ static __global__ void __launch_bounds__(kBlock, CC_REFILL_MINB) k_link_refill(
         navail = b0 < total ? (uint32_t)min(32ull, total - b0) : 0u;
         const bool ok = lane < navail;
         nb = ok ? pend[b0 + lane] : make_uint2(0u, 0u);
-        npu = ok ? ld_relaxed(P + nb.x) : 0u;
-        npv = ok ? ld_relaxed(P + nb.y) : 0u;
+        npu = ok ? ld_link(P + nb.x) : 0u;
+        npv = ok ? ld_link(P + nb.y) : 0u;
         chunk += nwarps;
     };
     fetch();
@@ -186,10 +188,10 @@ static __global__ void __launch_bounds__(kBlock, CC_REFILL_MINB) k_link_refill(
                 } else {
                     ++fails;
                     pu = old;
-                    pv = ld_relaxed(P + rv);
+                    pv = ld_link(P + rv);
                 }
             } else {
-                const uint32_t w = ld_relaxed(P + pu);       // SplitAtomicOne on ru
+                const uint32_t w = ld_link(P + pu);          // SplitAtomicOne on ru
                 if (w != pu) cas(P + ru, pu, w);
                 ru = pu;
                 pu = w;
@@ -218,6 +220,8 @@ static __global__ void __launch_bounds__(kBlock) k_forest_filter(const uint2* F,
                                                                  uint32_t* edges, int64_t* num_edges,
                                                                  const float* Fw = nullptr, float* out_w = nullptr)
 {
+    pdl_trigger();
+    pdl_wait();
     constexpr unsigned long long kAgg = 1ull << 62, kPre = 2ull << 62, kVal = (1ull << 62) - 1;
     constexpr int NW = kBlock / 32, SEG = kFTile / NW;      // slots per warp
     __shared__ uint32_t s_tile;

@@ -34,38 +34,12 @@ __global__ void __launch_bounds__(kBlock) k_iota(uint32_t* P, uint32_t n)
 template <int MODE>
 __global__ void __launch_bounds__(kBlock) k_insert(uint32_t* P, const uint2* __restrict__ ins, int64_t n_ins)
 {
+    pdl_trigger();                                // the next batch's kernel may be scheduled now
+    pdl_wait();                                   // ... and this one starts after the previous kernel
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_ins) return;
     const uint2 e = ins[i];
     link<MODE>(P, e.x, e.y, NoForest{});
-}
-
-// Batched form (the default for UF-Rem-CAS): each thread takes kIB inserts spaced
-// one block apart (coalesced pair loads) and issues all 2 kIB first parent reads
-// together, then enters the Rem loop of each with them (link_rem_from) -- kIB
-// times the memory-level parallelism of one link per thread.  Same unions, same
-// partition; only the first reads move.
-constexpr int kIB = 4;
-
-template <bool HALVE>
-__global__ void __launch_bounds__(kBlock) k_insert4(uint32_t* P, const uint2* __restrict__ ins, int64_t n_ins)
-{
-    const int64_t base = (int64_t)blockIdx.x * (kBlock * kIB) + threadIdx.x;
-    uint2 e[kIB];
-    uint32_t pu[kIB], pv[kIB];
-#pragma unroll
-    for (int q = 0; q < kIB; ++q) {
-        const int64_t i = base + (int64_t)q * kBlock;
-        e[q] = i < n_ins ? ins[i] : make_uint2(0u, 0u);
-    }
-#pragma unroll
-    for (int q = 0; q < kIB; ++q) {
-        pu[q] = ld_relaxed(P + e[q].x);
-        pv[q] = ld_relaxed(P + e[q].y);
-    }
-#pragma unroll
-    for (int q = 0; q < kIB; ++q)
-        if (pu[q] != pv[q]) link_rem_from<HALVE>(P, e[q].x, e[q].y, pu[q], pv[q], NoForest{});
 }
 
 // Queries run after the insert kernel: no hook can happen concurrently, so
@@ -84,43 +58,12 @@ __device__ __forceinline__ uint32_t query_find(uint32_t* P, uint32_t x)
     else return find_halve_quiet(P, x);
 }
 
-// Default queries (FIND 0, path halving with plain stores) batched like
-// k_insert4: kIB queries per thread, the 2 kIB first parent reads issued
-// together; a query whose two first parents agree is answered without a walk.
-__global__ void __launch_bounds__(kBlock) k_query4(uint32_t* P, const uint2* __restrict__ q, int64_t n_q,
-                                                   uint8_t* __restrict__ ans)
-{
-    const int64_t base = (int64_t)blockIdx.x * (kBlock * kIB) + threadIdx.x;
-    uint2 e[kIB];
-    uint32_t pa[kIB], pb[kIB];
-#pragma unroll
-    for (int k = 0; k < kIB; ++k) {
-        const int64_t i = base + (int64_t)k * kBlock;
-        e[k] = i < n_q ? q[i] : make_uint2(0u, 0u);
-    }
-#pragma unroll
-    for (int k = 0; k < kIB; ++k) {
-        pa[k] = ld_relaxed(P + e[k].x);
-        pb[k] = ld_relaxed(P + e[k].y);
-    }
-#pragma unroll
-    for (int k = 0; k < kIB; ++k) {
-        const int64_t i = base + (int64_t)k * kBlock;
-        if (i >= n_q) break;
-        uint8_t a = 1;
-        if (pa[k] != pb[k]) {
-            const uint32_t ra = pa[k] == e[k].x ? pa[k] : find_halve_quiet(P, pa[k]);
-            const uint32_t rb = pb[k] == e[k].y ? pb[k] : find_halve_quiet(P, pb[k]);
-            a = ra == rb ? 1 : 0;
-        }
-        ans[i] = a;
-    }
-}
-
 template <int FIND>
 __global__ void __launch_bounds__(kBlock) k_query(uint32_t* P, const uint2* __restrict__ q, int64_t n_q,
                                                   uint8_t* __restrict__ ans)
 {
+    pdl_trigger();                                // the next batch's kernel may be scheduled now
+    pdl_wait();                                   // ... and this one starts after the previous kernel
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_q) return;
     const uint2 e = q[i];
@@ -173,13 +116,16 @@ __global__ void __launch_bounds__(kBlock) k_mixed(uint32_t* P, const uint2* __re
 // insert/query barrier, P:986-993 -- and answers all queries: one launch
 // instead of two.  The hooks are device-scope CAS and the query reads are
 // relaxed device-scope loads, so the barrier also orders their visibility.
-constexpr int64_t kSmallBatch = 8192;
+constexpr int64_t kSmallBatch = 256;      // one cc_incr_batch call: above this, two PDL kernels
+constexpr int64_t kSmallBatches = 8192;   // cc_incr_batches: every batch up to this -> one CTA walks them all
 
 template <int MODE, int FIND>
 __global__ void __launch_bounds__(1024) k_small_batch(uint32_t* P, const uint2* __restrict__ ins, int64_t n_ins,
                                                       const uint2* __restrict__ q, int64_t n_q,
                                                       uint8_t* __restrict__ ans)
 {
+    pdl_trigger();                                // the next batch's kernel may be scheduled now
+    pdl_wait();                                   // ... and this one starts after the previous kernel
     for (int64_t i = threadIdx.x; i < n_ins; i += blockDim.x) {
         const uint2 e = ins[i];
         link<MODE>(P, e.x, e.y, NoForest{});
@@ -240,7 +186,6 @@ __global__ void __launch_bounds__(kBlock) k_labels(uint32_t* P, uint32_t n, uint
 }
 
 static unsigned nblocks(int64_t count) { return (unsigned)((count + kBlock - 1) / kBlock); }
-static unsigned nblocks4(int64_t count) { return (unsigned)((count + kBlock * kIB - 1) / (kBlock * kIB)); }
 
 static cc_status insert_query(cc_incr* h, const uint32_t* ins, int64_t n_ins, const uint32_t* qs, int64_t n_q,
                               uint8_t* ans, cudaStream_t s)
@@ -270,19 +215,15 @@ static cc_status insert_query(cc_incr* h, const uint32_t* ins, int64_t n_ins, co
         const uint2* e = reinterpret_cast<const uint2*>(ins);
         const uint2* q = reinterpret_cast<const uint2*>(qs);
         const int find = (h->flags & CC_FLAG_FIND_SPLIT) ? 1 : (h->flags & CC_FLAG_FIND_NAIVE) ? 2 : 0;
-        if (h->flags & CC_FLAG_UF_ASYNC) {
-            if (find == 1) k_small_batch<2, 1><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
-            else if (find == 2) k_small_batch<2, 2><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
-            else k_small_batch<2, 0><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
-        } else if (h->flags & CC_FLAG_HALVE) {
-            if (find == 1) k_small_batch<1, 1><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
-            else if (find == 2) k_small_batch<1, 2><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
-            else k_small_batch<1, 0><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
-        } else {
-            if (find == 1) k_small_batch<0, 1><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
-            else if (find == 2) k_small_batch<0, 2><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
-            else k_small_batch<0, 0><<<1, 1024, 0, s>>>(h->P, e, n_ins, q, n_q, ans);
-        }
+        // one warp per 32 operations, up to 1024 threads: a 10-op batch is one warp
+        const int64_t mx = std::max(n_ins, n_q);
+        const unsigned thr = (unsigned)std::min<int64_t>(1024, std::max<int64_t>(32, (mx + 31) / 32 * 32));
+        const int mode = (h->flags & CC_FLAG_UF_ASYNC) ? 2 : (h->flags & CC_FLAG_HALVE) ? 1 : 0;
+        void (*kern)(uint32_t*, const uint2*, int64_t, const uint2*, int64_t, uint8_t*) =
+            mode == 2 ? (find == 1 ? k_small_batch<2, 1> : find == 2 ? k_small_batch<2, 2> : k_small_batch<2, 0>)
+            : mode == 1 ? (find == 1 ? k_small_batch<1, 1> : find == 2 ? k_small_batch<1, 2> : k_small_batch<1, 0>)
+                        : (find == 1 ? k_small_batch<0, 1> : find == 2 ? k_small_batch<0, 2> : k_small_batch<0, 0>);
+        CC_CUDA_TRY(launch_pdl(kern, 1, thr, s, h->P, e, n_ins, q, n_q, ans));
         CC_LAUNCH_CHECK("k_small_batch");
         return CC_OK;
     }
@@ -298,21 +239,25 @@ static cc_status insert_query(cc_incr* h, const uint32_t* ins, int64_t n_ins, co
     }
     if (n_ins > 0) {
         const uint2* e = reinterpret_cast<const uint2*>(ins);
-        if (h->flags & CC_FLAG_UF_ASYNC) k_insert<2><<<nblocks(n_ins), kBlock, 0, s>>>(h->P, e, n_ins);
-        else if (h->flags & CC_FLAG_HALVE) k_insert<1><<<nblocks(n_ins), kBlock, 0, s>>>(h->P, e, n_ins);
-        // (the static path's lane-refill kernel measured slower here: 26.1 vs 28.0 G ops/s
-        // on C5 -- random u, and one link per thread already fills the machine)
-        else if (h->flags & CC_FLAG_INSERT1) k_insert<0><<<nblocks(n_ins), kBlock, 0, s>>>(h->P, e, n_ins);
-        else k_insert4<false><<<nblocks4(n_ins), kBlock, 0, s>>>(h->P, e, n_ins);
+        cudaError_t le;
+        if (h->flags & CC_FLAG_UF_ASYNC) le = launch_pdl(k_insert<2>, nblocks(n_ins), kBlock, s, h->P, e, n_ins);
+        else if (h->flags & CC_FLAG_HALVE) le = launch_pdl(k_insert<1>, nblocks(n_ins), kBlock, s, h->P, e, n_ins);
+        // one link per thread: measured faster on C5 than the static path's lane-refill
+        // kernel (28.0 vs 26.1 G ops/s) and than 2 or 4 links per thread with their
+        // first parent reads batched (26.3 / 24.4 vs 28.4 G ops/s: a quarter of the
+        // threads, each walking its links one after another)
+        else le = launch_pdl(k_insert<0>, nblocks(n_ins), kBlock, s, h->P, e, n_ins);
+        CC_CUDA_TRY(le);
         CC_LAUNCH_CHECK("k_insert");
     }
     // ---- kernel boundary: the insert/query barrier of type (3) ----
     if (n_q > 0) {
         const uint2* q = reinterpret_cast<const uint2*>(qs);
-        if (h->flags & CC_FLAG_FIND_SPLIT) k_query<1><<<nblocks(n_q), kBlock, 0, s>>>(h->P, q, n_q, ans);
-        else if (h->flags & CC_FLAG_FIND_NAIVE) k_query<2><<<nblocks(n_q), kBlock, 0, s>>>(h->P, q, n_q, ans);
-        else if (h->flags & CC_FLAG_INSERT1) k_query<0><<<nblocks(n_q), kBlock, 0, s>>>(h->P, q, n_q, ans);
-        else k_query4<<<nblocks4(n_q), kBlock, 0, s>>>(h->P, q, n_q, ans);
+        cudaError_t le;
+        if (h->flags & CC_FLAG_FIND_SPLIT) le = launch_pdl(k_query<1>, nblocks(n_q), kBlock, s, h->P, q, n_q, ans);
+        else if (h->flags & CC_FLAG_FIND_NAIVE) le = launch_pdl(k_query<2>, nblocks(n_q), kBlock, s, h->P, q, n_q, ans);
+        else le = launch_pdl(k_query<0>, nblocks(n_q), kBlock, s, h->P, q, n_q, ans);
+        CC_CUDA_TRY(le);
         CC_LAUNCH_CHECK("k_query");
     }
     return CC_OK;
@@ -526,7 +471,7 @@ cc_status cc_incr_batches(cc_incr* h, int64_t nb, const int64_t* ins_counts, con
         if (e) { set_error("cc_incr_batches: vertex id >= n"); return CC_EINVAL; }
     }
     const bool host = k_ins != MEM_DEVICE || k_q != MEM_DEVICE || k_ans != MEM_DEVICE;
-    if (maxops <= kSmallBatch && !(h->flags & CC_FLAG_WAIT_FREE)) {
+    if (maxops <= kSmallBatches && !(h->flags & CC_FLAG_WAIT_FREE)) {
         int64_t* d_off = nullptr;
         CC_CUDA_TRY(scratch_alloc((void**)&d_off, sizeof(int64_t) * 2 * (size_t)(nb + 1), s));
         std::vector<int64_t> both(oi);

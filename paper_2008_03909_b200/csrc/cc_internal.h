@@ -60,6 +60,25 @@ constexpr int kBlock = 256;
         if (_e != cudaSuccess) return ::ccb::cuda_fail(_e, name); \
     } while (0)
 
+// Launch with programmatic dependent launch (PDL) allowed: the kernel may be
+// scheduled while the previous kernel of the stream still runs; it must execute
+// pdl_wait() before touching memory the previous kernel writes.
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStream_t s, Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // Device pipeline entry points (device pointers only; validated args).
 cc_status static_pipeline(const int64_t* off, const uint32_t* adj, uint32_t n, int64_t m, uint32_t* P,
                           uint32_t* labels_out, uint32_t* edges, int64_t* num_edges, bool sf, const cc_opts& o,

@@ -85,6 +85,8 @@ __global__ void __launch_bounds__(kBlock, 3) k_sample_init(
     uint64_t seed, uint32_t full_deg, uint32_t* __restrict__ P, uint2* __restrict__ F,
     uint2* __restrict__ pend, uint32_t* __restrict__ bm, uint2* __restrict__ rbw, Ctl* ctl, cc_counters* cnt)
 {
+    pdl_trigger();
+    pdl_wait();
     __shared__ uint32_t s_wtot[kBlock / 32];
     __shared__ unsigned long long s_wbase[kBlock / 32];
     const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -525,6 +527,8 @@ template <bool CNT>
 __global__ void __launch_bounds__(kBlock, CC_COMPRESS_MINB) k_compress(uint32_t* P, uint32_t n, uint32_t* out,
                                                                        cc_counters* cnt, const Ctl* gate)
 {
+    pdl_trigger();
+    pdl_wait();
     if (gate && gate->skip_mid) return;
     uint32_t writes = 0, gathers = 0;
     const uint64_t ntiles = ((uint64_t)n + kCTile - 1) / kCTile;
@@ -573,6 +577,8 @@ __global__ void __launch_bounds__(kBlock, CC_COMPRESS_MINB) k_compress(uint32_t*
 __global__ void __launch_bounds__(kBlock) k_compress_scalar(uint32_t* P, uint32_t n, uint32_t* out, cc_counters* cnt,
                                                             const Ctl* gate)
 {
+    pdl_trigger();
+    pdl_wait();
     if (gate && gate->skip_mid) return;
     const uint64_t v64 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t writes = 0;
@@ -595,10 +601,10 @@ static cc_status launch_compress(uint32_t* P, uint32_t n, uint32_t* out, cc_coun
     // costs one short wave, not 65k empty blocks; otherwise one block per tile
     const uint64_t ntiles = ((uint64_t)n + kCTile - 1) / kCTile;
     const unsigned grid = (unsigned)(gate ? std::min<uint64_t>(ntiles, (uint64_t)grid_blocks(8)) : ntiles);
-    if (aligned16(P) && aligned16(out) && cnt) k_compress<true><<<grid, kBlock, 0, s>>>(P, n, out, cnt, gate);
-    else if (aligned16(P) && aligned16(out)) k_compress<false><<<grid, kBlock, 0, s>>>(P, n, out, nullptr, gate);
+    if (aligned16(P) && aligned16(out) && cnt) CC_CUDA_TRY(launch_pdl(k_compress<true>, grid, kBlock, s, P, n, out, cnt, gate));
+    else if (aligned16(P) && aligned16(out)) CC_CUDA_TRY(launch_pdl(k_compress<false>, grid, kBlock, s, P, n, out, nullptr, gate));
     else
-        k_compress_scalar<<<(unsigned)(((uint64_t)n + kBlock - 1) / kBlock), kBlock, 0, s>>>(P, n, out, cnt, gate);
+        CC_CUDA_TRY(launch_pdl(k_compress_scalar, (unsigned)(((uint64_t)n + kBlock - 1) / kBlock), kBlock, s, P, n, out, cnt, gate));
     CC_LAUNCH_CHECK(what);
     return CC_OK;
 }
@@ -616,6 +622,8 @@ constexpr uint64_t PROBE_STREAM = 18;
 __global__ void __launch_bounds__(1024) k_probe(const uint32_t* P, uint32_t n, uint64_t seed, Ctl* ctl,
                                                 cc_counters* cnt)
 {
+    pdl_trigger();
+    pdl_wait();
     __shared__ uint32_t s_deep;
     if (threadIdx.x == 0) s_deep = 0;
     __syncthreads();
@@ -647,6 +655,8 @@ template <int MODE, bool SF>
 __global__ void __launch_bounds__(kBlock) k_link_pending(
     uint32_t* P, const uint2* __restrict__ pend, const Ctl* ctl, uint2* F, cc_counters* cnt)
 {
+    pdl_trigger();
+    pdl_wait();
     const unsigned long long total = ctl->pend_count;
     const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
     const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -873,6 +883,8 @@ __global__ void __launch_bounds__(1024) k_identify(uint32_t* P, uint32_t n, uint
                                                    uint32_t samples, const uint32_t* force, Ctl* ctl,
                                                    uint32_t* lmax_out, const uint2* rbw, const uint32_t* rid)
 {
+    pdl_trigger();
+    pdl_wait();
     __shared__ uint32_t keys[kIdTable];
     __shared__ uint32_t cnts[kIdTable];
     __shared__ unsigned long long best[32];
@@ -1076,46 +1088,14 @@ __global__ void __launch_bounds__(kBlock, CC_FINISH_MINB) k_finish(uint32_t* P, 
                                                    const uint2* __restrict__ rbw, const uint32_t* __restrict__ rid,
                                                    uint32_t* __restrict__ wsum, uint8_t* __restrict__ td)
 {
+    pdl_trigger();
+    pdl_wait();
     const uint32_t lmax = no_skip ? kSentinel : ctl->lmax;
     const uint64_t tile = blockIdx.x;
     const bool full = VEC && (tile + 1) * kCTile <= n;
     uint32_t pp[kCV], w0, w1, writes = 0, gathers = 0;
     finish_load(P, bm, n, tile, full, pp, w0, w1);
     finish_tile<CNT, CONTRACT>(P, n, tile, full, pp, w0, w1, lmax, ctl, cq, rbw, rid, wsum, td, writes, gathers);
-    if (CNT) {
-        warp_count(&cnt->compress_writes, writes);
-        warp_count(&cnt->finish_gathers, gathers);
-    }
-}
-
-// Persistent variant (CC_FINISH_PERSIST): each block walks tiles blockIdx.x,
-// + gridDim.x, ... and issues the NEXT tile's P / bitmap loads before resolving
-// the current one's roots, so a tile's streaming reads overlap the previous
-// tile's gathers (twice the bytes in flight per thread).
-#ifndef CC_FINISH_PMINB
-#define CC_FINISH_PMINB 6
-#endif
-template <bool VEC, bool CNT, bool CONTRACT>
-__global__ void __launch_bounds__(kBlock, CC_FINISH_PMINB) k_finish_persist(
-    uint32_t* P, const uint32_t* __restrict__ bm, uint32_t n, Ctl* ctl, bool no_skip, uint32_t* cq, cc_counters* cnt,
-    const uint2* __restrict__ rbw, const uint32_t* __restrict__ rid, uint32_t* __restrict__ wsum,
-    uint8_t* __restrict__ td)
-{
-    const uint32_t lmax = no_skip ? kSentinel : ctl->lmax;
-    const uint64_t ntiles = ((uint64_t)n + kCTile - 1) / kCTile;
-    uint32_t pp[kCV], w0 = 0, w1 = 0, writes = 0, gathers = 0;
-    uint64_t tile = blockIdx.x;
-    if (tile < ntiles) finish_load(P, bm, n, tile, VEC && (tile + 1) * kCTile <= n, pp, w0, w1);
-    for (; tile < ntiles; tile += gridDim.x) {
-        const bool full = VEC && (tile + 1) * kCTile <= n;
-        uint32_t cur[kCV];
-#pragma unroll
-        for (int s = 0; s < kCV; ++s) cur[s] = pp[s];
-        const uint32_t c0 = w0, c1 = w1;
-        const uint64_t nt = tile + gridDim.x;
-        if (nt < ntiles) finish_load(P, bm, n, nt, VEC && (nt + 1) * kCTile <= n, pp, w0, w1);
-        finish_tile<CNT, CONTRACT>(P, n, tile, full, cur, c0, c1, lmax, ctl, cq, rbw, rid, wsum, td, writes, gathers);
-    }
     if (CNT) {
         warp_count(&cnt->compress_writes, writes);
         warp_count(&cnt->finish_gathers, gathers);
@@ -1150,6 +1130,8 @@ __global__ void __launch_bounds__(kBlock) k_finish_proc(
     const uint32_t* __restrict__ cq, Ctl* ctl, uint32_t skip_prefix, uint32_t* big, unsigned long long big_cap,
     uint2* F, cc_counters* cnt, uint8_t* td)
 {
+    pdl_trigger();
+    pdl_wait();
     const unsigned long long total = ctl->cand_count;
     const unsigned lane = threadIdx.x & 31;
     const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1236,6 +1218,8 @@ __global__ void __launch_bounds__(512) k_finish_big(const int64_t* __restrict__ 
                                                     const Ctl* ctl, uint32_t skip_prefix, uint2* F, cc_counters* cnt,
                                                     uint8_t* td)
 {
+    pdl_trigger();
+    pdl_wait();
     __shared__ uint32_t s_ru;
     const unsigned long long nbig = ctl->big_count, nhuge = ctl->huge_count;
     uint32_t hooks = 0;
@@ -1285,6 +1269,8 @@ __global__ void __launch_bounds__(kBlock) k_relabel(uint32_t* P, uint32_t n, con
                                                     const uint32_t* __restrict__ wsum, const uint8_t* __restrict__ td,
                                                     cc_counters* cnt)
 {
+    pdl_trigger();
+    pdl_wait();
     const unsigned lane = threadIdx.x & 31;
     uint32_t lm = no_skip ? kSentinel : ctl->lmax;
     if (lm >= n) lm = kSentinel;                                      // a forced out-of-range L_max skips nothing
@@ -1425,23 +1411,20 @@ __global__ void k_sv_scan(unsigned long long* bsum, unsigned long long nb, unsig
     *total_edges = acc;
 }
 
-// one warp per 32 candidates: each candidate's list is copied cooperatively to
-// its slot range of the flat edge list
-__global__ void __launch_bounds__(kBlock) k_sv_fill(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
-                                                    const uint32_t* __restrict__ cq, const uint32_t* __restrict__ deg,
-                                                    const unsigned long long* __restrict__ bsum,
-                                                    unsigned long long total, uint32_t skip_prefix, uint2* edges)
+// Each candidate's start in the flat edge list (exclusive prefix of deg[]: the
+// block sums of k_sv_blocksum, scanned, plus a block-level scan).
+__global__ void __launch_bounds__(kBlock) k_sv_starts(const uint32_t* __restrict__ deg,
+                                                      const unsigned long long* __restrict__ bsum,
+                                                      unsigned long long total, unsigned long long* __restrict__ start)
 {
     const unsigned lane = threadIdx.x & 31;
     const uint64_t i = (uint64_t)blockIdx.x * kFTile + (uint64_t)threadIdx.x * kFItems;
-    // exclusive position of each of this thread's kFItems candidates
     unsigned long long c = 0, pos[kFItems];
 #pragma unroll
     for (int j = 0; j < kFItems; ++j) {
         pos[j] = c;
         c += (i + j < total) ? deg[i + j] : 0u;
     }
-    // block-level exclusive scan of c (64-bit) via warp shuffles + shared memory
     unsigned long long incl = c;
     for (int o = 1; o < 32; o <<= 1) {
         const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
@@ -1453,13 +1436,72 @@ __global__ void __launch_bounds__(kBlock) k_sv_fill(const int64_t* __restrict__ 
     unsigned long long wbase = 0;
     for (unsigned w = 0; w < (threadIdx.x >> 5); ++w) wbase += ws[w];
     const unsigned long long tbase = bsum[blockIdx.x] + wbase + incl - c;
-#pragma unroll 1
-    for (int j = 0; j < kFItems; ++j) {
-        if (i + j >= total) break;
-        const uint32_t u = cq[i + j];
-        const int64_t b = off[u] + skip_prefix;
-        const uint32_t d = deg[i + j];
-        for (uint32_t x = 0; x < d; ++x) edges[tbase + pos[j] + x] = make_uint2(u, adj[b + x]);
+#pragma unroll
+    for (int j = 0; j < kFItems; ++j)
+        if (i + j < total) start[i + j] = tbase + pos[j];
+}
+
+// Edge-parallel copy of the candidates' lists: a warp takes 32 candidates and
+// sweeps their concatenated lists 32 entries at a time (each lane finds its
+// entry's owner by a binary search over the warp's exclusive prefix), so a
+// hub's million-entry list is copied by many lanes, not one thread.
+// FILTER (every marked vertex is a candidate: no skip, or no sampling): an edge
+// between two candidates is materialised from both ends, so keep (u, v) only
+// when u < v or v is not a candidate -- half the edges, appended in any order.
+template <bool FILTER>
+__global__ void __launch_bounds__(kBlock) k_sv_copy(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                                                    const uint32_t* __restrict__ cq, const uint32_t* __restrict__ deg,
+                                                    const unsigned long long* __restrict__ start,
+                                                    unsigned long long total, uint32_t skip_prefix, uint2* edges,
+                                                    const uint32_t* __restrict__ bm, const Ctl* ctl, bool no_skip,
+                                                    unsigned long long* kept)
+{
+    const uint32_t lmax = no_skip ? kSentinel : ctl->lmax;
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    for (unsigned long long base = warp * 32; base < total; base += nwarps * 32) {
+        const unsigned long long i = base + lane;
+        const bool ok = i < total;
+        const uint32_t u = ok ? cq[i] : 0u;
+        const uint64_t d = ok ? deg[i] : 0u;
+        const int64_t b = ok ? off[u] + (int64_t)skip_prefix : 0;
+        const unsigned long long st = ok && !FILTER ? start[i] : 0ull;
+        uint64_t incl = d;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (unsigned)o) incl += t;
+        }
+        const uint64_t tot = __shfl_sync(0xffffffffu, incl, 31);
+        const uint64_t excl = incl - d;
+        for (uint64_t t0 = 0; t0 < tot; t0 += 32) {
+            const uint64_t t = t0 + lane;
+            int lo = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const uint64_t pe = __shfl_sync(0xffffffffu, excl, lo + step);
+                if (pe <= t) lo += step;
+            }
+            const uint32_t ou = __shfl_sync(0xffffffffu, u, lo);
+            const int64_t ob = __shfl_sync(0xffffffffu, b, lo);
+            const uint64_t oex = __shfl_sync(0xffffffffu, excl, lo);
+            const unsigned long long ost = __shfl_sync(0xffffffffu, st, lo);
+            if constexpr (FILTER) {
+                uint32_t v = 0;
+                bool keep = false;
+                if (t < tot) {
+                    v = adj[ob + (int64_t)(t - oex)];
+                    const bool cand_v = ((bm[v >> 5] >> (v & 31)) & 1u) && v != lmax;
+                    keep = ou < v || !cand_v;
+                }
+                const unsigned long long pos = warp_append(kept, keep ? 1u : 0u);
+                if (keep) edges[pos] = make_uint2(ou, v);
+            } else {
+                (void)ost;
+                if (t < tot) edges[ost + (t - oex)] = make_uint2(ou, adj[ob + (int64_t)(t - oex)]);
+            }
+        }
     }
 }
 
@@ -1586,7 +1628,7 @@ __global__ void __launch_bounds__(kBlock) k_lt_alter(const uint32_t* P, const Lt
 template <bool SF>
 static cc_status sv_finish(const int64_t* off, const uint32_t* adj, uint32_t* P, uint32_t n, const uint32_t* cq,
                            Ctl* ctl, uint32_t skip_prefix, uint2* F, cc_counters* cnt, cudaStream_t s,
-                           bool crfa = false)
+                           bool crfa, const uint32_t* bm, bool no_skip, bool all_marked_candidates)
 {
     void* le[2] = {nullptr, nullptr};
     unsigned long long* lcnt = nullptr;
@@ -1596,7 +1638,7 @@ static cc_status sv_finish(const int64_t* off, const uint32_t* adj, uint32_t* P,
     if (cand == 0) return CC_OK;
     const unsigned long long nbk = (cand + kFTile - 1) / kFTile;
     uint32_t *deg = nullptr, *bits = nullptr;
-    unsigned long long *bsum = nullptr, *tot = nullptr;
+    unsigned long long *bsum = nullptr, *tot = nullptr, *starts = nullptr;
     uint2* edges = nullptr;
     unsigned int* changed = nullptr;
     cc_status rc = CC_OK;
@@ -1617,8 +1659,22 @@ static cc_status sv_finish(const int64_t* off, const uint32_t* adj, uint32_t* P,
         CC_CUDA_TRY(scratch_alloc((void**)&edges, sizeof(uint2) * ne, s));
         CC_CUDA_TRY(scratch_alloc((void**)&bits, sizeof(uint32_t) * (((uint64_t)n + 31) / 32), s));
         CC_CUDA_TRY(scratch_alloc((void**)&changed, sizeof(unsigned int), s));
-        k_sv_fill<<<(unsigned)nbk, kBlock, 0, s>>>(off, adj, cq, deg, bsum, cand, skip_prefix, edges);
-        CC_LAUNCH_CHECK("k_sv_fill");
+        if (all_marked_candidates) {
+            CC_CUDA_TRY(cudaMemsetAsync(tot, 0, sizeof(unsigned long long), s));
+            k_sv_copy<true><<<grid_blocks(8), kBlock, 0, s>>>(off, adj, cq, deg, nullptr, cand, skip_prefix, edges,
+                                                                bm, ctl, no_skip, tot);
+            CC_LAUNCH_CHECK("k_sv_copy");
+            CC_CUDA_TRY(cudaMemcpyAsync(&ne, tot, sizeof(ne), cudaMemcpyDeviceToHost, s));
+            CC_CUDA_TRY(cudaStreamSynchronize(s));
+            if (ne == 0) return CC_OK;
+        } else {
+            CC_CUDA_TRY(scratch_alloc((void**)&starts, sizeof(unsigned long long) * cand, s));
+            k_sv_starts<<<(unsigned)nbk, kBlock, 0, s>>>(deg, bsum, cand, starts);
+            CC_LAUNCH_CHECK("k_sv_starts");
+            k_sv_copy<false><<<grid_blocks(8), kBlock, 0, s>>>(off, adj, cq, deg, starts, cand, skip_prefix, edges,
+                                                                 nullptr, ctl, no_skip, nullptr);
+            CC_LAUNCH_CHECK("k_sv_copy");
+        }
         const unsigned nbv = (unsigned)(((uint64_t)n + kBlock - 1) / kBlock);
         if (crfa) {
             // Liu-Tarjan CRFA: rounds until Alter leaves no edge
@@ -1679,6 +1735,7 @@ static cc_status sv_finish(const int64_t* off, const uint32_t* adj, uint32_t* P,
     scratch_free(deg, s);
     scratch_free(bsum, s);
     scratch_free(tot, s);
+    scratch_free(starts, s);
     scratch_free(edges, s);
     scratch_free(bits, s);
     scratch_free(changed, s);
@@ -1832,17 +1889,17 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
                                                             o.counters);
             CC_LAUNCH_CHECK("k_sample_link");
         } else if (contract && win)
-            k_sample_init<VAR, SF, true, true><<<nblk0, kBlock, 0, s>>>(off, adj, n, m, k, o.seed, full_deg, P, F,
-                                                                          pend, bm, rbw, ctl, o.counters);
+            CC_CUDA_TRY(launch_pdl(k_sample_init<VAR, SF, true, true>, nblk0, kBlock, s, off, adj, n, m, k, o.seed, full_deg, P, F,
+                                                                          pend, bm, rbw, ctl, o.counters));
         else if (contract)
-            k_sample_init<VAR, SF, false, true><<<nblk0, kBlock, 0, s>>>(off, adj, n, m, k, o.seed, full_deg, P, F,
-                                                                           pend, bm, rbw, ctl, o.counters);
+            CC_CUDA_TRY(launch_pdl(k_sample_init<VAR, SF, false, true>, nblk0, kBlock, s, off, adj, n, m, k, o.seed, full_deg, P, F,
+                                                                           pend, bm, rbw, ctl, o.counters));
         else if (win)
-            k_sample_init<VAR, SF, true, false><<<nblk0, kBlock, 0, s>>>(off, adj, n, m, k, o.seed, full_deg, P, F,
-                                                                           pend, bm, nullptr, ctl, o.counters);
+            CC_CUDA_TRY(launch_pdl(k_sample_init<VAR, SF, true, false>, nblk0, kBlock, s, off, adj, n, m, k, o.seed, full_deg, P, F,
+                                                                           pend, bm, nullptr, ctl, o.counters));
         else
-            k_sample_init<VAR, SF, false, false><<<nblk0, kBlock, 0, s>>>(off, adj, n, m, k, o.seed, full_deg, P, F,
-                                                                            pend, bm, nullptr, ctl, o.counters);
+            CC_CUDA_TRY(launch_pdl(k_sample_init<VAR, SF, false, false>, nblk0, kBlock, s, off, adj, n, m, k, o.seed, full_deg, P, F,
+                                                                            pend, bm, nullptr, ctl, o.counters));
         if (!fused) CC_LAUNCH_CHECK("k_sample_init");
         CC_CUDA_TRY(mark(CC_MARK_INIT));
         if (contract) {
@@ -1862,7 +1919,7 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
             // (grid-like inputs); k_probe decides on the device unless a flag forces it
             const bool force = (o.flags & CC_FLAG_MIDCOMPRESS) != 0;
             if (!force) {
-                k_probe<<<1, 1024, 0, s>>>(P, n, o.seed, ctl, o.counters);
+                CC_CUDA_TRY(launch_pdl(k_probe, 1, 1024, s, P, n, o.seed, ctl, o.counters));
                 CC_LAUNCH_CHECK("k_probe");
             }
             cc_status r = launch_compress(P, n, nullptr, nullptr, s, "k_compress(mid)", force ? nullptr : ctl);
@@ -1877,10 +1934,10 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
             k_contract_final<<<grid_blocks(8), kBlock, 0, s>>>(Cc, rid, Rtot);
             CC_LAUNCH_CHECK("k_contract_final");
         } else if (k > 0 && MODE == 0 && !(o.flags & CC_FLAG_NO_REFILL)) {
-            k_link_refill<SF><<<refill_grid<SF>(), kBlock, 0, s>>>(P, pend, &ctl->pend_count, 0, F, o.counters);
+            CC_CUDA_TRY(launch_pdl(k_link_refill<SF>, refill_grid<SF>(), kBlock, s, P, pend, &ctl->pend_count, 0, F, o.counters));
             CC_LAUNCH_CHECK("k_link_refill");
         } else if (k > 0) {
-            k_link_pending<MODE, SF><<<resident_grid(k_link_pending<MODE, SF>, kBlock), kBlock, 0, s>>>(P, pend, ctl, F, o.counters);
+            CC_CUDA_TRY(launch_pdl(k_link_pending<MODE, SF>, resident_grid(k_link_pending<MODE, SF>, kBlock), kBlock, s, P, pend, ctl, F, o.counters));
             CC_LAUNCH_CHECK("k_link_pending");
         }
         CC_CUDA_TRY(mark(CC_MARK_LINK));
@@ -1899,45 +1956,40 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
         CC_CUDA_TRY(mark(CC_MARK_SAMPLED));
         if (o.timings) CC_CUDA_TRY(cudaEventRecord(ev[1], s));
         // H4 (roots of the sampled forest; identical before or after H3)
-        k_identify<<<1, 1024, 0, s>>>(P, n, o.seed, o.samples, o.lmax_force, ctl, o.lmax_out, rbw, rid);
+        CC_CUDA_TRY(launch_pdl(k_identify, 1, 1024, s, P, n, o.seed, o.samples, o.lmax_force, ctl, o.lmax_out, rbw, rid));
         CC_LAUNCH_CHECK("k_identify");
         CC_CUDA_TRY(mark(CC_MARK_IDENTIFY));
         if (o.timings) CC_CUDA_TRY(cudaEventRecord(ev[2], s));
         // H3 + H5
         {
-#ifdef CC_FINISH_PERSIST
-#define K_FINISH k_finish_persist
-            const unsigned nb = std::min<unsigned>((unsigned)ntile, resident_grid(k_finish_persist<true, false, false>, kBlock));
-#else
-#define K_FINISH k_finish
             const unsigned nb = (unsigned)ntile;
-#endif
             if (contract && aligned16(P) && o.counters)
-                K_FINISH<true, true, true><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters, rbw, rid, wsum, td);
+                CC_CUDA_TRY(launch_pdl(k_finish<true, true, true>, nb, kBlock, s, P, bm, n, ctl, no_skip, cq, o.counters, rbw, rid, wsum, td));
             else if (contract && aligned16(P))
-                K_FINISH<true, false, true><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, nullptr, rbw, rid, wsum, td);
+                CC_CUDA_TRY(launch_pdl(k_finish<true, false, true>, nb, kBlock, s, P, bm, n, ctl, no_skip, cq, nullptr, rbw, rid, wsum, td));
             else if (contract)
-                K_FINISH<false, true, true><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters, rbw, rid, wsum, td);
+                CC_CUDA_TRY(launch_pdl(k_finish<false, true, true>, nb, kBlock, s, P, bm, n, ctl, no_skip, cq, o.counters, rbw, rid, wsum, td));
             else if (aligned16(P) && o.counters)
-                K_FINISH<true, true, false><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters, nullptr, nullptr, wsum, td);
+                CC_CUDA_TRY(launch_pdl(k_finish<true, true, false>, nb, kBlock, s, P, bm, n, ctl, no_skip, cq, o.counters, nullptr, nullptr, wsum, td));
             else if (aligned16(P))
-                K_FINISH<true, false, false><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, nullptr, nullptr, nullptr, wsum, td);
+                CC_CUDA_TRY(launch_pdl(k_finish<true, false, false>, nb, kBlock, s, P, bm, n, ctl, no_skip, cq, nullptr, nullptr, nullptr, wsum, td));
             else
-                K_FINISH<false, true, false><<<nb, kBlock, 0, s>>>(P, bm, n, ctl, no_skip, cq, o.counters, nullptr, nullptr, wsum, td);
-#undef K_FINISH
+                CC_CUDA_TRY(launch_pdl(k_finish<false, true, false>, nb, kBlock, s, P, bm, n, ctl, no_skip, cq, o.counters, nullptr, nullptr, wsum, td));
             CC_LAUNCH_CHECK("k_finish");
         }
         CC_CUDA_TRY(mark(CC_MARK_FINISH));
         if (sv) {
+            // every marked vertex is a finish candidate when the skip is off or nothing was
+            // sampled (P is the identity, so only L_max itself is skipped)
             cc_status r = sv_finish<SF>(off, adj, P, n, cq, ctl, skip_prefix, F, o.counters, s,
-                                        (o.flags & CC_FLAG_FINISH_CRFA) != 0);
+                                        (o.flags & CC_FLAG_FINISH_CRFA) != 0, bm, no_skip, no_skip || k == 0);
             if (r) return r;
         } else {
-            k_finish_proc<MODE, SF><<<resident_grid(k_finish_proc<MODE, SF>, kBlock), kBlock, 0, s>>>(
-                off, adj, P, cq, ctl, skip_prefix, big, big_cap, F, o.counters, td);
+            CC_CUDA_TRY(launch_pdl(k_finish_proc<MODE, SF>, resident_grid(k_finish_proc<MODE, SF>, kBlock), kBlock, s, 
+                off, adj, P, cq, ctl, skip_prefix, big, big_cap, F, o.counters, td));
             CC_LAUNCH_CHECK("k_finish_proc");
-            k_finish_big<MODE, SF><<<resident_grid(k_finish_big<MODE, SF>, 512), 512, 0, s>>>(
-                off, adj, P, big, big_cap, ctl, skip_prefix, F, o.counters, td);
+            CC_CUDA_TRY(launch_pdl(k_finish_big<MODE, SF>, resident_grid(k_finish_big<MODE, SF>, 512), 512, s, 
+                off, adj, P, big, big_cap, ctl, skip_prefix, F, o.counters, td));
             CC_LAUNCH_CHECK("k_finish_big");
         }
         CC_CUDA_TRY(mark(CC_MARK_FINISH_BIG));
@@ -1951,11 +2003,11 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
             if (r) return r;
         } else if (want_labels) {
             if (o.counters)
-                k_relabel<true><<<resident_grid(k_relabel<true>, kBlock), kBlock, 0, s>>>(P, n, ctl, no_skip, wsum, td,
-                                                                                          o.counters);
+                CC_CUDA_TRY(launch_pdl(k_relabel<true>, resident_grid(k_relabel<true>, kBlock), kBlock, s, P, n, ctl, no_skip, wsum, td,
+                                                                                          o.counters));
             else
-                k_relabel<false><<<resident_grid(k_relabel<false>, kBlock), kBlock, 0, s>>>(P, n, ctl, no_skip, wsum,
-                                                                                            td, nullptr);
+                CC_CUDA_TRY(launch_pdl(k_relabel<false>, resident_grid(k_relabel<false>, kBlock), kBlock, s, P, n, ctl, no_skip, wsum,
+                                                                                            td, nullptr));
             CC_LAUNCH_CHECK("k_relabel(H6)");
         }
         CC_CUDA_TRY(mark(CC_MARK_COMPRESS));
@@ -1964,7 +2016,7 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
             // one-pass Filter: status words (foff) and the ticket (fcnt[0]) start at zero
             CC_CUDA_TRY(cudaMemsetAsync(foff, 0, sizeof(unsigned long long) * nfb, s));
             CC_CUDA_TRY(cudaMemsetAsync(fcnt, 0, sizeof(uint32_t), s));
-            k_forest_filter<<<nfb, kBlock, 0, s>>>(F, n, nfb, foff, fcnt, edges, num_edges);
+            CC_CUDA_TRY(launch_pdl(k_forest_filter, nfb, kBlock, s, F, n, nfb, foff, fcnt, edges, num_edges, nullptr, nullptr));
             CC_LAUNCH_CHECK("k_forest_filter");
         }
         CC_CUDA_TRY(mark(CC_MARK_FOREST));

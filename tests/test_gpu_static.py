@@ -457,3 +457,27 @@ def test_huge_list_bin_labels_and_forest(opt):
         if opt["k"] == 0 or opt.get("flags") == cc.FLAG_NO_SKIP or (name == "two_hubs" and opt["k"] == 1):
             # the hub list went through the finish (the huge bin) -- not skipped
             assert cnt["finish_edges"] > (1 << 20), (name, opt, cnt["finish_edges"])
+
+
+def test_cuda_graph_capture_replay():
+    """cc_labels with device buffers is stream-ordered with no host synchronisation, so a
+    caller can capture it into a CUDA graph (kernels, stream-ordered scratch allocations,
+    programmatic-dependent launches) and replay it -- the launch-bound small configs (C1)
+    then pay one graph launch per call.  Replays must give the same labels."""
+    off, adj = gen.er(seed=1)                       # C1's recipe
+    n = off.size - 1
+    want = oracle.cc_bfs(off, adj)
+    d_off, d_adj = to_dev(off, adj)
+    lab = torch.empty(n, dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        cc.cc_labels(d_off, d_adj, n, adj.size, lab, cc.make_opts(), s)      # warm-up outside capture
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
+        cc.cc_labels(d_off, d_adj, n, adj.size, lab, cc.make_opts(), s)
+    for _ in range(5):
+        lab.fill_(-1)
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(u32(lab), want)
