@@ -194,6 +194,8 @@ def run_reference(a, rank, ws):
     import inputs
     cfg = inputs.BY_INDEX[a.config]
     import oracle
+    if cfg.kind == "incr":
+        return run_reference_incr(a, cfg, use_gpu)
     m, dt0, off_s, adj_s, _ = cpu_oracle_sample(a.cpu_scale, use_gpu)     # sample generated once
     times = []
     for i in range(a.warmup + a.steps):
@@ -205,12 +207,79 @@ def run_reference(a, rank, ws):
     t = sum(times) / len(times)
     value = m / t / 1e9
     sample = f"oracle.cc_bfs (sequential BFS, 1 thread) on RMAT scale {a.cpu_scale} (C4 recipe a/b/c/d=.57/.19/.19/.05, ef 16, seed 4), m={m}"
+    # once, outside the K steps: the same oracle on the reported workload itself (one run; the
+    # graph comes from the seeded input generator, not from the product)
+    full = None
+    if not a.no_cpu_baseline:
+        try:
+            import numpy as np
+            import psutil
+            if use_gpu and cfg.kind != "incr":
+                from inputs import gpu as ggen
+                d_off, d_adj = ggen.config_graph(cfg)
+                n_f, m_f = d_off.numel() - 1, d_adj.numel()
+                if (8 * (n_f + 1) + 4 * m_f + 12 * n_f) * 1.2 < psutil.virtual_memory().available:
+                    off_h = d_off.cpu().numpy()
+                    adj_h = d_adj.cpu().numpy().view(np.uint32)
+                    del d_off, d_adj
+                    torch.cuda.empty_cache()
+                    t0 = time.perf_counter()
+                    oracle.cc_bfs(off_h, adj_h)
+                    dt = time.perf_counter() - t0
+                    full = {"value": round(m_f / dt / 1e9, 5), "unit": "GTEPS", "seconds": round(dt, 3),
+                            "sample": f"oracle.cc_bfs, 1 thread, on {cfg.name} itself (n={n_f}, m={m_f}), one run"}
+                    del off_h, adj_h
+        except Exception as e:                    # never fail the reference arm over the extra number
+            full = {"skipped": str(e)[:200]}
     line = {"impl": "reference", "metric": "connectivity edges/sec (GTEPS)", "value": value, "unit": "GTEPS",
             "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": t * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic", "config": {"workload": cfg.name, "sample": sample},
             "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if full is not None:
+        line["full_workload"] = full
+    print(json.dumps(line), flush=True)
+
+
+def run_reference_incr(a, cfg, use_gpu):
+    """--impl reference --config 5: the DSU oracle (oracle.incr_run, 1 thread) replaying the
+    first a.cpu_batches // 16 batches of the C5 stream per step (a bounded sample)."""
+    import numpy as np
+
+    import oracle
+    from inputs import gen
+    nbs = max(1, min(cfg.n_batches, a.cpu_batches // 16))
+    if use_gpu:
+        import torch
+        from inputs import gpu as ggen
+        bi = torch.empty((cfg.n_ins, 2), dtype=torch.int32, device="cuda")
+        bq = torch.empty((cfg.n_q, 2), dtype=torch.int32, device="cuda")
+        batches = []
+        for b in range(nbs):
+            ggen.incr_batch(cfg.seed, cfg.scale, b, cfg.n_ins, cfg.n_q, bi, bq)
+            batches.append((bi.cpu().numpy().view(np.uint32).copy(), bq.cpu().numpy().view(np.uint32).copy()))
+    else:
+        batches = [gen.incr_batch(cfg.seed, cfg.scale, b, cfg.n_ins, cfg.n_q) for b in range(nbs)]
+    n = 1 << cfg.scale
+    ops = nbs * (cfg.n_ins + cfg.n_q)
+    times = []
+    for i in range(a.warmup + a.steps):
+        t0 = time.perf_counter()
+        oracle.incr_run(n, batches)
+        dt = time.perf_counter() - t0
+        if i >= a.warmup:
+            times.append(dt)
+    t = sum(times) / len(times)
+    value = ops / t / 1e9
+    sample = (f"oracle.incr_run (sequential union-find, 1 thread) on the first {nbs} batches of the C5 stream "
+              f"({ops} ops) per step")
+    line = {"impl": "reference", "metric": "incremental connectivity ops/sec", "value": value, "unit": "Gops/s",
+            "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic", "config": {"workload": cfg.name, "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "Gops/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "Gops/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -281,7 +350,7 @@ def byte_model(off_h_deg_pos, n, m, k, ctr, sampled, final, mid_ran, f0=None, pa
              "candidates_queue_offsets_Pu": 28 * fin_v,
              "4W_label_writes": 4 * (ctr["compress_writes"] + ctr["h6_writes"]), "4H_hooks": 4 * ctr["finish_hooks"],
              "4n_compress_read": 0 if partial_h6 else 4 * n,
-             "tile_summaries": 34 * ntiles if partial_h6 else 0,
+             "tile_summaries": (34 if partial_h6 else 17) * ntiles,     # written by k_finish, read by a partial H6
              "dirty_tile_rereads": 8192 * ctr.get("h6_tiles", 0) if partial_h6 else 0}
     return B, {"relabelled": relab, "sampled_nonroots": nonroot, "mid_nonroots_bound": npos, "B_fin_terms": terms,
                "root_check_reads_not_counted": int(ctr["finish_gathers"] + ctr["h6_gathers"])}

@@ -50,7 +50,10 @@ struct Ctl {
     unsigned int skip_mid;      // set by k_probe: the round-0 chains are short
 };
 
-constexpr int kBigDeg = 4096;     // >  : one CTA per vertex (second kernel)
+#ifndef CC_BIG_DEG
+#define CC_BIG_DEG 4096
+#endif
+constexpr int kBigDeg = CC_BIG_DEG; // >  : one CTA per vertex (second kernel)
 constexpr int64_t kHugeDeg = 1 << 20;   // >  : every CTA takes a slice of the list
 
 // ---------------------------------------------------------------------------
@@ -671,8 +674,8 @@ __global__ void __launch_bounds__(kBlock) k_link_pending(
         }
 #pragma unroll
         for (int q = 0; q < kLB; ++q) {
-            pu[q] = ld_relaxed(P + pr[q].x);
-            pv[q] = ld_relaxed(P + pr[q].y);
+            pu[q] = ld_link(P + pr[q].x);
+            pv[q] = ld_link(P + pr[q].y);
         }
         uint32_t hooked = 0;
 #pragma unroll
@@ -860,10 +863,13 @@ __global__ void __launch_bounds__(kBlock) k_rank_fill(uint2* rbw, uint32_t nw, c
     }
 }
 
-// Grid of the static k-out link kernel.  CC_REFILL_GRID blocks per SM (default
-// 8: 1.33 waves at its 6 resident blocks per SM), 0 = exactly one resident wave.
+// Grid of the static k-out link kernel.  CC_REFILL_GRID blocks per SM, 0 (default)
+// = exactly one resident wave (6 blocks per SM).  With L1-cached Rem reads and PDL
+// launches the one-wave grid measured fastest: C4 link 1.93 -> 1.70 ms, C3 0.285 ->
+// 0.24 ms, C2 0.374 -> 0.30 ms (8 per SM = 1.33 waves had been faster with the
+// round-1 L2-only reads).
 #ifndef CC_REFILL_GRID
-#define CC_REFILL_GRID 8
+#define CC_REFILL_GRID 0
 #endif
 template <bool SF>
 static unsigned refill_grid()
@@ -1189,7 +1195,7 @@ __global__ void __launch_bounds__(kBlock) k_finish_proc(
             const uint32_t oex = __shfl_sync(0xffffffffu, excl, lo);
             if (t < tot) {
                 const uint32_t v = adj[ob + (t - oex)];
-                const uint32_t pv = ld_relaxed(P + v);
+                const uint32_t pv = ld_link(P + v);
                 if (pv != orr) {                            // enter the Rem loop with both reads done
                     if constexpr (MODE == 2) {
                         if constexpr (SF) hooks += link_async(P, ou, v, TileMarked<Forest>{Forest{F}, td});
@@ -1241,7 +1247,7 @@ __global__ void __launch_bounds__(512) k_finish_big(const int64_t* __restrict__ 
             const int64_t step = pass == 1 ? (int64_t)gridDim.x * blockDim.x : (int64_t)blockDim.x;
             for (int64_t x = x0; x < e; x += step) {
                 const uint32_t v = adj[x];
-                if (ld_relaxed(P + v) == ru) continue;
+                if (ld_link(P + v) == ru) continue;          // equal: v already in u's set (R5)
                 if constexpr (SF) hooks += link<MODE>(P, u, v, TileMarked<Forest>{Forest{F}, td});
                 else hooks += link<MODE>(P, u, v, TileMarked<NoForest>{NoForest{}, td});
             }

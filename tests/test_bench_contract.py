@@ -52,3 +52,29 @@ def test_bench_cpu_baseline_and_reference_arm():
     assert r["cpu_baseline"]["kind"] == "oracle"
     assert r["e2e"]["h2d_bytes_per_step"] == 0 and r["e2e"]["d2h_bytes_per_step"] == 0
     assert r["e2e"]["value"] == r["value"]
+
+
+def test_byte_model_b_fin_terms():
+    """bench.byte_model: the finish-phase bytes are SURVEY 8(d)'s B_fin for the implemented
+    design -- its terms add up to the finish kernels' bytes; the full final compress adds
+    exactly the 4n compress read (and drops the tile summaries / re-reads); second-level
+    root checks (finish_gathers, h6_gathers) are never counted."""
+    import numpy as np
+    import bench
+    n = 1 << 14
+    ctr = {k: 0 for k in ("pending_links", "finish_vertices", "finish_edges", "sample_hooks", "finish_hooks",
+                          "compress_writes", "h6_writes", "finish_gathers", "h6_gathers", "contract_roots")}
+    ctr.update(pending_links=900, finish_vertices=7, finish_edges=55, finish_hooks=3, compress_writes=120,
+               h6_writes=9, finish_gathers=10 ** 6, h6_gathers=10 ** 6, h6_tiles=2)
+    lab = np.arange(n, dtype=np.uint32)
+    Bp, xp = bench.byte_model((n // 2, n), n, 4 * n, 2, ctr, lab, lab, False, None, True)
+    Bf, xf = bench.byte_model((n // 2, n), n, 4 * n, 2, ctr, lab, lab, False, None, False)
+    tp, tf = xp["B_fin_terms"], xf["B_fin_terms"]
+    assert sum(tp.values()) == Bp["finish_phase"]
+    assert sum(tf.values()) == Bf["finish_phase"]
+    assert Bf["finish_phase"] - Bp["finish_phase"] == (4 * n - (tp["tile_summaries"] - tf["tile_summaries"])
+                                                       - tp["dirty_tile_rereads"])
+    # the 10^6 second-level root checks appear nowhere in the bytes
+    ctr2 = dict(ctr, finish_gathers=0, h6_gathers=0)
+    assert bench.byte_model((n // 2, n), n, 4 * n, 2, ctr2, lab, lab, False, None, True)[0] == Bp
+    assert xp["root_check_reads_not_counted"] == 2 * 10 ** 6
