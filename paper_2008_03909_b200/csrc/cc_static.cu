@@ -375,8 +375,8 @@ __global__ void __launch_bounds__(kBlock, CC_SL_MINB) k_sample_link(
         navail = b0 < total ? min(32u, total - b0) : 0u;
         const bool ok = lane < navail;
         nb = ok ? s_q[b0 + lane] : make_uint2(0u, 0u);
-        npu = ok ? ld_relaxed(P + nb.x) : 0u;
-        npv = ok ? ld_relaxed(P + nb.y) : 0u;
+        npu = ok ? ld_link(P + nb.x) : 0u;
+        npv = ok ? ld_link(P + nb.y) : 0u;
         chunk += NW;
     };
     fetch();
@@ -427,10 +427,10 @@ __global__ void __launch_bounds__(kBlock, CC_SL_MINB) k_sample_link(
                 } else {
                     ++fails;
                     pu = old;
-                    pv = ld_relaxed(P + rv);
+                    pv = ld_link(P + rv);
                 }
             } else {
-                const uint32_t wg = ld_relaxed(P + pu);
+                const uint32_t wg = ld_link(P + pu);
                 if (wg != pu) cas(P + ru, pu, wg);
                 ru = pu;
                 pu = wg;

@@ -1,5 +1,5 @@
 """The bench.py JSON line contract, checked on the committed round measurements
-(profiles/r1_bench_*.json, written by bench.py on a B200): every key the driver
+(profiles/r2_bench_*.json, written by bench.py on a B200): every key the driver
 and the tier contract require, with the right types and units."""
 import json
 import os
@@ -17,7 +17,7 @@ def line(name):
     return json.loads(open(path).read().strip().splitlines()[-1])
 
 
-@pytest.mark.parametrize("name", ["r1_bench_default.json", "r1_bench_c5.json"])
+@pytest.mark.parametrize("name", ["r2_bench_default.json", "r2_bench_c5.json", "r2_bench_c1_graph.json"])
 def test_bench_line_keys(name):
     d = line(name)
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
@@ -42,16 +42,19 @@ def test_bench_line_keys(name):
 
 
 def test_bench_cpu_baseline_and_reference_arm():
-    d = line("r1_bench_default.json")
+    d = line("r2_bench_default.json")
     cb = d["cpu_baseline"]
     for k in ("value", "unit", "cores", "kind", "sample"):
         assert k in cb, k
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["unit"] == d["unit"]
-    r = line("r1_bench_reference.json")
+    r = line("r2_bench_reference.json")
     assert r["impl"] == "reference" and r["unit"] == d["unit"] and r["metric"] == d["metric"]
     assert r["cpu_baseline"]["kind"] == "oracle"
     assert r["e2e"]["h2d_bytes_per_step"] == 0 and r["e2e"]["d2h_bytes_per_step"] == 0
     assert r["e2e"]["value"] == r["value"]
+    # the oracle timed on the reported graph itself in the same run
+    assert d["config"]["workload"] in cb["sample"] and cb["gpu_labels_bit_exact"] is True
+    assert "secondary_sample" in cb and r["full_workload"]["value"] > 0
 
 
 def test_byte_model_b_fin_terms():

@@ -277,3 +277,41 @@ def test_multi_batch_pinned_validate():
     h.close()
     assert torch.equal(lab0, lab1)                        # nothing applied
     assert np.array_equal(u32(lab0), want_lab)
+
+
+def test_repeat_random_batch_shapes():
+    """SURVEY 8(c) test matrix, C5 column "small": repeated streams whose batch sizes, insert /
+    query mix and options are random, so every launch path is taken in every order (the one-CTA
+    small batch, the two PDL kernels, the multi-batch kernel, validation) -- answers bit-exact."""
+    rng = np.random.default_rng(5)
+    n = 1 << 13
+    flag_pool = [0, cc.FLAG_HALVE, cc.FLAG_UF_ASYNC, cc.FLAG_FIND_SPLIT, cc.FLAG_FIND_NAIVE, cc.FLAG_VALIDATE]
+    for it in range(40):
+        flags = int(rng.choice(flag_pool))
+        nb = int(rng.integers(1, 12))
+        batches = []
+        for b in range(nb):
+            size = int(rng.choice([1, 7, 32, 255, 256, 257, 1000, 5000, 20000]))
+            n_q = int(rng.integers(0, size + 1))
+            ins, qs = gen.incr_batch(seed=100 + it, scale=13, b=b, n_ins=max(size - n_q, 0), n_q=n_q)
+            batches.append((ins, qs))
+        want, want_lab = oracle.incr_run(n, batches, want_labels=True)
+        if it % 2:
+            got, lab = run_stream(n, batches, flags)
+        else:                                         # the same batches through one cc_incr_batches call
+            h = cc.Incr(n, flags)
+            ic = np.array([b[0].size // 2 for b in batches], dtype=np.int64)
+            qc = np.array([b[1].size // 2 for b in batches], dtype=np.int64)
+            d_ins = dev(np.concatenate([b[0] for b in batches])) if ic.sum() else torch.zeros((0, 2), dtype=torch.int32,
+                                                                                                device="cuda")
+            d_q = dev(np.concatenate([b[1] for b in batches])) if qc.sum() else torch.zeros((0, 2), dtype=torch.int32,
+                                                                                              device="cuda")
+            ans = torch.empty(max(int(qc.sum()), 1), dtype=torch.uint8, device="cuda")
+            h.batches(ic, d_ins, qc, d_q, ans)
+            lab_t = torch.empty(n, dtype=torch.int32, device="cuda")
+            h.labels(lab_t)
+            torch.cuda.synchronize()
+            got, lab = ans.cpu().numpy()[: int(qc.sum())], u32(lab_t)
+            h.close()
+        assert np.array_equal(got, want), (it, flags, [b[0].size // 2 for b in batches])
+        assert np.array_equal(lab, want_lab), it

@@ -195,3 +195,27 @@ def test_exp_weights_generator():
     assert w.min() > 0 and abs(float(w.mean()) - 1.0) < 0.05
     x = np.concatenate([np.random.default_rng(1).random(10000) * 0.999 + 1e-12, 1 - np.arange(1, 50) * 2.0 ** -53])
     assert np.max(np.abs(gen.neg_ln_fixed(x) + np.log(x)) / np.abs(np.log(x))) < 1e-11
+
+
+def test_amsf_self_loops_keep_the_guarantee():
+    """Reading R25 counts self-loop entries in W_min / W_max.  Pin it to what the paper fixes
+    rather than to itself: with loops lighter and heavier than every real edge (so the
+    reading moves every bucket boundary), the result is still a valid spanning forest of input
+    edges whose per-bucket sizes are the rank increases of the prefix graphs (scipy), inside
+    the (1+eps) sandwich around Kruskal -- and a loop never enters the forest."""
+    rng = np.random.default_rng(11)
+    for trial in range(20):
+        off0, adj0 = gen.er(seed=200 + trial, n0=300, pairs=900, isolated=2)
+        n = off0.size - 1
+        src = np.repeat(np.arange(n), np.diff(off0))
+        pairs = [(int(a), int(b)) for a, b in zip(src, adj0) if a < b]
+        loops = rng.choice(n, size=12, replace=False)
+        off, adj = csr(n, pairs + [(int(x), int(x)) for x in loops], keep_loops=True)
+        w = gen.exp_weights(off, adj, trial)
+        src = np.repeat(np.arange(n), np.diff(off))
+        is_loop = src == adj
+        w[is_loop] = np.where(rng.random(int(is_loop.sum())) < 0.5, w.min() * 1e-3, w.max() * 7).astype(np.float32)
+        for eps in (0.25, 1.0):
+            r, wopt = check_amsf(off, adj, w, eps)
+            P = r["pairs"]
+            assert not np.any(P[:, 0] == P[:, 1])
