@@ -67,38 +67,9 @@ __global__ void __launch_bounds__(kBlock) k_query(uint32_t* P, const uint2* __re
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_q) return;
     const uint2 e = q[i];
-    if constexpr (FIND == 0) {
-        // The default: both finds' path-halving walks (find_halve_quiet) advanced together,
-        // one step of each per iteration with their loads in flight at once, and stopped as
-        // soon as the two walks meet (equal parents / equal nodes prove one set: ancestors
-        // stay in the set) or both reached a root.  Same answers, half the dependent latency.
-        uint32_t xa = e.x, xb = e.y;
-        uint32_t pa = ld_relaxed(P + xa), pb = ld_relaxed(P + xb);
-        uint8_t r;
-        while (true) {
-            if (pa == pb || xa == xb) { r = 1; break; }
-            const bool ra = pa == xa, rb = pb == xb;          // roots reached (no hook runs now)
-            if (ra && rb) { r = 0; break; }
-            const uint32_t ga = ra ? pa : ld_relaxed(P + pa);
-            const uint32_t gb = rb ? pb : ld_relaxed(P + pb);
-            const bool ma = !ra && ga != pa, mb = !rb && gb != pb;   // halving moves x to g
-            if (!ra) {
-                if (ma) P[xa] = ga;                            // plain store of an ancestor
-                xa = ma ? ga : pa;
-            }
-            if (!rb) {
-                if (mb) P[xb] = gb;
-                xb = mb ? gb : pb;
-            }
-            if (ma) pa = ld_relaxed(P + xa);
-            if (mb) pb = ld_relaxed(P + xb);
-        }
-        ans[i] = r;
-    } else {
-        const uint32_t ra = query_find<FIND>(P, e.x);
-        const uint32_t rb = query_find<FIND>(P, e.y);
-        ans[i] = ra == rb ? 1 : 0;
-    }
+    const uint32_t ra = query_find<FIND>(P, e.x);
+    const uint32_t rb = query_find<FIND>(P, e.y);
+    ans[i] = ra == rb ? 1 : 0;
 }
 
 // Wait-free type (1) batch (Theorem P:2663-2682): inserts and

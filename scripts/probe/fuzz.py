@@ -64,17 +64,24 @@ while time.time() - t0 < secs:
     variant = ["afforest", "hybrid", "pure"][int(rng.integers(0, 3))]
     fl = int(rng.choice(FLAGS)) | int(rng.choice(FLAGS))
     seed = int(rng.integers(1 << 30))
-    lab = pkg.connected_components(d_off, d_adj, k=k, variant=variant, seed=seed, flags=fl)
+    grid = int(rng.choice([0, 0, 0, 1, 3, 37, 1000, 5000]))      # random launch configuration
+    cc.set_grid(grid)
+    hooks = {}
+    if rng.random() < 0.1 and n:                                  # forced L_max (any vertex or none)
+        forced = int(rng.integers(0, n)) if rng.random() < 0.8 else 0xFFFFFFFF
+        hooks["lmax_force"] = torch.tensor([np.uint32(forced).view(np.int32)], dtype=torch.int32, device="cuda")
+    lab = pkg.connected_components(d_off, d_adj, k=k, variant=variant, seed=seed, flags=fl, **hooks)
     got = lab.cpu().numpy().view(np.uint32)
     if not np.array_equal(got, want):
-        print("LABELS MISMATCH", name, k, variant, fl, seed, np.nonzero(got != want)[0][:5])
+        print("LABELS MISMATCH", name, k, variant, fl, seed, grid, hooks, np.nonzero(got != want)[0][:5])
         sys.exit(1)
     runs["labels"] += 1
     if rng.random() < 0.5:
-        edges, lab2 = pkg.spanning_forest(d_off, d_adj, k=k, variant=variant, seed=seed, flags=fl)
+        wl = rng.random() < 0.7
+        edges, lab2 = pkg.spanning_forest(d_off, d_adj, k=k, variant=variant, seed=seed, flags=fl, with_labels=wl)
         c = int(np.sum(want == np.arange(n)))
         rc, bad = oracle.forest_check(off, adj, c, edges.cpu().numpy().view(np.uint32))
-        if rc or not np.array_equal(lab2.cpu().numpy().view(np.uint32), want):
+        if rc or (wl and not np.array_equal(lab2.cpu().numpy().view(np.uint32), want)):
             print("FOREST MISMATCH", name, k, variant, fl, seed, oracle.FOREST_ERRORS.get(rc), bad)
             sys.exit(1)
         runs["forest"] += 1
@@ -112,4 +119,5 @@ while time.time() - t0 < secs:
             print("INCR MISMATCH", name, ifl)
             sys.exit(1)
         runs["incr"] += 1
+cc.set_grid(0)
 print("fuzz ok", runs, f"{time.time() - t0:.0f}s")
