@@ -66,7 +66,13 @@ constexpr int64_t kHugeDeg = 1 << 20;   // >  : every CTA takes a slice of the l
 // appended in vertex order within a block with ONE atomicAdd per block (a
 // per-warp atomic on a single address serialised the first version at L2).
 // The finish bitmap has bit (u & 31) of word u >> 5 set iff deg(u) > full_deg.
-constexpr int kV = 8;                        // vertices per lane
+#ifndef CC_SI_KV
+#define CC_SI_KV 8
+#endif
+#ifndef CC_SI_MINB
+#define CC_SI_MINB 3
+#endif
+constexpr int kV = CC_SI_KV;                 // vertices per lane
 constexpr int kWarpTile = 32 * kV;           // 256 vertices per warp
 constexpr int kBlockTile = kWarpTile * (kBlock / 32);
 
@@ -83,7 +89,7 @@ __device__ __forceinline__ uint32_t pick4(uint4 w, uint32_t r)
 // VAR: 0 = afforest (positions 0..k-1), 1 = hybrid (0, then k-1 uniform picks),
 // 2 = pure (k uniform picks) -- cc.h CC_VARIANT_*.
 template <int VAR, bool SF, bool WIN, bool RB>
-__global__ void __launch_bounds__(kBlock, 3) k_sample_init(
+__global__ void __launch_bounds__(kBlock, CC_SI_MINB) k_sample_init(
     const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, uint32_t n, int64_t m, uint32_t k,
     uint64_t seed, uint32_t full_deg, uint32_t* __restrict__ P, uint2* __restrict__ F,
     uint2* __restrict__ pend, uint32_t* __restrict__ bm, uint2* __restrict__ rbw, Ctl* ctl, cc_counters* cnt)
@@ -1001,7 +1007,8 @@ __device__ __forceinline__ uint32_t warp_foreign_summary(const uint32_t (&rr)[kC
 // One tile of the scan, with its P words (pp) and bitmap words already loaded.
 template <bool CNT, bool CONTRACT>
 __device__ __forceinline__ void finish_tile(uint32_t* P, uint32_t n, uint64_t tile, bool full, uint32_t (&pp)[kCV],
-                                            uint32_t w0, uint32_t w1, uint32_t lmax, Ctl* ctl, uint32_t* cq,
+                                            uint32_t w0, uint32_t w1, uint32_t lmax, uint32_t known, Ctl* ctl,
+                                            uint32_t* cq,
                                             const uint2* __restrict__ rbw, const uint32_t* __restrict__ rid,
                                             uint32_t* __restrict__ wsum, uint8_t* __restrict__ td, uint32_t& writes,
                                             uint32_t& gathers)
@@ -1024,7 +1031,7 @@ __device__ __forceinline__ void finish_tile(uint32_t* P, uint32_t n, uint64_t ti
             if (CNT) gathers += cr;
         }
     } else {
-        const uint32_t g = roots8(P, vv, pp, rr, lmax);     // L_max stays a root: no hook runs here
+        const uint32_t g = roots8(P, vv, pp, rr, known);    // L_max stays a root: no hook runs here
         if (CNT) gathers += g;
     }
     if (CNT) {
@@ -1097,11 +1104,17 @@ __global__ void __launch_bounds__(kBlock, CC_FINISH_MINB) k_finish(uint32_t* P, 
     pdl_trigger();
     pdl_wait();
     const uint32_t lmax = no_skip ? kSentinel : ctl->lmax;
+    // L_max is a root of the sampled forest (IdentifyFrequent walks to roots), so a slot
+    // holding it needs no gather -- unless a caller forced a non-root L_max (cc_opts.
+    // lmax_force): then it is no shortcut, and since the slots' roots never equal it,
+    // nothing is skipped (P stays height-one after this pass, as the SV / CRFA rounds need)
+    const uint32_t known = lmax < n && ld_relaxed(P + lmax) == lmax ? lmax : kSentinel;
     const uint64_t tile = blockIdx.x;
     const bool full = VEC && (tile + 1) * kCTile <= n;
     uint32_t pp[kCV], w0, w1, writes = 0, gathers = 0;
     finish_load(P, bm, n, tile, full, pp, w0, w1);
-    finish_tile<CNT, CONTRACT>(P, n, tile, full, pp, w0, w1, lmax, ctl, cq, rbw, rid, wsum, td, writes, gathers);
+    finish_tile<CNT, CONTRACT>(P, n, tile, full, pp, w0, w1, lmax, known, ctl, cq, rbw, rid, wsum, td, writes,
+                               gathers);
     if (CNT) {
         warp_count(&cnt->compress_writes, writes);
         warp_count(&cnt->finish_gathers, gathers);

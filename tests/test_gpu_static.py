@@ -140,6 +140,34 @@ def test_lmax_forcing_changes_nothing():
             assert np.array_equal(u32(lab), want), (forced, k)
 
 
+def test_lmax_forcing_non_roots_every_finish():
+    """A forced L_max that is not a root of the sampled forest (cc_opts.lmax_force) must change
+    nothing either, for every finish: UF-Rem-CAS, SV and CRFA (whose rounds need a height-one
+    P after the scan -- the fuzz campaign found a grid where a non-root L_max broke that),
+    with and without the degree skip and with the contracted link."""
+    graphs = [gen.grid(seed=3, rows=69, cols=173), gen.grid(seed=4, rows=40, cols=90, p32=3 << 30),
+              gen.rmat(seed=10, scale=11)]
+    for off, adj in graphs:
+        n = off.size - 1
+        want = oracle.cc_bfs(off, adj)
+        d_off, d_adj = to_dev(off, adj)
+        for k in (1, 2):
+            sampled = torch.empty(n, dtype=torch.int32, device="cuda")
+            pkg.connected_components(d_off, d_adj, k=k, sampled_out=sampled)
+            s_lab = u32(sampled)
+            nonroots = np.nonzero(s_lab != np.arange(n))[0]
+            picks = [int(x) for x in nonroots[:: max(1, nonroots.size // 5)][:5]]
+            for forced in picks:
+                f = torch.tensor([np.uint32(forced).view(np.int32)], dtype=torch.int32, device="cuda")
+                for fl in (0, cc.FLAG_FINISH_SV, cc.FLAG_FINISH_CRFA, cc.FLAG_FINISH_SV | cc.FLAG_NO_DEGSKIP,
+                           cc.FLAG_CONTRACT, cc.FLAG_NO_DEGSKIP):
+                    lab = pkg.connected_components(d_off, d_adj, k=k, lmax_force=f, flags=fl)
+                    assert np.array_equal(u32(lab), want), (n, k, forced, fl)
+                    edges, lab2 = pkg.spanning_forest(d_off, d_adj, k=k, lmax_force=f, flags=fl)
+                    c = int(np.sum(want == np.arange(n)))
+                    assert oracle.forest_check(off, adj, c, u32(edges).reshape(-1, 2))[0] == 0, (k, forced, fl)
+
+
 def test_permutation_and_list_order_metamorphic():
     off, adj = gen.rmat(seed=12, scale=11, permuted=False)
     n = off.size - 1
