@@ -631,7 +631,7 @@ def run_ours(a, rank, ws):
         # lane-refill kernel (default): link_steps counts Rem iterations that issued a
         # load or CAS, each lost CAS adds the re-read of P[rv]; round-1 kernel: every
         # loop iteration plus the hook CAS
-        refill = not (a.flags & (cc.FLAG_NO_REFILL | cc.FLAG_HALVE | cc.FLAG_UF_ASYNC))
+        refill = not ctr.get("link_pending") and not (a.flags & (cc.FLAG_NO_REFILL | cc.FLAG_HALVE | cc.FLAG_UF_ASYNC))
         acc = ctr["pending_links"] + ctr["link_steps"] + (ctr["cas_failures"] if refill else ctr["sample_hooks"])
         ach = acc / (lk["ms"] * 1e-3) / 1e9
         line["roofline"]["random_access_view"] = {

@@ -95,8 +95,12 @@ typedef int cc_status;
                                           cc_labels); ignored with CC_FLAG_NO_SKIP.
                                           Measured slower than the default in place link
                                           on C3/C4                               */
-#define CC_FLAG_NO_REFILL   (1u << 11) /* k-out links: one warp step per slowest lane (the
-                                          round-1 kernel) instead of lane refill           */
+#define CC_FLAG_NO_REFILL   (1u << 11) /* k-out links: always k_link_pending (links per thread
+                                          with their first parent reads batched)           */
+#define CC_FLAG_LINK_REFILL (1u << 18) /* k-out links: always the lane-refill kernel.  Default
+                                          (neither flag): the round-0 chain probe picks on the
+                                          device -- short chains k_link_pending, long chains
+                                          (grid-like ids) lane refill                        */
 #define CC_FLAG_FUSED_LINK  (1u << 16) /* run k-out sampling and its CAS links in one kernel
                                           (links queued in shared memory, P initialised first);
                                           UF-Rem-CAS + SplitAtomicOne with k <= 2 only, else
@@ -159,7 +163,10 @@ typedef struct {
     uint64_t amsf_links;       /* cc_amsf: in-bucket edges linked (diagnostics build only)*/
     uint64_t h6_tiles;         /* tiles of kCTile = 2048 slots the partial final compress
                                   re-resolved (dirty: a root they hold or name was
-                                  hooked by H5, L_max was hooked, or > 3 foreign roots)*/
+                                  hooked by H5, L_max was hooked, or two distinct foreign
+                                  roots in one of its 256-slot warp summaries)               */
+    uint64_t link_pending;     /* 1 if the k-out links ran in k_link_pending (0: lane refill,
+                                  the contracted or the fused link)                        */
 } cc_counters;
 
 typedef struct {

@@ -38,6 +38,7 @@ FLAG_FINISH_CRFA = 1 << 13
 FLAG_AMSF_NO_INDEX = 1 << 14
 FLAG_FUSED_LINK = 1 << 16
 FLAG_FIND_NAIVE = 1 << 15
+FLAG_LINK_REFILL = 1 << 18
 
 # every symbol include/cc.h and include/cc_bench.h declare
 EXPORTS = [
@@ -62,7 +63,7 @@ COUNTER_FIELDS = ["pending_links", "worklist", "finish_vertices", "finish_edges"
                   "big_vertices", "compress_writes",
                   "link_steps", "cas_failures", "probe_deep", "finish_gathers", "h6_writes", "h6_gathers",
                   "sv_rounds", "contract_roots", "amsf_rounds", "amsf_visits", "amsf_edges", "amsf_hooks",
-                  "amsf_rebuilds", "fused_link", "amsf_links", "h6_tiles"]
+                  "amsf_rebuilds", "fused_link", "amsf_links", "h6_tiles", "link_pending"]
 
 
 class Opts(ctypes.Structure):

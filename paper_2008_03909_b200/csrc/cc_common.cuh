@@ -118,10 +118,11 @@ static __global__ void __launch_bounds__(kBlock) k_forest_scan(const uint32_t* b
 template <bool SF>
 static __global__ void __launch_bounds__(kBlock, CC_REFILL_MINB) k_link_refill(
     uint32_t* P, const uint2* __restrict__ pend, const unsigned long long* count_dev, unsigned long long count_host,
-    uint2* F, cc_counters* cnt)
+    uint2* F, cc_counters* cnt, const unsigned int* skip_if)
 {
     pdl_trigger();
     pdl_wait();
+    if (skip_if && *skip_if) return;                 // the device-side kernel choice picked k_link_pending
     const unsigned lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     const unsigned long long total = count_dev ? *count_dev : count_host;

@@ -649,23 +649,29 @@ __global__ void __launch_bounds__(1024) k_probe(const uint32_t* P, uint32_t n, u
 }
 
 // ---------------------------------------------------------------------------
-// K1: UF-Rem-CAS links of the pending sampled edges.  Each thread takes 4
+// K1: UF-Rem-CAS links of the pending sampled edges.  Each thread takes kLB
 // links spaced one grid apart (coalesced pair loads) and issues their first
-// parent reads together (8 independent loads in flight); most links end at
-// that first test (equal parents), the rest continue in link_rem_from.  The
-// __syncwarp re-converges the warp so the next group's loads are issued as
-// whole-warp transactions again.
+// parent reads together; most links end at that first test (equal parents),
+// the rest continue in link_rem_from.  The __syncwarp re-converges the warp so
+// the next group's loads are issued as whole-warp transactions again.  With
+// the L1-cached Rem reads, PDL and a one-wave grid, ONE link per thread per
+// iteration measured fastest (round 2; kLB 1 / 2 / 3 / 4, C4 link 1.49 / 1.56 /
+// 1.57 / 1.63 ms, C3 0.18 / 0.19 / 0.20 / 0.20 ms) and faster than the lane-
+// refill kernel (C4 1.68, C3 0.25 ms) except on grid-like inputs with long
+// round-0 chains (C2: 0.40 vs 0.30 ms), which the probe recognises.
 #ifndef CC_LINK_BATCH
-#define CC_LINK_BATCH 4
+#define CC_LINK_BATCH 1
 #endif
 constexpr int kLB = CC_LINK_BATCH;
 
 template <int MODE, bool SF>
 __global__ void __launch_bounds__(kBlock) k_link_pending(
-    uint32_t* P, const uint2* __restrict__ pend, const Ctl* ctl, uint2* F, cc_counters* cnt)
+    uint32_t* P, const uint2* __restrict__ pend, const Ctl* ctl, uint2* F, cc_counters* cnt, bool gated)
 {
     pdl_trigger();
     pdl_wait();
+    if (gated && !ctl->skip_mid) return;             // the device-side kernel choice picked k_link_refill
+    if (cnt && blockIdx.x == 0 && threadIdx.x == 0) cnt->link_pending = 1;
     const unsigned long long total = ctl->pend_count;
     const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
     const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1896,6 +1902,7 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
             return o.marks ? cudaEventRecord((cudaEvent_t)o.marks[i], s) : cudaSuccess;
         };
         CC_CUDA_TRY(mark(CC_MARK_START));
+        bool probed = false;                  // k_probe ran: ctl->skip_mid holds its verdict
         // H1 + H2 (first round) + finish bitmap
         const uint32_t nblk0 = (uint32_t)(((uint64_t)n + kBlockTile - 1) / kBlockTile);
         // 16-byte list-head windows pay off when adj is read over PCIe (pinned host,
@@ -1933,16 +1940,20 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
                 CC_CUDA_TRY(cudaMemcpyAsync(&o.counters->contract_roots, Rtot, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
             cc_status r = launch_compress(P, n, nullptr, nullptr, s, "k_compress(F0)");
             if (r) return r;
-        } else if (k > 0 && !fused && !(o.flags & CC_FLAG_NO_MIDCOMPRESS)) {
+        } else if (k > 0 && !fused) {
             // shorten the first-round chains before the CAS links when they are long
-            // (grid-like inputs); k_probe decides on the device unless a flag forces it
+            // (grid-like inputs); k_probe decides on the device unless a flag forces it --
+            // and its verdict also picks the link kernel below
             const bool force = (o.flags & CC_FLAG_MIDCOMPRESS) != 0;
             if (!force) {
                 CC_CUDA_TRY(launch_pdl(k_probe, 1, 1024, s, P, n, o.seed, ctl, o.counters));
                 CC_LAUNCH_CHECK("k_probe");
+                probed = true;
             }
-            cc_status r = launch_compress(P, n, nullptr, nullptr, s, "k_compress(mid)", force ? nullptr : ctl);
-            if (r) return r;
+            if (!(o.flags & CC_FLAG_NO_MIDCOMPRESS)) {
+                cc_status r = launch_compress(P, n, nullptr, nullptr, s, "k_compress(mid)", force ? nullptr : ctl);
+                if (r) return r;
+            }
         }
         CC_CUDA_TRY(mark(CC_MARK_MIDCOMPRESS));
         // H2: the remaining sampled edges
@@ -1952,11 +1963,23 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
             CC_LAUNCH_CHECK("k_link_contract");
             k_contract_final<<<grid_blocks(8), kBlock, 0, s>>>(Cc, rid, Rtot);
             CC_LAUNCH_CHECK("k_contract_final");
+        } else if (k > 0 && MODE == 0 && !(o.flags & (CC_FLAG_NO_REFILL | CC_FLAG_LINK_REFILL)) && probed) {
+            // device-side choice (no host sync): short round-0 chains (k_probe: skip_mid)
+            // -> k_link_pending (2 links per thread, first parents batched); long chains
+            // (grid-like inputs) -> the lane-refill kernel; the other one exits at once
+            CC_CUDA_TRY(launch_pdl(k_link_pending<MODE, SF>, resident_grid(k_link_pending<MODE, SF>, kBlock), kBlock, s,
+                                   P, pend, ctl, F, o.counters, true));
+            CC_LAUNCH_CHECK("k_link_pending");
+            CC_CUDA_TRY(launch_pdl(k_link_refill<SF>, refill_grid<SF>(), kBlock, s, P, pend, &ctl->pend_count, 0, F,
+                                   o.counters, &ctl->skip_mid));
+            CC_LAUNCH_CHECK("k_link_refill");
         } else if (k > 0 && MODE == 0 && !(o.flags & CC_FLAG_NO_REFILL)) {
-            CC_CUDA_TRY(launch_pdl(k_link_refill<SF>, refill_grid<SF>(), kBlock, s, P, pend, &ctl->pend_count, 0, F, o.counters));
+            CC_CUDA_TRY(launch_pdl(k_link_refill<SF>, refill_grid<SF>(), kBlock, s, P, pend, &ctl->pend_count, 0, F,
+                                   o.counters, (const unsigned int*)nullptr));
             CC_LAUNCH_CHECK("k_link_refill");
         } else if (k > 0) {
-            CC_CUDA_TRY(launch_pdl(k_link_pending<MODE, SF>, resident_grid(k_link_pending<MODE, SF>, kBlock), kBlock, s, P, pend, ctl, F, o.counters));
+            CC_CUDA_TRY(launch_pdl(k_link_pending<MODE, SF>, resident_grid(k_link_pending<MODE, SF>, kBlock), kBlock, s,
+                                   P, pend, ctl, F, o.counters, false));
             CC_LAUNCH_CHECK("k_link_pending");
         }
         CC_CUDA_TRY(mark(CC_MARK_LINK));
