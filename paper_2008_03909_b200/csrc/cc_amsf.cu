@@ -388,6 +388,8 @@ constexpr int kIdTable = 4096;
 __global__ void __launch_bounds__(1024) k_amsf_lmax(uint32_t* P, uint32_t n, uint64_t seed, uint32_t round,
                                                     uint32_t samples, AmsfCtl* ac)
 {
+    pdl_trigger();
+    pdl_wait();
     __shared__ uint32_t keys[kIdTable];
     __shared__ uint32_t cnts[kIdTable];
     __shared__ unsigned long long best[32];
@@ -470,6 +472,8 @@ __global__ void __launch_bounds__(kBlock, CC_AMSF_ROUND_MINB) k_amsf_round(
     uint2* F, float* Fw, uint2* chq, const unsigned long long* __restrict__ hstart,
     const uint32_t* __restrict__ hidx, uint32_t nbk, cc_counters* cnt)
 {
+    pdl_trigger();
+    pdl_wait();
     const unsigned lane = threadIdx.x & 31;
     const bool rebuild = ac->rebuild != 0;
     const unsigned long long s0 = rebuild ? 0ull : start[round], s1 = start[round + 1];
@@ -589,6 +593,8 @@ __global__ void __launch_bounds__(kBlock) k_amsf_hub_pieces(const int64_t* __res
                                                             const uint32_t* __restrict__ hidx, uint32_t nbk, uint2* F,
                                                             float* Fw, cc_counters* cnt)
 {
+    pdl_trigger();
+    pdl_wait();
     const unsigned lane = threadIdx.x & 31;
     const unsigned long long total = ac->chunks;
     const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -939,6 +945,8 @@ __global__ void __launch_bounds__(kBlock) k_amsf_chunks(const int64_t* __restric
                                                         const uint2* __restrict__ chq, const AmsfCtl* ac, uint2* F,
                                                         float* Fw, cc_counters* cnt)
 {
+    pdl_trigger();
+    pdl_wait();
     const unsigned lane = threadIdx.x & 31;
     const unsigned long long total = ac->chunks;
     const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1011,6 +1019,8 @@ __global__ void __launch_bounds__(kBlock) k_amsf_chunks(const int64_t* __restric
 
 __global__ void k_amsf_next(AmsfCtl* ac, int in_slot, cc_counters* cnt)
 {
+    pdl_trigger();
+    pdl_wait();
     ac->chunks = 0;
     ac->cnt[in_slot] = 0;                                      // becomes the next round's output
     if (cnt) {
@@ -1173,25 +1183,25 @@ cc_status amsf_run(const int64_t* off, const uint32_t* adj, const float* w, uint
         for (uint32_t i = 0; i < nb; ++i) {
             const int in_slot = i & 1;
             if (skip) {
-                k_amsf_lmax<<<1, 1024, 0, s>>>(P, n, o.seed, i, o.samples, ac);
+                CC_CUDA_TRY(launch_pdl(k_amsf_lmax, 1, 1024, s, P, n, o.seed, i, o.samples, ac));
                 CC_LAUNCH_CHECK("k_amsf_lmax");
             }
-            k_amsf_round<MODE><<<resident_grid(k_amsf_round<MODE>, kBlock), kBlock, 0, s>>>(off, adj, w, P, vi, order, start, i, b[i], b[i + 1],
+            CC_CUDA_TRY(launch_pdl(k_amsf_round<MODE>, resident_grid(k_amsf_round<MODE>, kBlock), kBlock, s, off, adj, w, P, vi, order, start, i, b[i], b[i + 1],
                                                           carry[in_slot], ac, in_slot, carry[in_slot ^ 1],
                                                           skip, plain, F, Fw, chq, index ? hstart : nullptr,
-                                                          hidx, nb, o.counters);
+                                                          hidx, nb, o.counters));
             CC_LAUNCH_CHECK("k_amsf_round");
             if (index)
-                k_amsf_hub_pieces<MODE><<<resident_grid(k_amsf_hub_pieces<MODE>, kBlock), kBlock, 0, s>>>(off, adj, w, P, i, chq, ac, vi, hstart, hidx,
-                                                                   nb, F, Fw, o.counters);
+                CC_CUDA_TRY(launch_pdl(k_amsf_hub_pieces<MODE>, resident_grid(k_amsf_hub_pieces<MODE>, kBlock), kBlock, s, off, adj, w, P, i, chq, ac, vi, hstart, hidx,
+                                                                   nb, F, Fw, o.counters));
             else if (((uintptr_t)w & 15u) == 0)
-                k_amsf_chunks<MODE, true><<<resident_grid(k_amsf_chunks<MODE, true>, kBlock), kBlock, 0, s>>>(off, adj, w, P, b[i], b[i + 1], chq, ac, F, Fw,
-                                                                     o.counters);
+                CC_CUDA_TRY(launch_pdl(k_amsf_chunks<MODE, true>, resident_grid(k_amsf_chunks<MODE, true>, kBlock), kBlock, s, off, adj, w, P, b[i], b[i + 1], chq, ac, F, Fw,
+                                                                     o.counters));
             else
-                k_amsf_chunks<MODE, false><<<resident_grid(k_amsf_chunks<MODE, false>, kBlock), kBlock, 0, s>>>(off, adj, w, P, b[i], b[i + 1], chq, ac, F,
-                                                                      Fw, o.counters);
+                CC_CUDA_TRY(launch_pdl(k_amsf_chunks<MODE, false>, resident_grid(k_amsf_chunks<MODE, false>, kBlock), kBlock, s, off, adj, w, P, b[i], b[i + 1], chq, ac, F,
+                                                                      Fw, o.counters));
             CC_LAUNCH_CHECK("k_amsf_chunks");
-            k_amsf_next<<<1, 1, 0, s>>>(ac, in_slot, o.counters);
+            CC_CUDA_TRY(launch_pdl(k_amsf_next, 1, 1, s, ac, in_slot, o.counters));
             CC_LAUNCH_CHECK("k_amsf_next");
             if (trace && o.counters) {                       // diagnostics only (CC_AMSF_TRACE=1)
                 cc_counters c{};
