@@ -628,11 +628,10 @@ def run_ours(a, rank, ws):
             "achieved_Gaccess_per_s": round(ach, 2), "uniform_random_gather_Gloads_per_s": rg,
             "frac_of_random_gather_rate": round(ach / rg, 3)}
     elif lk:
-        # lane-refill kernel (default): link_steps counts Rem iterations that issued a
-        # load or CAS, each lost CAS adds the re-read of P[rv]; round-1 kernel: every
-        # loop iteration plus the hook CAS
-        refill = not ctr.get("link_pending") and not (a.flags & (cc.FLAG_NO_REFILL | cc.FLAG_HALVE | cc.FLAG_UF_ASYNC))
-        acc = ctr["pending_links"] + ctr["link_steps"] + (ctr["cas_failures"] if refill else ctr["sample_hooks"])
+        # both link kernels: link_steps counts Rem iterations that issued a load or a CAS (the
+        # hook CAS included), each lost CAS adds the re-read of P[rv]; plus one P[v] gather
+        # per pending link (P[u] is read in vertex order: not counted as random)
+        acc = ctr["pending_links"] + ctr["link_steps"] + ctr["cas_failures"]
         ach = acc / (lk["ms"] * 1e-3) / 1e9
         line["roofline"]["random_access_view"] = {
             "kernel": "k_sample_link" if ctr.get("fused_link") else "k_link_pending",

@@ -163,8 +163,8 @@ __device__ __forceinline__ bool link_rem_from(uint32_t* P, uint32_t u, uint32_t 
 {
     uint32_t ru = u, rv = v;
     while (true) {
-        if (st) st->step();
         if (pu == pv) return false;
+        if (st) st->step();                          // an iteration that makes a memory access
         if (pu < pv) {
             uint32_t t = ru; ru = rv; rv = t;
             t = pu; pu = pv; pv = t;
