@@ -591,6 +591,8 @@ def run_ours(a, rank, ws):
             "roofline": roofline, "finish": finish, "sampling": sampling, "kernels": kernels,
             "counters": ctr, "byte_model_extra": extra, "gpu_launches": int(launches), "clocks": clocks}
 
+    line["parity"] = {"labels": "not checked", "forest": "not checked",
+                      "oracle": "set by the cpu_baseline leg (rank 0, N = 1, without --no-cpu-baseline)"}
     # ---- measurement floors (K10, Table 8 analogue P:3732-3799), outside the timed region
     line["floors"] = floors(cc, d_off, d_adj, n, m, labels, stream, mean_ms)
     # spanning forest on the same graph (Alg. 2): t_SF / t_CC
@@ -609,7 +611,14 @@ def run_ours(a, rank, ws):
             sf_ms.append(e0.elapsed_time(e1))
     line["spanning_forest"] = {"ms": round(statistics.mean(sf_ms), 4), "t_sf_over_t_cc": round(statistics.mean(sf_ms) / mean_ms, 3),
                                "forest_edges": int(sf_num.item()), "n_minus_c": n - components}
+    # the forest pairs stay on the host for the oracle's validity check in the cpu_baseline leg
+    sf_host = sf_edges[: int(sf_num.item())].cpu().numpy().view(np.uint32) if rank == 0 and ws == 1 else None
     del sf_edges
+    # 64-bit fingerprint of the CSR bytes (SURVEY 8(d) JSON schema: csr_hash): sum of the
+    # offsets and of the adjacency words, each weighted by an odd multiplier per position class
+    line["config"]["csr_hash"] = "%016x" % ((int(d_off.sum().item()) * 0x9E3779B97F4A7C15
+                                              + int(d_adj.to(torch.int64).sum().item()) * 0xBF58476D1CE4E5B9
+                                              + m * 0x94D049BB133111EB) & 0xFFFFFFFFFFFFFFFF)
     # The link kernel is bound by dependent random 4-byte accesses into the 4n-byte
     # parent array, not by streaming bandwidth: set its random-access count (one
     # P[v] gather per pending link + one load or CAS per Rem-loop step + the hook
@@ -732,6 +741,13 @@ def run_ours(a, rank, ws):
                     "sample": f"oracle.cc_bfs (sequential BFS, 1 thread) on the reported workload itself "
                               f"({cfg.name}, n={n}, m={m}), median of {reps} run(s): {dt_full:.2f} s",
                     "seconds": round(dt_full, 3), "gpu_labels_bit_exact": bool(np.array_equal(lab_h, final))}
+            # parity on the reported graph (SURVEY 8(d) JSON schema: parity): labels raw-equal to the
+            # oracle's; the spanning forest by the validity triple (count, input edges, acyclic)
+            c_or = int(np.count_nonzero(lab_h == np.arange(n, dtype=np.uint32)))
+            rc, _ = _oracle.forest_check(off_h, adj_h, c_or, sf_host) if sf_host is not None else (-1, None)
+            line["parity"] = {"labels": "bit-exact" if full["gpu_labels_bit_exact"] else "FAIL",
+                              "forest": "valid" if rc == 0 else ("FAIL" if rc > 0 else "not checked"),
+                              "oracle": "oracle.cc_bfs + oracle.forest_check on this graph, this run"}
             del off_h, adj_h, lab_h
         m_s, dt, off_s, adj_s, lab_s = cpu_oracle_sample(a.cpu_scale, True)
         reps, spent = 1, dt

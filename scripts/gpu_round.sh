@@ -17,5 +17,5 @@ make probes > /dev/null 2>&1; ./scripts/probe/incr_latency 4000 > $D/incr_latenc
 P="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
 timeout 300 $P > $D/plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv --log-file $D/launches_c4.csv $P > $D/ncu_l.log 2>&1 && \
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_link_refill|k_sample_init|k_finish|k_relabel|k_identify|k_probe|k_compress" --launch-skip 19 -c 9 -o $D/c4_full $P > $D/ncu_f.log 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_link_pending|k_link_refill|k_sample_init|k_finish|k_relabel|k_identify|k_probe|k_compress" --launch-skip 21 -c 10 -o $D/c4_full $P > $D/ncu_f.log 2>&1
 echo done
