@@ -676,43 +676,6 @@ __global__ void __launch_bounds__(kBlock) k_link_pending(
     const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
     const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
     Stat st;
-#ifdef CC_PEND_PREFETCH
-    // software-pipelined single link per thread: the next link's pair and first parents are
-    // in flight while the current one walks
-    uint32_t hk = 0;
-    unsigned long long i = tid;
-    uint2 nx = i < total ? pend[i] : make_uint2(0u, 0u);
-    uint32_t npu = i < total ? ld_link(P + nx.x) : 0u, npv = i < total ? ld_link(P + nx.y) : 0u;
-    for (; i < total; i += nthreads) {
-        const uint2 cur = nx;
-        const uint32_t cu = npu, cv = npv;
-        const unsigned long long j = i + nthreads;
-        if (j < total) {
-            nx = pend[j];
-            npu = ld_link(P + nx.x);
-            npv = ld_link(P + nx.y);
-        }
-        if (cu != cv) {
-            if constexpr (MODE == 2) {
-                if constexpr (SF) hk += link_async(P, cur.x, cur.y, Forest{F});
-                else hk += link_async(P, cur.x, cur.y, NoForest{});
-            } else {
-                if constexpr (SF) hk += link_rem_from<MODE == 1>(P, cur.x, cur.y, cu, cv, Forest{F}, cnt ? &st : nullptr);
-                else hk += link_rem_from<MODE == 1>(P, cur.x, cur.y, cu, cv, NoForest{}, cnt ? &st : nullptr);
-            }
-        }
-#ifndef CC_PEND_NOSYNC
-        __syncwarp(__activemask());
-#endif
-    }
-    if (cnt) {
-        __syncwarp();
-        warp_count(&cnt->sample_hooks, hk);
-        warp_count(&cnt->link_steps, st.steps);
-        warp_count(&cnt->cas_failures, st.fails);
-    }
-    return;
-#endif
     for (unsigned long long base = 0; base < total; base += nthreads * kLB) {
         uint2 pr[kLB];
         uint32_t pu[kLB], pv[kLB];
