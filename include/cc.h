@@ -205,7 +205,7 @@ typedef struct {
 void cc_opts_default(cc_opts* o);
 
 /* Connectivity, Alg. 1 with k-out sampling (Alg. 4), IdentifyFrequent
- * and the UF-Rem-CAS finish, then a full
+ * and the UF-Rem-CAS finish, then the final
  * compress.  labels (out, n) is also the parent array, used in place:
  * on return labels[v] = minimum vertex id of v's component (canonical).
  * The first k-out round hooks every vertex under its first sampled neighbour
@@ -213,7 +213,13 @@ void cc_opts_default(cc_opts* o);
  * unioned in place on labels (default), or, with CC_FLAG_CONTRACT, with the
  * same UF-Rem-CAS rule on a compact parent array with one slot per
  * non-isolated F0 root, numbered in id order (so the min-id orientation is
- * kept); the latter needs the symmetric-graph precondition above. */
+ * kept); the latter needs the symmetric-graph precondition above.  The scan
+ * of the finish leaves every slot at its sampled root, so the final compress
+ * re-resolves only the 2048-slot tiles whose labels the finish's hooks changed
+ * (all of them if L_max itself was hooked); with labels in a host buffer, or
+ * after an SV / CRFA finish, it is a full pass.  Every kernel is a
+ * programmatic dependent launch; with device buffers the call never
+ * synchronises, so it can be captured into a CUDA graph. */
 cc_status cc_labels(const int64_t* offsets, const uint32_t* adj, uint32_t n, int64_t m,
                     uint32_t* labels, const cc_opts* opts, void* stream);
 

@@ -228,7 +228,7 @@ size_t cc_workspace_bytes(uint32_t n, int64_t m, uint32_t kout_k, int op)
                + 4 * N                              // finish candidate queue
                + 8 * K * std::min(N, M)             // pending sampled links
                + 4 * std::min(N, M / 4096 + 1)      // big-list queue
-               + 65 * ntile                         // warp summaries (8 x 8 B) + hook flag per tile
+               + 33 * ntile                         // warp summaries (8 x 4 B) + hook flag per tile
                + 4 * N                              // parent array when labels are not device memory
                + 8 * (N + 1) + 4 * M + 4 * N        // staging of pageable offsets / adjacency / labels
                + 8 * nw + 8 * std::min(N, M) + 12 * (nw / 4096 + 1) + 8     // CC_FLAG_CONTRACT
