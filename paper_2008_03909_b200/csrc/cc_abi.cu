@@ -225,7 +225,7 @@ size_t cc_workspace_bytes(uint32_t n, int64_t m, uint32_t kout_k, int op)
     // allocations (cc_static.cu run(), cc_abi.cu staging):
     size_t b = 64                                   // control block
                + 4 * nw                             // finish bitmap
-               + 4 * N                              // finish candidate queue
+               + 4 * std::max(N, 4 * ntile)         // finish candidate queue (= relabel chunk queue)
                + 8 * K * std::min(N, M)             // pending sampled links
                + 4 * std::min(N, M / 4096 + 1)      // big-list queue
                + 33 * ntile                         // warp summaries (8 x 4 B) + hook flag per tile

@@ -48,6 +48,7 @@ struct Ctl {
     unsigned int lmax;
     unsigned int err;
     unsigned int skip_mid;      // set by k_probe: the round-0 chains are short
+    unsigned long long rl_count;   // k_relabel_decide: dirty 512-slot chunks queued for k_relabel
 };
 
 #ifndef CC_BIG_DEG
@@ -1289,10 +1290,69 @@ __global__ void __launch_bounds__(512) k_finish_big(const int64_t* __restrict__ 
 // first-level parents batched as in k_compress, writes only changed slots).
 // The result equals the full compress: every other slot already holds its
 // final root (the canonical min-id label, reading R13).
+// Re-resolve slots [base, base + 4 * 32 * Q) (Q uint4 per lane) of a tile-aligned chunk.
+template <bool CNT, int Q>
+__device__ __forceinline__ void relabel_span(uint32_t* P, uint32_t n, uint64_t base, bool vec, uint32_t known,
+                                             uint32_t& writes, uint32_t& gathers)
+{
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t span = 128ull * Q;
+    if (vec && base + span <= n) {
+#pragma unroll 1
+        for (int j = 0; j < Q; j += 4) {
+            uint4 q[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) q[h] = reinterpret_cast<const uint4*>(P)[base / 4 + lane + 32 * (j + h)];
+#pragma unroll
+            for (int h = 0; h < 4; h += 2) {
+                const uint64_t i0 = base + 4 * (lane + 32 * (uint64_t)(j + h)), i1 = i0 + 128;
+                const uint32_t pp[8] = {q[h].x, q[h].y, q[h].z, q[h].w, q[h + 1].x, q[h + 1].y, q[h + 1].z, q[h + 1].w};
+                uint32_t vv[8], rr[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) vv[k] = (uint32_t)((k < 4 ? i0 : i1) + (k & 3));
+                const uint32_t g = roots8(P, vv, pp, rr, known);
+                const uint4 r0 = make_uint4(rr[0], rr[1], rr[2], rr[3]);
+                const uint4 r1 = make_uint4(rr[4], rr[5], rr[6], rr[7]);
+                const uint32_t c0 = nchanged4(r0, q[h]), c1 = nchanged4(r1, q[h + 1]);
+                if (c0) reinterpret_cast<uint4*>(P)[i0 >> 2] = r0;
+                if (c1) reinterpret_cast<uint4*>(P)[i1 >> 2] = r1;
+                if (CNT) {
+                    gathers += g;
+                    writes += c0 + c1;
+                }
+            }
+        }
+    } else {
+        const uint64_t end = (base + span < n ? base + span : (uint64_t)n);
+        for (uint64_t v64 = base + lane; v64 < end; v64 += 32) {
+            const uint32_t v = (uint32_t)v64;
+            const uint32_t p = P[v];
+            const bool g = !(p == v || p == known);
+            const uint32_t r = g ? root_halve(P, p) : p;
+            if (r != p) P[v] = r;
+            if (CNT) {
+                gathers += g;
+                writes += r != p;
+            }
+        }
+    }
+}
+
+constexpr int kRlChunk = 512;                            // slots per queued relabel chunk
+constexpr int kRlPerTile = kCTile / kRlChunk;
+
+// Two kernels (the kernel boundary is the barrier; PDL overlaps the launch):
+// k_relabel_decide -- each warp decides its run of tiles (hook flag, 32 bytes of warp
+// summaries, a P[r] == r test per named root) and queues the dirty ones as 512-slot
+// chunks (in the candidate queue, free after H5); k_relabel -- every warp takes queued
+// chunks, so a few hundred dirty tiles are spread over all warps instead of being
+// walked by the few warps that own them.  If L_max was hooked, the decide kernel
+// queues nothing and k_relabel re-resolves every chunk grid-strided.
 template <bool CNT>
-__global__ void __launch_bounds__(kBlock) k_relabel(uint32_t* P, uint32_t n, const Ctl* ctl, bool no_skip,
-                                                    const uint32_t* __restrict__ wsum, const uint8_t* __restrict__ td,
-                                                    cc_counters* cnt)
+__global__ void __launch_bounds__(kBlock) k_relabel_decide(const uint32_t* P, uint32_t n, Ctl* ctl, bool no_skip,
+                                                           const uint32_t* __restrict__ wsum,
+                                                           const uint8_t* __restrict__ td, uint32_t* queue,
+                                                           cc_counters* cnt)
 {
     pdl_trigger();
     pdl_wait();
@@ -1301,19 +1361,17 @@ __global__ void __launch_bounds__(kBlock) k_relabel(uint32_t* P, uint32_t n, con
     if (lm >= n) lm = kSentinel;                                      // a forced out-of-range L_max skips nothing
     // L_max no longer a root: H5 hooked it, or a forced L_max was never one -- in
     // both cases slots holding it are not final, so every tile is re-resolved
-    const bool lmax_hooked = lm != kSentinel && P[lm] != lm;         // no hook runs in H6: plain loads
-    const uint32_t known = lmax_hooked ? kSentinel : lm;
+    if (lm != kSentinel && P[lm] != lm) return;                       // no hook runs in H6: plain loads
     const uint64_t ntiles = ((uint64_t)n + kCTile - 1) / kCTile;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t tpw = (ntiles + nwarps - 1) / nwarps < 32 ? (ntiles + nwarps - 1) / nwarps : (uint64_t)32;  // tiles per warp per sweep
-    const bool vec = ((uintptr_t)P & 15u) == 0;
-    uint32_t writes = 0, gathers = 0, tiles = 0;
+    const uint64_t tpw = (ntiles + nwarps - 1) / nwarps < 32 ? (ntiles + nwarps - 1) / nwarps : (uint64_t)32;
+    uint32_t tiles = 0;
     for (uint64_t t0 = warp * tpw; t0 < ntiles; t0 += nwarps * tpw) {
         const uint64_t t = t0 + lane;
         bool dirty = false;
         if (lane < tpw && t < ntiles) {
-            if (lmax_hooked || td[t]) {
+            if (td[t]) {
                 dirty = true;
             } else {
                 // the tile's kSumPerTile warp summaries (32 contiguous bytes)
@@ -1325,58 +1383,42 @@ __global__ void __launch_bounds__(kBlock) k_relabel(uint32_t* P, uint32_t n, con
                     dirty |= r8[c] == kWarpOverflow || (r8[c] != kSentinel && P[r8[c]] != r8[c]);
             }
         }
-        unsigned mask = __ballot_sync(0xffffffffu, dirty);
         if (CNT) tiles += dirty;
-        while (mask) {
-            const uint64_t base = (t0 + (unsigned)(__ffs(mask) - 1)) * kCTile;
-            mask &= mask - 1;
-            if (vec && base + kCTile <= n) {
-                // 512 uint4 per tile: 4 rounds of 4 uint4 (16 slots) per lane
-#pragma unroll 1
-                for (int j = 0; j < 16; j += 4) {
-                    uint4 q[4];
-#pragma unroll
-                    for (int h = 0; h < 4; ++h) q[h] = reinterpret_cast<const uint4*>(P)[base / 4 + lane + 32 * (j + h)];
-#pragma unroll
-                    for (int h = 0; h < 4; h += 2) {
-                        const uint64_t i0 = base + 4 * (lane + 32 * (uint64_t)(j + h)), i1 = i0 + 128;
-                        const uint32_t pp[8] = {q[h].x, q[h].y, q[h].z, q[h].w, q[h + 1].x, q[h + 1].y, q[h + 1].z,
-                                                q[h + 1].w};
-                        uint32_t vv[8], rr[8];
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) vv[k] = (uint32_t)((k < 4 ? i0 : i1) + (k & 3));
-                        const uint32_t g = roots8(P, vv, pp, rr, known);
-                        const uint4 r0 = make_uint4(rr[0], rr[1], rr[2], rr[3]);
-                        const uint4 r1 = make_uint4(rr[4], rr[5], rr[6], rr[7]);
-                        const uint32_t c0 = nchanged4(r0, q[h]), c1 = nchanged4(r1, q[h + 1]);
-                        if (c0) reinterpret_cast<uint4*>(P)[i0 >> 2] = r0;
-                        if (c1) reinterpret_cast<uint4*>(P)[i1 >> 2] = r1;
-                        if (CNT) {
-                            gathers += g;
-                            writes += c0 + c1;
-                        }
-                    }
-                }
-            } else {
-                const uint64_t end = (base + kCTile < n ? base + kCTile : (uint64_t)n);
-                for (uint64_t v64 = base + lane; v64 < end; v64 += 32) {
-                    const uint32_t v = (uint32_t)v64;
-                    const uint32_t p = P[v];
-                    const bool g = !(p == v || p == known);
-                    const uint32_t r = g ? root_halve(P, p) : p;
-                    if (r != p) P[v] = r;
-                    if (CNT) {
-                        gathers += g;
-                        writes += r != p;
-                    }
-                }
-            }
-        }
+        const unsigned long long pos = warp_append(&ctl->rl_count, dirty ? (uint32_t)kRlPerTile : 0u);
+        if (dirty)
+            for (int c = 0; c < kRlPerTile; ++c) queue[pos + c] = (uint32_t)(t * kRlPerTile + c);
+    }
+    if (CNT) warp_count(&cnt->h6_tiles, tiles);
+}
+
+template <bool CNT>
+__global__ void __launch_bounds__(kBlock) k_relabel(uint32_t* P, uint32_t n, const Ctl* ctl, bool no_skip,
+                                                    const uint32_t* __restrict__ queue, cc_counters* cnt)
+{
+    pdl_trigger();
+    pdl_wait();
+    uint32_t lm = no_skip ? kSentinel : ctl->lmax;
+    if (lm >= n) lm = kSentinel;
+    const bool lmax_hooked = lm != kSentinel && P[lm] != lm;
+    const uint32_t known = lmax_hooked ? kSentinel : lm;
+    const uint64_t ntiles = ((uint64_t)n + kCTile - 1) / kCTile;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const bool vec = ((uintptr_t)P & 15u) == 0;
+    uint32_t writes = 0, gathers = 0;
+    if (lmax_hooked) {
+        for (uint64_t c = warp; c < ntiles * kRlPerTile; c += nwarps)
+            relabel_span<CNT, kRlChunk / 128>(P, n, c * kRlChunk, vec, known, writes, gathers);
+        if (CNT && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt->h6_tiles),
+                                                                  (unsigned long long)ntiles);
+    } else {
+        const unsigned long long total = ctl->rl_count;
+        for (unsigned long long idx = warp; idx < total; idx += nwarps)
+            relabel_span<CNT, kRlChunk / 128>(P, n, (uint64_t)queue[idx] * kRlChunk, vec, known, writes, gathers);
     }
     if (CNT) {
         warp_count(&cnt->h6_writes, writes);
         warp_count(&cnt->h6_gathers, gathers);
-        warp_count(&cnt->h6_tiles, tiles);
     }
 }
 
@@ -1873,7 +1915,8 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
     auto body = [&]() -> cc_status {
         CC_CUDA_TRY(scratch_alloc((void**)&ctl, sizeof(Ctl), s));
         CC_CUDA_TRY(scratch_alloc((void**)&bm, sizeof(uint32_t) * bm_words, s));
-        CC_CUDA_TRY(scratch_alloc((void**)&cq, sizeof(uint32_t) * (size_t)n, s));
+        // the candidate queue; reused by k_relabel_decide for its chunk queue (kRlPerTile per tile)
+        CC_CUDA_TRY(scratch_alloc((void**)&cq, sizeof(uint32_t) * std::max<size_t>(n, kRlPerTile * ntile), s));
         if (k > 0 && !fused) CC_CUDA_TRY(scratch_alloc((void**)&pend, sizeof(uint2) * pend_cap, s));
         CC_CUDA_TRY(scratch_alloc((void**)&big, sizeof(uint32_t) * big_cap, s));
         CC_CUDA_TRY(scratch_alloc((void**)&wsum, sizeof(uint32_t) * kSumPerTile * ntile, s));
@@ -2044,12 +2087,19 @@ static cc_status run(const int64_t* off, const uint32_t* adj, uint32_t n, int64_
             cc_status r = launch_compress(P, n, labels_out, o.counters, s, "k_compress(H6)");
             if (r) return r;
         } else if (want_labels) {
-            if (o.counters)
-                CC_CUDA_TRY(launch_pdl(k_relabel<true>, resident_grid(k_relabel<true>, kBlock), kBlock, s, P, n, ctl, no_skip, wsum, td,
-                                                                                          o.counters));
-            else
-                CC_CUDA_TRY(launch_pdl(k_relabel<false>, resident_grid(k_relabel<false>, kBlock), kBlock, s, P, n, ctl, no_skip, wsum,
-                                                                                            td, nullptr));
+            if (o.counters) {
+                CC_CUDA_TRY(launch_pdl(k_relabel_decide<true>, resident_grid(k_relabel_decide<true>, kBlock), kBlock, s,
+                                       P, n, ctl, no_skip, wsum, td, cq, o.counters));
+                CC_LAUNCH_CHECK("k_relabel_decide");
+                CC_CUDA_TRY(launch_pdl(k_relabel<true>, resident_grid(k_relabel<true>, kBlock), kBlock, s, P, n, ctl,
+                                       no_skip, cq, o.counters));
+            } else {
+                CC_CUDA_TRY(launch_pdl(k_relabel_decide<false>, resident_grid(k_relabel_decide<false>, kBlock), kBlock,
+                                       s, P, n, ctl, no_skip, wsum, td, cq, (cc_counters*)nullptr));
+                CC_LAUNCH_CHECK("k_relabel_decide");
+                CC_CUDA_TRY(launch_pdl(k_relabel<false>, resident_grid(k_relabel<false>, kBlock), kBlock, s, P, n, ctl,
+                                       no_skip, cq, (cc_counters*)nullptr));
+            }
             CC_LAUNCH_CHECK("k_relabel(H6)");
         }
         CC_CUDA_TRY(mark(CC_MARK_COMPRESS));

@@ -16,6 +16,7 @@ for r in rows[1:]:
     d[r[mi]] = float(r[vi].replace(",", ""))
     d["name"] = r[ki].split("(")[0].split("<")[0].replace("void ", "").split("::")[-1]
 calls, cur = [], None
+# a call ends with its final compress: k_relabel (partial H6, after k_relabel_decide)
 for i, d in per.items():
     if d["name"] == "k_sample_init":
         cur = []
