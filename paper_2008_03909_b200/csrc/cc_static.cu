@@ -1,7 +1,9 @@
 // cc_static.cu -- static connectivity / spanning forest pipeline (H1-H7).
 //
 // Alg. 1 / Alg. 2 on one B200, stream-ordered with
-// no host synchronisation: L_max and every queue length stay in device memory.
+// no host synchronisation: L_max, every queue length and every kernel choice
+// stay in device memory.  Every kernel is a programmatic dependent launch
+// (launch_pdl; pdl_trigger + pdl_wait at its entry).
 //
 //   K0 k_sample_init  H1 P[v] = v fused with the first k-out round: each vertex
 //                     u with first neighbour v0 < u sets P[u] = v0 by a plain
@@ -11,21 +13,25 @@
 //                     sampled edges (v0 > u, j = 1..k-1) go to a pending list;
 //                     a bitmap marks vertices whose list was not wholly sampled
 //                     (degree skip).
-//   Kc k_compress     pointer-jumping compress ("fully compress"; H6),
+//   Kp k_probe        round-0 chain depth from 1024 seeded walks: gates the mid
+//                     compress and picks the link kernel (device-side flag)
+//   Kc k_compress     pointer-jumping compress ("fully compress"),
 //                     root walks halving deep chains (root_halve)
-//   K1 k_link_refill  UF-Rem-CAS + SplitAtomicOne links of the pending sampled
-//                     edges with lane refill (H2; cc_common.cuh); k_link_pending
-//                     for Halve / UF-Async / CC_FLAG_NO_REFILL; k_link_contract
-//                     on the contracted forest with CC_FLAG_CONTRACT
+//   K1 k_link_pending UF-Rem-CAS + SplitAtomicOne links of the pending sampled
+//                     edges, one per thread (short chains: the default on RMAT/ER),
+//      k_link_refill  or with lane refill (long chains: grid-like ids; cc_common.cuh);
+//                     k_link_contract on the contracted forest (CC_FLAG_CONTRACT)
 //   K4 k_identify     IdentifyFrequent over S seeded samples (R9)
 //   K5 k_finish       ONE pass over P fusing the sampling compress (H3) with
 //                     the finish scan (H5): every vertex is compressed to its
 //                     root r; a marked vertex with r != L_max is queued, and
 //                     k_finish_proc / k_finish_big union its list,
 //                     degree-binned: warp-shared sweep / CTA per list / all
-//                     CTAs per huge list
+//                     CTAs per huge list; per-warp foreign-root summaries
 //   K5' sv_finish     the finish as Shiloach-Vishkin (= Liu-Tarjan PRF) or
 //                     Liu-Tarjan CRFA rounds (CC_FLAG_FINISH_SV / _CRFA)
+//   K6 k_relabel_decide + k_relabel   H6 as a partial pass: only the tiles
+//                     whose labels H5 changed (k_compress for a full pass)
 //   K7 forest         Filter of Alg. 2: compact non-sentinel slots in
 //                     slot order (cc_common.cuh)
 #include <cuda_runtime.h>
