@@ -429,7 +429,7 @@ def run_ours(a, rank, ws):
     del sampled_t, deg
     # the mid compress runs when forced, or when the device probe found long chains
     mid_ran = a.k > 0 and not (a.flags & cc.FLAG_NO_MIDCOMPRESS) and (
-        bool(a.flags & cc.FLAG_MIDCOMPRESS) or ctr["probe_deep"] * 8 >= 1024)
+        bool(a.flags & cc.FLAG_MIDCOMPRESS) or bool(ctr.get("mid_compress")))
     contract = a.k > 0 and bool(a.flags & cc.FLAG_CONTRACT) and not (a.flags & cc.FLAG_NO_SKIP)
     f0 = None
     if contract:

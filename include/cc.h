@@ -167,6 +167,8 @@ typedef struct {
                                   roots in one of its 256-slot warp summaries)               */
     uint64_t link_pending;     /* 1 if the k-out links ran in k_link_pending (0: lane refill,
                                   the contracted or the fused link)                        */
+    uint64_t mid_compress;     /* 1 if the chain probe ran the compress between the k-out
+                                  rounds (also 0 when a flag forced or forbade it)          */
 } cc_counters;
 
 typedef struct {

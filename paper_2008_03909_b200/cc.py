@@ -63,7 +63,7 @@ COUNTER_FIELDS = ["pending_links", "worklist", "finish_vertices", "finish_edges"
                   "big_vertices", "compress_writes",
                   "link_steps", "cas_failures", "probe_deep", "finish_gathers", "h6_writes", "h6_gathers",
                   "sv_rounds", "contract_roots", "amsf_rounds", "amsf_visits", "amsf_edges", "amsf_hooks",
-                  "amsf_rebuilds", "fused_link", "amsf_links", "h6_tiles", "link_pending"]
+                  "amsf_rebuilds", "fused_link", "amsf_links", "h6_tiles", "link_pending", "mid_compress"]
 
 
 class Opts(ctypes.Structure):

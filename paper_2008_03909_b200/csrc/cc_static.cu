@@ -651,7 +651,10 @@ __global__ void __launch_bounds__(1024) k_probe(const uint32_t* P, uint32_t n, u
     __syncthreads();
     if (threadIdx.x == 0) {
         ctl->skip_mid = s_deep * 8 < blockDim.x ? 1u : 0u;
-        if (cnt) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt->probe_deep), (unsigned long long)s_deep);
+        if (cnt) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(&cnt->probe_deep), (unsigned long long)s_deep);
+            if (!ctl->skip_mid) cnt->mid_compress = 1;
+        }
     }
 }
 
