@@ -33,6 +33,37 @@ static __device__ __forceinline__ unsigned long long warp_append(unsigned long l
     return base + incl - c;
 }
 
+// Order-free append of a warp's kept items through a per-warp shared-memory
+// buffer of CAP entries: one atomicAdd on the output counter per ~CAP items
+// instead of one per 32 (a single counter takes its atomics one at a time at
+// its L2 slice: ~1.3 ns each, 100 ms for the 79M appends of SV's edge copy at
+// C4 k = 0), and the items leave in coalesced runs.  Every lane of the warp
+// calls put() / flush() together.
+template <class T, int CAP>
+struct WarpBuf {
+    T* buf;            // this warp's CAP shared-memory entries
+    uint32_t fill;     // warp-uniform
+    __device__ __forceinline__ void put(bool keep, const T& x, unsigned long long* counter, T* out)
+    {
+        const unsigned lane = threadIdx.x & 31;
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (keep) buf[fill + __popc(m & ((1u << lane) - 1u))] = x;
+        fill += __popc(m);
+        if (fill > CAP - 32) flush(counter, out);
+    }
+    __device__ __forceinline__ void flush(unsigned long long* counter, T* out)
+    {
+        const unsigned lane = threadIdx.x & 31;
+        __syncwarp();
+        unsigned long long base = 0;
+        if (lane == 0 && fill) base = atomicAdd(counter, (unsigned long long)fill);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        for (uint32_t j = lane; j < fill; j += 32) out[base + j] = buf[j];
+        __syncwarp();
+        fill = 0;
+    }
+};
+
 static __device__ __forceinline__ void warp_count(uint64_t* ctr, uint32_t c)
 {
     if (!ctr) return;

@@ -1524,6 +1524,8 @@ __global__ void __launch_bounds__(kBlock) k_sv_starts(const uint32_t* __restrict
 // FILTER (every marked vertex is a candidate: no skip, or no sampling): an edge
 // between two candidates is materialised from both ends, so keep (u, v) only
 // when u < v or v is not a candidate -- half the edges, appended in any order.
+constexpr int kSvBuf = 384;                 // WarpBuf entries per warp (3 KB of uint2)
+
 template <bool FILTER>
 __global__ void __launch_bounds__(kBlock) k_sv_copy(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                                                     const uint32_t* __restrict__ cq, const uint32_t* __restrict__ deg,
@@ -1536,6 +1538,8 @@ __global__ void __launch_bounds__(kBlock) k_sv_copy(const int64_t* __restrict__ 
     const unsigned lane = threadIdx.x & 31;
     const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    __shared__ uint2 s_buf[FILTER ? kBlock / 32 : 1][FILTER ? kSvBuf : 1];
+    WarpBuf<uint2, kSvBuf> wb{s_buf[FILTER ? threadIdx.x >> 5 : 0], 0u};
     for (unsigned long long base = warp * 32; base < total; base += nwarps * 32) {
         const unsigned long long i = base + lane;
         const bool ok = i < total;
@@ -1571,14 +1575,14 @@ __global__ void __launch_bounds__(kBlock) k_sv_copy(const int64_t* __restrict__ 
                     const bool cand_v = ((bm[v >> 5] >> (v & 31)) & 1u) && v != lmax;
                     keep = ou < v || !cand_v;
                 }
-                const unsigned long long pos = warp_append(kept, keep ? 1u : 0u);
-                if (keep) edges[pos] = make_uint2(ou, v);
+                wb.put(keep, make_uint2(ou, v), kept, edges);
             } else {
                 (void)ost;
                 if (t < tot) edges[ost + (t - oex)] = make_uint2(ou, adj[ob + (int64_t)(t - oex)]);
             }
         }
     }
+    if constexpr (FILTER) wb.flush(kept, edges);
 }
 
 __global__ void __launch_bounds__(kBlock) k_sv_rootbits(const uint32_t* P, uint32_t n, uint32_t* bits)
@@ -1607,7 +1611,12 @@ __global__ void __launch_bounds__(kBlock) k_sv_hook(uint32_t* P, const uint2* __
         const uint32_t a = sv_label(P, bits, e.x), b = sv_label(P, bits, e.y);
         if (a == b) continue;
         const uint32_t h = max(a, b), l = min(a, b);     // h is a root of the round's start (a label)
-        ch |= atomicMin(P + h, l) > l ? 1u : 0u;         // writeMin
+        // writeMin, tested first: P[h] only decreases, so a value read at
+        // or below l (even a stale one) means the writeMin would change nothing -- which
+        // spares the hot roots' slots the serialised atomics of every edge that targets
+        // them (C4 k = 0, round 3: 789M atomicMin on few addresses, 567 ms)
+        if (ld_link(P + h) <= l) continue;
+        ch |= atomicMin(P + h, l) > l ? 1u : 0u;
     }
     if (__any_sync(0xffffffffu, ch != 0) && (threadIdx.x & 31) == 0) atomicOr(changed, 1u);
 }
@@ -1658,6 +1667,7 @@ __global__ void __launch_bounds__(kBlock) k_lt_connect(uint32_t* P, const LtEdge
         const LtEdge<SF> x = e[i];
         const uint32_t h = max(x.x, x.y), l = min(x.x, x.y);
         if (h == l || !((bits[h >> 5] >> (h & 31)) & 1u)) continue;     // RootUp: h a root at round start
+        if (ld_link(P + h) <= l) continue;                                // the writeMin would not change P[h]
         ch |= atomicMin(P + h, l) > l ? 1u : 0u;                          // Connect, writeMin
     }
     if (__any_sync(0xffffffffu, ch != 0) && (threadIdx.x & 31) == 0) atomicOr(changed, 1u);
@@ -1686,6 +1696,9 @@ __global__ void __launch_bounds__(kBlock) k_lt_alter(const uint32_t* P, const Lt
 {
     const unsigned long long total = *ne;
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    constexpr int CAP = SF ? kSvBuf / 2 : kSvBuf;
+    __shared__ LtEdge<SF> s_buf[kBlock / 32][CAP];
+    WarpBuf<LtEdge<SF>, CAP> wb{s_buf[threadIdx.x >> 5], 0u};
     for (unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x; base < total; base += stride) {
         const unsigned long long i = base + threadIdx.x;
         LtEdge<SF> x{};
@@ -1696,9 +1709,9 @@ __global__ void __launch_bounds__(kBlock) k_lt_alter(const uint32_t* P, const Lt
             x.y = P[x.y];
             keep = x.x != x.y;
         }
-        const unsigned long long pos = warp_append(ne_out, keep ? 1u : 0u);
-        if (keep) out[pos] = x;
+        wb.put(keep, x, ne_out, out);
     }
+    wb.flush(ne_out, out);
 }
 
 template <bool SF>
@@ -1754,11 +1767,16 @@ static cc_status sv_finish(const int64_t* off, const uint32_t* adj, uint32_t* P,
         const unsigned nbv = (unsigned)(((uint64_t)n + kBlock - 1) / kBlock);
         if (crfa) {
             // Liu-Tarjan CRFA: rounds until Alter leaves no edge
-            CC_CUDA_TRY(scratch_alloc((void**)&le[0], sizeof(LtEdge<SF>) * ne, s));
             CC_CUDA_TRY(scratch_alloc((void**)&le[1], sizeof(LtEdge<SF>) * ne, s));
             CC_CUDA_TRY(scratch_alloc((void**)&lcnt, 2 * sizeof(unsigned long long), s));
-            k_lt_init<SF><<<grid_blocks(8), kBlock, 0, s>>>(edges, ne, (LtEdge<SF>*)le[0]);
-            CC_LAUNCH_CHECK("k_lt_init");
+            if constexpr (SF) {
+                CC_CUDA_TRY(scratch_alloc((void**)&le[0], sizeof(LtEdge<SF>) * ne, s));
+                k_lt_init<SF><<<grid_blocks(8), kBlock, 0, s>>>(edges, ne, (LtEdge<SF>*)le[0]);
+                CC_LAUNCH_CHECK("k_lt_init");
+            } else {                          // (a, b) = (u, v): the materialised list is round 1's
+                le[0] = edges;
+                edges = nullptr;
+            }
             CC_CUDA_TRY(cudaMemcpyAsync(lcnt, &ne, sizeof(ne), cudaMemcpyHostToDevice, s));
             for (uint64_t round = 1;; ++round) {
                 const int a = (round - 1) & 1;
