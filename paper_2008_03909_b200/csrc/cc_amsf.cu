@@ -463,6 +463,8 @@ __global__ void __launch_bounds__(1024) k_amsf_lmax(uint32_t* P, uint32_t n, uin
 #ifndef CC_AMSF_ROUND_MINB
 #define CC_AMSF_ROUND_MINB 4
 #endif
+constexpr int kCarryBuf = 256;
+
 template <int MODE>
 __global__ void __launch_bounds__(kBlock, CC_AMSF_ROUND_MINB) k_amsf_round(
     const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, const float* __restrict__ w, uint32_t* P,
@@ -484,6 +486,8 @@ __global__ void __launch_bounds__(kBlock, CC_AMSF_ROUND_MINB) k_amsf_round(
     const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
     const unsigned cpw = (unsigned)max(1ull, min(32ull, (total + nwarps - 1) / nwarps));
+    __shared__ uint32_t s_carry[kBlock / 32][kCarryBuf];
+    WarpBuf<uint32_t, kCarryBuf> carry{s_carry[threadIdx.x >> 5], 0u};   // survivors, one atomic per ~kCarryBuf
     uint32_t visits = 0, hooks = 0, links = 0;
     unsigned long long scanned = 0;
     for (unsigned long long base = warp * cpw; base < total; base += nwarps * cpw) {
@@ -505,8 +509,7 @@ __global__ void __launch_bounds__(kBlock, CC_AMSF_ROUND_MINB) k_amsf_round(
                 work = lo_w < bhi;                             // maybe an edge in this bucket
             }
         }
-        const unsigned long long pos = warp_append(out_cnt, keep ? 1u : 0u);
-        if (keep) carry_out[pos] = u;
+        carry.put(keep, u, out_cnt, carry_out);
         const int64_t b = work ? off[u] : 0;
         const int64_t dfull = work ? off[u + 1] - b : 0;
         // an indexed list (> kIdxMin entries, bucket index built) contributes only this
@@ -570,6 +573,7 @@ __global__ void __launch_bounds__(kBlock, CC_AMSF_ROUND_MINB) k_amsf_round(
             __syncwarp();
         }
     }
+    carry.flush(out_cnt, carry_out);
     if (cnt) {
         warp_count(&cnt->amsf_visits, visits);
         warp_count(&cnt->amsf_hooks, hooks);
