@@ -31,8 +31,14 @@ __global__ void __launch_bounds__(kBlock) k_iota(uint32_t* P, uint32_t n)
     if (i < n) P[i] = (uint32_t)i;
 }
 
+// 128-thread blocks: the batch's inserts spread over more, shorter blocks, so the
+// kernel's tail (the last blocks' longest Rem walks) is shorter (C5: 34.1 -> 34.7 G
+// ops/s; 64 threads 34.3; one resident grid-strided wave 31.0)
+constexpr int kInsBlock = 128;
+constexpr int kQryBlock = 256;               // 128 / 64: within noise (C5 34.7 G ops/s)
+
 template <int MODE>
-__global__ void __launch_bounds__(kBlock) k_insert(uint32_t* P, const uint2* __restrict__ ins, int64_t n_ins)
+__global__ void __launch_bounds__(kInsBlock) k_insert(uint32_t* P, const uint2* __restrict__ ins, int64_t n_ins)
 {
     pdl_trigger();                                // the next batch's kernel may be scheduled now
     pdl_wait();                                   // ... and this one starts after the previous kernel
@@ -59,7 +65,7 @@ __device__ __forceinline__ uint32_t query_find(uint32_t* P, uint32_t x)
 }
 
 template <int FIND>
-__global__ void __launch_bounds__(kBlock) k_query(uint32_t* P, const uint2* __restrict__ q, int64_t n_q,
+__global__ void __launch_bounds__(kQryBlock) k_query(uint32_t* P, const uint2* __restrict__ q, int64_t n_q,
                                                   uint8_t* __restrict__ ans)
 {
     pdl_trigger();                                // the next batch's kernel may be scheduled now
@@ -240,13 +246,14 @@ static cc_status insert_query(cc_incr* h, const uint32_t* ins, int64_t n_ins, co
     if (n_ins > 0) {
         const uint2* e = reinterpret_cast<const uint2*>(ins);
         cudaError_t le;
-        if (h->flags & CC_FLAG_UF_ASYNC) le = launch_pdl(k_insert<2>, nblocks(n_ins), kBlock, s, h->P, e, n_ins);
-        else if (h->flags & CC_FLAG_HALVE) le = launch_pdl(k_insert<1>, nblocks(n_ins), kBlock, s, h->P, e, n_ins);
+        const unsigned nbi = (unsigned)((n_ins + kInsBlock - 1) / kInsBlock);
+        if (h->flags & CC_FLAG_UF_ASYNC) le = launch_pdl(k_insert<2>, nbi, kInsBlock, s, h->P, e, n_ins);
+        else if (h->flags & CC_FLAG_HALVE) le = launch_pdl(k_insert<1>, nbi, kInsBlock, s, h->P, e, n_ins);
         // one link per thread: measured faster on C5 than the static path's lane-refill
         // kernel (28.0 vs 26.1 G ops/s) and than 2 or 4 links per thread with their
         // first parent reads batched (26.3 / 24.4 vs 28.4 G ops/s: a quarter of the
         // threads, each walking its links one after another)
-        else le = launch_pdl(k_insert<0>, nblocks(n_ins), kBlock, s, h->P, e, n_ins);
+        else le = launch_pdl(k_insert<0>, nbi, kInsBlock, s, h->P, e, n_ins);
         CC_CUDA_TRY(le);
         CC_LAUNCH_CHECK("k_insert");
     }
@@ -254,9 +261,10 @@ static cc_status insert_query(cc_incr* h, const uint32_t* ins, int64_t n_ins, co
     if (n_q > 0) {
         const uint2* q = reinterpret_cast<const uint2*>(qs);
         cudaError_t le;
-        if (h->flags & CC_FLAG_FIND_SPLIT) le = launch_pdl(k_query<1>, nblocks(n_q), kBlock, s, h->P, q, n_q, ans);
-        else if (h->flags & CC_FLAG_FIND_NAIVE) le = launch_pdl(k_query<2>, nblocks(n_q), kBlock, s, h->P, q, n_q, ans);
-        else le = launch_pdl(k_query<0>, nblocks(n_q), kBlock, s, h->P, q, n_q, ans);
+        const unsigned nbq = (unsigned)((n_q + kQryBlock - 1) / kQryBlock);
+        if (h->flags & CC_FLAG_FIND_SPLIT) le = launch_pdl(k_query<1>, nbq, kQryBlock, s, h->P, q, n_q, ans);
+        else if (h->flags & CC_FLAG_FIND_NAIVE) le = launch_pdl(k_query<2>, nbq, kQryBlock, s, h->P, q, n_q, ans);
+        else le = launch_pdl(k_query<0>, nbq, kQryBlock, s, h->P, q, n_q, ans);
         CC_CUDA_TRY(le);
         CC_LAUNCH_CHECK("k_query");
     }
