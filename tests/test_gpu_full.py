@@ -71,12 +71,17 @@ def test_static_config_bit_exact(cfg):
     check_static(cfg)
 
 
-@pytest.mark.parametrize("opt", [dict(k=0), dict(k=2, variant="hybrid", seed=4)], ids=["k0", "hybrid-k2"])
+@pytest.mark.parametrize("opt", [dict(k=0), dict(k=2, variant="hybrid", seed=4),
+                                 dict(k=0, flags=1 << 9), dict(k=0, flags=1 << 13)],
+                         ids=["k0", "hybrid-k2", "k0-sv", "k0-crfa"])
 def test_c4_no_sampling_and_hybrid(opt):
     """SURVEY 8(c) test matrix, C4 column: k in {0, 2}.  k = 0 is Table 3's 'No Sampling'
     regime: every one of the 4.2e9 entries goes through the finish meta-loop
     (P:4091-4100), hub lists of > 2^20 entries through the all-CTA bin; hybrid k = 2 is the
-    paper's default sampling.  Labels bit-exact, forest validity triple."""
+    paper's default sampling.  The NEXT-3 finishes (Shiloach-Vishkin,
+    CC_FLAG_FINISH_SV = 1 << 9; Liu-Tarjan CRFA, CC_FLAG_FINISH_CRFA = 1 << 13) run here on
+    every edge too, in the configuration profiles/r2_next3_sv_crfa.json times.  Labels
+    bit-exact, forest validity triple."""
     check_static(inputs.C4, **opt)
 
 
