@@ -1519,12 +1519,34 @@ __global__ void __launch_bounds__(kBlock) k_sv_starts(const uint32_t* __restrict
 
 // Edge-parallel copy of the candidates' lists: a warp takes 32 candidates and
 // sweeps their concatenated lists 32 entries at a time (each lane finds its
-// entry's owner by a binary search over the warp's exclusive prefix), so a
-// hub's million-entry list is copied by many lanes, not one thread.
+// entry's owner by a binary search over the warp's exclusive prefix).  A list
+// longer than kSvPiece entries contributes only its first piece there; its other
+// pieces are queued (candidate, piece) and copied by k_sv_pieces, one warp per
+// piece, so a hub's million-entry list is spread over many warps instead of
+// serialising one (C4 at k = 0: 1.7M-entry hubs, 75 ms in one warp's loop).
 // FILTER (every marked vertex is a candidate: no skip, or no sampling): an edge
 // between two candidates is materialised from both ends, so keep (u, v) only
 // when u < v or v is not a candidate -- half the edges, appended in any order.
 constexpr int kSvBuf = 384;                 // WarpBuf entries per warp (3 KB of uint2)
+constexpr uint32_t kSvPiece = 4096;         // entries per piece of a long list
+#ifndef CC_SV_R
+#define CC_SV_R 4
+#endif
+constexpr int kSvR = CC_SV_R;               // entries per lane per sweep of k_sv_copy
+
+template <bool FILTER>
+struct SvCopy {
+    const uint32_t* adj;
+    uint2* edges;
+    const uint32_t* bm;
+    uint32_t lmax;
+    unsigned long long* kept;
+    __device__ __forceinline__ bool keep_edge(uint32_t u, uint32_t v) const
+    {
+        const bool cand_v = ((bm[v >> 5] >> (v & 31)) & 1u) && v != lmax;
+        return u < v || !cand_v;
+    }
+};
 
 template <bool FILTER>
 __global__ void __launch_bounds__(kBlock) k_sv_copy(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
@@ -1532,7 +1554,7 @@ __global__ void __launch_bounds__(kBlock) k_sv_copy(const int64_t* __restrict__ 
                                                     const unsigned long long* __restrict__ start,
                                                     unsigned long long total, uint32_t skip_prefix, uint2* edges,
                                                     const uint32_t* __restrict__ bm, const Ctl* ctl, bool no_skip,
-                                                    unsigned long long* kept)
+                                                    unsigned long long* kept, uint2* pieces, unsigned long long* npieces)
 {
     const uint32_t lmax = no_skip ? kSentinel : ctl->lmax;
     const unsigned lane = threadIdx.x & 31;
@@ -1540,13 +1562,20 @@ __global__ void __launch_bounds__(kBlock) k_sv_copy(const int64_t* __restrict__ 
     const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
     __shared__ uint2 s_buf[FILTER ? kBlock / 32 : 1][FILTER ? kSvBuf : 1];
     WarpBuf<uint2, kSvBuf> wb{s_buf[FILTER ? threadIdx.x >> 5 : 0], 0u};
+    const SvCopy<FILTER> sc{adj, edges, bm, lmax, kept};
     for (unsigned long long base = warp * 32; base < total; base += nwarps * 32) {
         const unsigned long long i = base + lane;
         const bool ok = i < total;
         const uint32_t u = ok ? cq[i] : 0u;
-        const uint64_t d = ok ? deg[i] : 0u;
+        const uint32_t dfull = ok ? deg[i] : 0u;
+        const uint64_t d = min(dfull, kSvPiece);            // the first piece here, the rest queued
         const int64_t b = ok ? off[u] + (int64_t)skip_prefix : 0;
         const unsigned long long st = ok && !FILTER ? start[i] : 0ull;
+        {
+            const uint32_t np = dfull > kSvPiece ? (dfull - 1) / kSvPiece : 0u;   // pieces 1 .. np
+            const unsigned long long pos = warp_append(npieces, np);
+            for (uint32_t q = 0; q < np; ++q) pieces[pos + q] = make_uint2((uint32_t)i, (uint32_t)(i >> 32) | ((q + 1) << 8));
+        }
         uint64_t incl = d;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -1555,30 +1584,90 @@ __global__ void __launch_bounds__(kBlock) k_sv_copy(const int64_t* __restrict__ 
         }
         const uint64_t tot = __shfl_sync(0xffffffffu, incl, 31);
         const uint64_t excl = incl - d;
-        for (uint64_t t0 = 0; t0 < tot; t0 += 32) {
-            const uint64_t t = t0 + lane;
-            int lo = 0;
+        // kSvR entries per lane per sweep, their owner searches first and their loads together
+        for (uint64_t t0 = 0; t0 < tot; t0 += 32 * kSvR) {
+            uint32_t ou[kSvR], v[kSvR];
+            int64_t src[kSvR];
+            unsigned long long dst[kSvR];
 #pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                const uint64_t pe = __shfl_sync(0xffffffffu, excl, lo + step);
-                if (pe <= t) lo += step;
-            }
-            const uint32_t ou = __shfl_sync(0xffffffffu, u, lo);
-            const int64_t ob = __shfl_sync(0xffffffffu, b, lo);
-            const uint64_t oex = __shfl_sync(0xffffffffu, excl, lo);
-            const unsigned long long ost = __shfl_sync(0xffffffffu, st, lo);
-            if constexpr (FILTER) {
-                uint32_t v = 0;
-                bool keep = false;
-                if (t < tot) {
-                    v = adj[ob + (int64_t)(t - oex)];
-                    const bool cand_v = ((bm[v >> 5] >> (v & 31)) & 1u) && v != lmax;
-                    keep = ou < v || !cand_v;
+            for (int r = 0; r < kSvR; ++r) {
+                const uint64_t t = t0 + (uint64_t)r * 32 + lane;
+                int lo = 0;
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1) {
+                    const uint64_t pe = __shfl_sync(0xffffffffu, excl, lo + step);
+                    if (pe <= t) lo += step;
                 }
-                wb.put(keep, make_uint2(ou, v), kept, edges);
-            } else {
-                (void)ost;
-                if (t < tot) edges[ost + (t - oex)] = make_uint2(ou, adj[ob + (int64_t)(t - oex)]);
+                ou[r] = __shfl_sync(0xffffffffu, u, lo);
+                const int64_t ob = __shfl_sync(0xffffffffu, b, lo);
+                const uint64_t oex = __shfl_sync(0xffffffffu, excl, lo);
+                const unsigned long long ost = __shfl_sync(0xffffffffu, st, lo);
+                src[r] = ob + (int64_t)(t - oex);
+                dst[r] = ost + (t - oex);
+            }
+#pragma unroll
+            for (int r = 0; r < kSvR; ++r) v[r] = t0 + (uint64_t)r * 32 + lane < tot ? adj[src[r]] : 0u;
+#pragma unroll
+            for (int r = 0; r < kSvR; ++r) {
+                const bool in = t0 + (uint64_t)r * 32 + lane < tot;
+                if constexpr (FILTER) {
+                    wb.put(in && sc.keep_edge(ou[r], v[r]), make_uint2(ou[r], v[r]), kept, edges);
+                } else {
+                    (void)dst;
+                    if (in) edges[dst[r]] = make_uint2(ou[r], v[r]);
+                }
+            }
+        }
+    }
+    if constexpr (FILTER) wb.flush(kept, edges);
+}
+
+// The queued pieces of the long lists: one warp per piece (kSvPiece entries), 8
+// entries per lane per sweep with their loads issued together.  A piece word is
+// (candidate index low 32 bits, high 8 bits of it | piece number << 8).
+template <bool FILTER>
+__global__ void __launch_bounds__(kBlock) k_sv_pieces(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                                                      const uint32_t* __restrict__ cq, const uint32_t* __restrict__ deg,
+                                                      const unsigned long long* __restrict__ start,
+                                                      uint32_t skip_prefix, uint2* edges, const uint32_t* __restrict__ bm,
+                                                      const Ctl* ctl, bool no_skip, unsigned long long* kept,
+                                                      const uint2* __restrict__ pieces,
+                                                      const unsigned long long* __restrict__ npieces)
+{
+    const uint32_t lmax = no_skip ? kSentinel : ctl->lmax;
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    __shared__ uint2 s_buf[FILTER ? kBlock / 32 : 1][FILTER ? kSvBuf : 1];
+    WarpBuf<uint2, kSvBuf> wb{s_buf[FILTER ? threadIdx.x >> 5 : 0], 0u};
+    const SvCopy<FILTER> sc{adj, edges, bm, lmax, kept};
+    const unsigned long long np = *npieces;
+    constexpr int R = 8;
+    for (unsigned long long pc = warp; pc < np; pc += nwarps) {
+        const uint2 pw = pieces[pc];
+        const unsigned long long i = (unsigned long long)pw.x | ((unsigned long long)(pw.y & 0xFFu) << 32);
+        const uint32_t q = pw.y >> 8;
+        const uint32_t u = cq[i];
+        const uint64_t p0 = (uint64_t)q * kSvPiece;
+        const uint64_t len = min((uint64_t)deg[i] - p0, (uint64_t)kSvPiece);
+        const int64_t b = off[u] + (int64_t)skip_prefix + (int64_t)p0;
+        const unsigned long long st = FILTER ? 0ull : start[i] + p0;
+        for (uint64_t t0 = 0; t0 < len; t0 += 32 * R) {
+            uint32_t v[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint64_t t = t0 + (uint64_t)r * 32 + lane;
+                v[r] = t < len ? adj[b + (int64_t)t] : 0u;
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint64_t t = t0 + (uint64_t)r * 32 + lane;
+                if constexpr (FILTER) {
+                    const bool keep = t < len && sc.keep_edge(u, v[r]);
+                    wb.put(keep, make_uint2(u, v[r]), kept, edges);
+                } else {
+                    if (t < len) edges[st + t] = make_uint2(u, v[r]);
+                }
             }
         }
     }
@@ -1727,8 +1816,9 @@ static cc_status sv_finish(const int64_t* off, const uint32_t* adj, uint32_t* P,
     if (cand == 0) return CC_OK;
     const unsigned long long nbk = (cand + kFTile - 1) / kFTile;
     uint32_t *deg = nullptr, *bits = nullptr;
-    unsigned long long *bsum = nullptr, *tot = nullptr, *starts = nullptr;
+    unsigned long long *bsum = nullptr, *tot = nullptr, *starts = nullptr, *npieces = nullptr;
     uint2* edges = nullptr;
+    uint2* pieces = nullptr;              // the long lists' pieces after the first (k_sv_pieces)
     unsigned int* changed = nullptr;
     cc_status rc = CC_OK;
     auto body = [&]() -> cc_status {
@@ -1748,11 +1838,17 @@ static cc_status sv_finish(const int64_t* off, const uint32_t* adj, uint32_t* P,
         CC_CUDA_TRY(scratch_alloc((void**)&edges, sizeof(uint2) * ne, s));
         CC_CUDA_TRY(scratch_alloc((void**)&bits, sizeof(uint32_t) * (((uint64_t)n + 31) / 32), s));
         CC_CUDA_TRY(scratch_alloc((void**)&changed, sizeof(unsigned int), s));
+        CC_CUDA_TRY(scratch_alloc((void**)&pieces, sizeof(uint2) * (ne / kSvPiece + 1), s));
+        CC_CUDA_TRY(scratch_alloc((void**)&npieces, sizeof(unsigned long long), s));
+        CC_CUDA_TRY(cudaMemsetAsync(npieces, 0, sizeof(unsigned long long), s));
         if (all_marked_candidates) {
             CC_CUDA_TRY(cudaMemsetAsync(tot, 0, sizeof(unsigned long long), s));
             k_sv_copy<true><<<grid_blocks(8), kBlock, 0, s>>>(off, adj, cq, deg, nullptr, cand, skip_prefix, edges,
-                                                                bm, ctl, no_skip, tot);
+                                                                bm, ctl, no_skip, tot, pieces, npieces);
             CC_LAUNCH_CHECK("k_sv_copy");
+            k_sv_pieces<true><<<grid_blocks(8), kBlock, 0, s>>>(off, adj, cq, deg, nullptr, skip_prefix, edges, bm, ctl,
+                                                                  no_skip, tot, pieces, npieces);
+            CC_LAUNCH_CHECK("k_sv_pieces");
             CC_CUDA_TRY(cudaMemcpyAsync(&ne, tot, sizeof(ne), cudaMemcpyDeviceToHost, s));
             CC_CUDA_TRY(cudaStreamSynchronize(s));
             if (ne == 0) return CC_OK;
@@ -1761,8 +1857,11 @@ static cc_status sv_finish(const int64_t* off, const uint32_t* adj, uint32_t* P,
             k_sv_starts<<<(unsigned)nbk, kBlock, 0, s>>>(deg, bsum, cand, starts);
             CC_LAUNCH_CHECK("k_sv_starts");
             k_sv_copy<false><<<grid_blocks(8), kBlock, 0, s>>>(off, adj, cq, deg, starts, cand, skip_prefix, edges,
-                                                                 nullptr, ctl, no_skip, nullptr);
+                                                                 nullptr, ctl, no_skip, nullptr, pieces, npieces);
             CC_LAUNCH_CHECK("k_sv_copy");
+            k_sv_pieces<false><<<grid_blocks(8), kBlock, 0, s>>>(off, adj, cq, deg, starts, skip_prefix, edges, nullptr,
+                                                                   ctl, no_skip, nullptr, pieces, npieces);
+            CC_LAUNCH_CHECK("k_sv_pieces");
         }
         const unsigned nbv = (unsigned)(((uint64_t)n + kBlock - 1) / kBlock);
         if (crfa) {
@@ -1831,6 +1930,8 @@ static cc_status sv_finish(const int64_t* off, const uint32_t* adj, uint32_t* P,
     scratch_free(tot, s);
     scratch_free(starts, s);
     scratch_free(edges, s);
+    scratch_free(pieces, s);
+    scratch_free(npieces, s);
     scratch_free(bits, s);
     scratch_free(changed, s);
     scratch_free(le[0], s);

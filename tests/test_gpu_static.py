@@ -463,11 +463,15 @@ def _huge_graphs():
 
 
 @pytest.mark.parametrize("opt", [dict(k=0), dict(k=1), dict(k=1, flags=cc.FLAG_NO_SKIP), dict(k=2),
-                                 dict(k=0, flags=cc.FLAG_UF_ASYNC), dict(k=1, variant="hybrid", seed=3)],
+                                 dict(k=0, flags=cc.FLAG_UF_ASYNC), dict(k=1, variant="hybrid", seed=3),
+                                 dict(k=0, flags=cc.FLAG_FINISH_SV), dict(k=1, flags=cc.FLAG_FINISH_CRFA),
+                                 dict(k=1, flags=cc.FLAG_FINISH_SV), dict(k=0, flags=cc.FLAG_FINISH_CRFA)],
                          ids=lambda o: "-".join(f"{k}{v}" for k, v in o.items()))
 def test_huge_list_bin_labels_and_forest(opt):
     """>2^20-entry lists: labels bit-exact and forests valid for k in {0, 1} (the
-    'No Sampling' regime of Table 3) and with the skip off."""
+    'No Sampling' regime of Table 3) and with the skip off.  With the SV /
+    CRFA finishes the hub lists are materialised in pieces of 4096 entries by other warps
+    (k_sv_pieces), through the filtered (k = 0) and the positioned (k = 1) copy."""
     for name, off, adj in _huge_graphs():
         n = off.size - 1
         assert int(np.diff(off).max()) > (1 << 20) + 1, name
@@ -482,7 +486,8 @@ def test_huge_list_bin_labels_and_forest(opt):
         assert rc == 0, (name, opt, oracle.FOREST_ERRORS[rc], bad)
         assert np.array_equal(u32(lab2), want), (name, opt)
         cnt = dict(zip(cc.COUNTER_FIELDS, ctr.cpu().tolist()))
-        if opt["k"] == 0 or opt.get("flags") == cc.FLAG_NO_SKIP or (name == "two_hubs" and opt["k"] == 1):
+        sv = opt.get("flags", 0) & (cc.FLAG_FINISH_SV | cc.FLAG_FINISH_CRFA)
+        if not sv and (opt["k"] == 0 or opt.get("flags") == cc.FLAG_NO_SKIP or (name == "two_hubs" and opt["k"] == 1)):
             # the hub list went through the finish (the huge bin) -- not skipped
             assert cnt["finish_edges"] > (1 << 20), (name, opt, cnt["finish_edges"])
 
