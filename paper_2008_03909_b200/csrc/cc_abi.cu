@@ -233,6 +233,7 @@ size_t cc_workspace_bytes(uint32_t n, int64_t m, uint32_t kout_k, int op)
                + 8 * (N + 1) + 4 * M + 4 * N        // staging of pageable offsets / adjacency / labels
                + 8 * nw + 8 * std::min(N, M) + 12 * (nw / 4096 + 1) + 8     // CC_FLAG_CONTRACT
                + 12 * N + 8 * (N / 4096 + 1) + 8 + 8 * M + 4 * nw + 4       // FINISH_SV / CRFA edge list
+               + 8 * (M / 4096 + 1) + 8                                     // ... and its long-list pieces
                + 2 * (op == 1 ? 16 : 8) * M + 16;                           // CRFA's two edge buffers
     if (op == 1) b += 8 * N + 12 * nfb             // forest slots + Filter status words
                       + 8 * N + 8;                  // staging of pageable edges / num_edges
