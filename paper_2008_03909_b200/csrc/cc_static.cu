@@ -29,7 +29,10 @@
 //                     degree-binned: warp-shared sweep / CTA per list / all
 //                     CTAs per huge list; per-warp foreign-root summaries
 //   K5' sv_finish     the finish as Shiloach-Vishkin (= Liu-Tarjan PRF) or
-//                     Liu-Tarjan CRFA rounds (CC_FLAG_FINISH_SV / _CRFA)
+//                     Liu-Tarjan CRFA rounds (CC_FLAG_FINISH_SV / _CRFA) over the
+//                     candidates' edges (k_sv_copy + k_sv_pieces for lists in
+//                     4096-entry pieces; appends through WarpBuf; writeMin tested
+//                     before the atomic)
 //   K6 k_relabel_decide + k_relabel   H6 as a partial pass: only the tiles
 //                     whose labels H5 changed (k_compress for a full pass)
 //   K7 forest         Filter of Alg. 2: compact non-sentinel slots in
