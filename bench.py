@@ -154,8 +154,8 @@ def peaks():
 
 
 def ncu_traffic(workload: str, kernel: str):
-    """dram read+write bytes per launch of `kernel` from a committed `ncu --set full`
-    capture of THIS workload (profiles/ncu_traffic.json is keyed by workload, then by
+    """dram read+write bytes per launch of `kernel` from a committed ncu capture (launch list
+    with dram__bytes_read.sum / dram__bytes_write.sum, or --set full) of THIS workload (profiles/ncu_traffic.json is keyed by workload, then by
     bench mark name); None when no capture of this workload / kernel exists."""
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
@@ -567,7 +567,8 @@ def run_ours(a, rank, ws):
         finish["dram_view"] = {"dram_bytes": int(sum(dram)), "GB/s": round(sum(dram) / (fin_ms * 1e-3) / 1e9, 1),
                                "frac_of_8TBs": round(sum(dram) / (fin_ms * 1e-3) / 1e9 / CONTRACT_GBS, 4),
                                "dram_over_B_fin": round(sum(dram) / max(1, B["finish_phase"]), 3),
-                               "source": f"profiles/ncu_traffic.json[{cfg.name}] (ncu --set full, cold cache, per launch)"}
+                               "source": f"profiles/ncu_traffic.json[{cfg.name}] (ncu dram__bytes_read.sum + "
+                                         f"dram__bytes_write.sum, cold cache, per launch)"}
     else:
         finish["dram_view"] = None
     phase_ms = {"sample": round(smp_ms, 5), "identify": round(kern_ms["k_identify"], 5),
