@@ -2,4 +2,4 @@
 D=gpurun_out/${1:-fuzz}; mkdir -p $D
 timeout 700 python scripts/probe/fuzz.py 600 101 > $D/fuzz_101.txt 2>&1; echo "rc=$?" >> $D/fuzz_101.txt
 timeout 700 python scripts/probe/fuzz.py 600 202 > $D/fuzz_202.txt 2>&1; echo "rc=$?" >> $D/fuzz_202.txt
-tail -2 $D/fuzz_*.txt
+for f in $D/fuzz_*.txt; do tail -n 2 $f; done
