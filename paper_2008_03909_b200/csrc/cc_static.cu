@@ -1174,6 +1174,51 @@ __global__ void __launch_bounds__(kBlock) k_finish_proc(
     const unsigned lane = threadIdx.x & 31;
     const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+#ifndef CC_FINISH_PROC_NOSPLIT
+    if (total > 0 && 2 * total <= nwarps) {
+        // Few candidates (the sampled regime: C4 253, C3 40): G >= 2 warps per candidate,
+        // warp g of a candidate's group takes the list's 32-edge sweeps g, g + G, ... -- one
+        // warp walking a list of hundreds of entries sweep after sweep was the kernel's
+        // critical path (ncu on C3: SMs active 7 % of its 21.7 us)
+        const unsigned long long G = nwarps / total;
+        const unsigned long long c = warp / G, g = warp % G;
+        if (c >= total) return;
+        const uint32_t u = cq[c];
+        int64_t b = off[u];
+        const int64_t e = off[u + 1];
+        b += min((int64_t)skip_prefix, e - b);
+        const int64_t d = e - b;
+        const bool isbig = d > kBigDeg;
+        if (g == 0) {
+            if (cnt && lane == 0) {
+                atomicAdd((unsigned long long*)&cnt->finish_vertices, 1ull);
+                atomicAdd((unsigned long long*)&cnt->finish_edges, (unsigned long long)d);
+                if (isbig) atomicAdd((unsigned long long*)&cnt->big_vertices, 1ull);
+            }
+            if (isbig && lane == 0) {                    // the long lists keep their own kernel
+                if (d > kHugeDeg) big[big_cap - 1 - atomicAdd(&ctl->huge_count, 1ull)] = u;
+                else big[atomicAdd(&ctl->big_count, 1ull)] = u;
+            }
+        }
+        if (isbig || d <= 0) return;
+        const uint32_t ru = ld_relaxed(P + u);
+        uint32_t hooks = 0;
+        for (int64_t t = (int64_t)(g * 32 + lane); t < d; t += (int64_t)G * 32) {
+            const uint32_t v = adj[b + t];
+            const uint32_t pv = ld_link(P + v);
+            if (pv == ru) continue;
+            if constexpr (MODE == 2) {
+                if constexpr (SF) hooks += link_async(P, u, v, TileMarked<Forest>{Forest{F}, td});
+                else hooks += link_async(P, u, v, TileMarked<NoForest>{NoForest{}, td});
+            } else {
+                if constexpr (SF) hooks += link_rem_from<MODE == 1>(P, u, v, ru, pv, TileMarked<Forest>{Forest{F}, td});
+                else hooks += link_rem_from<MODE == 1>(P, u, v, ru, pv, TileMarked<NoForest>{NoForest{}, td});
+            }
+        }
+        if (cnt) warp_count(&cnt->finish_hooks, hooks);
+        return;
+    }
+#endif
     // candidates per warp: 32 when there is plenty of work, fewer when the queue
     // is short so that every warp gets some (short queues are latency-bound)
     const unsigned cpw = (unsigned)max(1ull, min(32ull, (total + nwarps - 1) / nwarps));
