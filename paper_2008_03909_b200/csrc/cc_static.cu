@@ -1161,7 +1161,9 @@ struct TileMarked {
 // finding its edge's owner by a binary search over the prefix (shuffles), so
 // every lane has an independent link in flight whatever the degree mix; an
 // edge whose endpoint already hangs directly under the owner's root is
-// skipped without a link.  Lists longer than kBigDeg go to k_finish_big.
+// skipped without a link.  Lists longer than kBigDeg go to k_finish_big.  With
+// few candidates (at most half as many as warps) several warps share each
+// candidate's list instead (DESIGN.md §6 item 20).
 template <int MODE, bool SF>
 __global__ void __launch_bounds__(kBlock) k_finish_proc(
     const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, uint32_t* P,
