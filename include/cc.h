@@ -295,7 +295,13 @@ cc_status cc_incr_batch(cc_incr* h, const uint32_t* inserts, int64_t n_ins,
  * staging buffers by DMA on an internal copy stream, batch b+1 while batch b
  * computes (scratch: 2 x 8 B per pair of the largest batch); pinned answers
  * are written in place; pageable arrays are staged batch by batch.  A call
- * with host arrays returns after the work is complete.  Errors as
+ * with host arrays returns after the work is complete.  Stream order: the
+ * call's first kernel is an ordinary launch (it starts after all earlier work
+ * of `stream` has completed), every later one a programmatic dependent launch
+ * that reads its batch's pairs and first parent slots BEFORE waiting for the
+ * previous kernel (DESIGN.md §6 item 21) -- so all batches' pairs must be in
+ * place when the call is made (written by earlier work of `stream`, or by the
+ * host), not by work enqueued on another stream afterwards.  Errors as
  * cc_incr_batch (with CC_FLAG_VALIDATE, all ids are checked first). */
 cc_status cc_incr_batches(cc_incr* h, int64_t nb, const int64_t* ins_counts, const uint32_t* inserts,
                           const int64_t* q_counts, const uint32_t* queries, uint8_t* answers, void* stream);

@@ -123,6 +123,22 @@ __device__ __forceinline__ uint32_t find_halve_quiet(uint32_t* P, uint32_t x)
     return x;
 }
 
+// The same walk entered with p = a value P[x] held after the last hook of x's tree
+// was ordered before this call (a read of x's slot taken earlier, then refreshed by the
+// caller when it claimed x a root): p is x or an ancestor, so the walk below -- whose
+// root tests all read L2 -- returns x's current root.
+__device__ __forceinline__ uint32_t find_halve_quiet_from(uint32_t* P, uint32_t x, uint32_t p)
+{
+    while (p != x) {
+        const uint32_t g = ld_relaxed(P + p);
+        if (g == p) return p;
+        P[x] = g;
+        x = g;
+        p = ld_relaxed(P + x);
+    }
+    return x;
+}
+
 struct NoForest {
     __device__ __forceinline__ void record(uint32_t, uint32_t, uint32_t) const {}
 };

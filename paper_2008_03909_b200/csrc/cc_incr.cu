@@ -38,11 +38,30 @@ constexpr int kInsBlock = 128;
 constexpr int kQryBlock = 256;               // 128 / 64: within noise (C5 34.7 G ops/s)
 
 template <int MODE>
-__global__ void __launch_bounds__(kInsBlock) k_insert(uint32_t* P, const uint2* __restrict__ ins, int64_t n_ins)
+__global__ void __launch_bounds__(kInsBlock) k_insert(uint32_t* P, const uint2* __restrict__ ins, int64_t n_ins,
+                                                   bool pre)
 {
     pdl_trigger();                                // the next batch's kernel may be scheduled now
-    pdl_wait();                                   // ... and this one starts after the previous kernel
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+#ifndef CC_INCR_NOPREFETCH
+    if (MODE == 0 && pre) {
+        // Before the wait (while the previous batch's query kernel drains): the pair and its
+        // two first parent reads.  They may be stale w.r.t. that kernel's halving stores, which
+        // the Rem loop tolerates (R5: every value a slot held is an ancestor in its set; the
+        // hook CAS validates a root claim), so a block resident early starts its walk at once.
+        uint2 e = make_uint2(0u, 0u);
+        uint32_t pu = 0, pv = 0;
+        if (i < n_ins) {
+            e = ins[i];
+            pu = ld_relaxed(P + e.x);
+            pv = ld_relaxed(P + e.y);
+        }
+        pdl_wait();                               // ... the hooks start after the previous kernel
+        if (i < n_ins) link_rem_from<false>(P, e.x, e.y, pu, pv, NoForest{});
+        return;
+    }
+#endif
+    pdl_wait();                                   // ... and this one starts after the previous kernel
     if (i >= n_ins) return;
     const uint2 e = ins[i];
     link<MODE>(P, e.x, e.y, NoForest{});
@@ -66,11 +85,32 @@ __device__ __forceinline__ uint32_t query_find(uint32_t* P, uint32_t x)
 
 template <int FIND>
 __global__ void __launch_bounds__(kQryBlock) k_query(uint32_t* P, const uint2* __restrict__ q, int64_t n_q,
-                                                  uint8_t* __restrict__ ans)
+                                                  uint8_t* __restrict__ ans, bool pre)
 {
     pdl_trigger();                                // the next batch's kernel may be scheduled now
-    pdl_wait();                                   // ... and this one starts after the previous kernel
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+#ifndef CC_INCR_NOPREFETCH
+    if (FIND == 0 && pre) {
+        // Before the wait (while this batch's insert kernel drains): the pair and the two first
+        // parent reads.  A stale value is an ancestor of the vertex (hooks and splits only move
+        // a slot up its tree), so the walk may start there; only a stale ROOT claim (the vertex
+        // itself) is re-read after the wait, and every root test below reads L2 after the wait.
+        uint2 e = make_uint2(0u, 0u);
+        uint32_t pa = 0, pb = 0;
+        if (i < n_q) {
+            e = q[i];
+            pa = ld_relaxed(P + e.x);
+            pb = ld_relaxed(P + e.y);
+        }
+        pdl_wait();                               // ... the answers read the state after all inserts
+        if (i >= n_q) return;
+        if (pa == e.x) pa = ld_relaxed(P + e.x);
+        if (pb == e.y) pb = ld_relaxed(P + e.y);
+        ans[i] = find_halve_quiet_from(P, e.x, pa) == find_halve_quiet_from(P, e.y, pb) ? 1 : 0;
+        return;
+    }
+#endif
+    pdl_wait();                                   // ... and this one starts after the previous kernel
     if (i >= n_q) return;
     const uint2 e = q[i];
     const uint32_t ra = query_find<FIND>(P, e.x);
@@ -193,8 +233,13 @@ __global__ void __launch_bounds__(kBlock) k_labels(uint32_t* P, uint32_t n, uint
 
 static unsigned nblocks(int64_t count) { return (unsigned)((count + kBlock - 1) / kBlock); }
 
+// pdl: launch the batch's first kernel with PDL (false: a full dependency on the stream's
+// previous work).  pre: the kernels may read their pairs (and first parents) BEFORE their PDL
+// wait -- only when the pairs were written before the start of a full-dependency kernel that
+// precedes them in this stream (cc_incr_batches: its first kernel is launched without PDL), so
+// that the pre-wait reads see them.
 static cc_status insert_query(cc_incr* h, const uint32_t* ins, int64_t n_ins, const uint32_t* qs, int64_t n_q,
-                              uint8_t* ans, cudaStream_t s)
+                              uint8_t* ans, cudaStream_t s, bool pdl = true, bool pre = false)
 {
     if (h->flags & CC_FLAG_VALIDATE) {
         unsigned int* err = nullptr;
@@ -229,7 +274,7 @@ static cc_status insert_query(cc_incr* h, const uint32_t* ins, int64_t n_ins, co
             mode == 2 ? (find == 1 ? k_small_batch<2, 1> : find == 2 ? k_small_batch<2, 2> : k_small_batch<2, 0>)
             : mode == 1 ? (find == 1 ? k_small_batch<1, 1> : find == 2 ? k_small_batch<1, 2> : k_small_batch<1, 0>)
                         : (find == 1 ? k_small_batch<0, 1> : find == 2 ? k_small_batch<0, 2> : k_small_batch<0, 0>);
-        CC_CUDA_TRY(launch_pdl(kern, 1, thr, s, h->P, e, n_ins, q, n_q, ans));
+        CC_CUDA_TRY(launch_pdl_if(pdl, kern, 1, thr, s, h->P, e, n_ins, q, n_q, ans));
         CC_LAUNCH_CHECK("k_small_batch");
         return CC_OK;
     }
@@ -247,13 +292,13 @@ static cc_status insert_query(cc_incr* h, const uint32_t* ins, int64_t n_ins, co
         const uint2* e = reinterpret_cast<const uint2*>(ins);
         cudaError_t le;
         const unsigned nbi = (unsigned)((n_ins + kInsBlock - 1) / kInsBlock);
-        if (h->flags & CC_FLAG_UF_ASYNC) le = launch_pdl(k_insert<2>, nbi, kInsBlock, s, h->P, e, n_ins);
-        else if (h->flags & CC_FLAG_HALVE) le = launch_pdl(k_insert<1>, nbi, kInsBlock, s, h->P, e, n_ins);
+        if (h->flags & CC_FLAG_UF_ASYNC) le = launch_pdl_if(pdl, k_insert<2>, nbi, kInsBlock, s, h->P, e, n_ins, pre);
+        else if (h->flags & CC_FLAG_HALVE) le = launch_pdl_if(pdl, k_insert<1>, nbi, kInsBlock, s, h->P, e, n_ins, pre);
         // one link per thread: measured faster on C5 than the static path's lane-refill
         // kernel (28.0 vs 26.1 G ops/s) and than 2 or 4 links per thread with their
         // first parent reads batched (26.3 / 24.4 vs 28.4 G ops/s: a quarter of the
         // threads, each walking its links one after another)
-        else le = launch_pdl(k_insert<0>, nbi, kInsBlock, s, h->P, e, n_ins);
+        else le = launch_pdl_if(pdl, k_insert<0>, nbi, kInsBlock, s, h->P, e, n_ins, pre);
         CC_CUDA_TRY(le);
         CC_LAUNCH_CHECK("k_insert");
     }
@@ -262,9 +307,9 @@ static cc_status insert_query(cc_incr* h, const uint32_t* ins, int64_t n_ins, co
         const uint2* q = reinterpret_cast<const uint2*>(qs);
         cudaError_t le;
         const unsigned nbq = (unsigned)((n_q + kQryBlock - 1) / kQryBlock);
-        if (h->flags & CC_FLAG_FIND_SPLIT) le = launch_pdl(k_query<1>, nbq, kQryBlock, s, h->P, q, n_q, ans);
-        else if (h->flags & CC_FLAG_FIND_NAIVE) le = launch_pdl(k_query<2>, nbq, kQryBlock, s, h->P, q, n_q, ans);
-        else le = launch_pdl(k_query<0>, nbq, kQryBlock, s, h->P, q, n_q, ans);
+        if (h->flags & CC_FLAG_FIND_SPLIT) le = launch_pdl_if(pdl || n_ins > 0, k_query<1>, nbq, kQryBlock, s, h->P, q, n_q, ans, pre);
+        else if (h->flags & CC_FLAG_FIND_NAIVE) le = launch_pdl_if(pdl || n_ins > 0, k_query<2>, nbq, kQryBlock, s, h->P, q, n_q, ans, pre);
+        else le = launch_pdl_if(pdl || n_ins > 0, k_query<0>, nbq, kQryBlock, s, h->P, q, n_q, ans, pre);
         CC_CUDA_TRY(le);
         CC_LAUNCH_CHECK("k_query");
     }
@@ -404,7 +449,7 @@ cc_status pipelined_batches(cc_incr* h, int64_t nb, const std::vector<int64_t>& 
             }
             CC_CUDA_TRY(cudaEventRecord(ready[k], cs));
             CC_CUDA_TRY(cudaStreamWaitEvent(s, ready[k], 0));
-            cc_status r = insert_query(h, pi, ins_counts[b], pq, q_counts[b], ans + oq[b], s);
+            cc_status r = insert_query(h, pi, ins_counts[b], pq, q_counts[b], ans + oq[b], s, b > 0, true);
             if (r) return r;
             CC_CUDA_TRY(cudaEventRecord(freed[k], s));
         }
@@ -521,7 +566,8 @@ cc_status cc_incr_batches(cc_incr* h, int64_t nb, const int64_t* ins_counts, con
                                k_q == MEM_PINNED, d_ans, s);
     } else {
         for (int64_t b = 0; b < nb && rc == CC_OK; ++b)
-            rc = insert_query(h, d_ins + 2 * oi[b], ins_counts[b], d_q + 2 * oq[b], q_counts[b], d_ans + oq[b], s);
+            rc = insert_query(h, d_ins + 2 * oi[b], ins_counts[b], d_q + 2 * oq[b], q_counts[b], d_ans + oq[b], s,
+                              b > 0, true);
     }
     h->flags = saved;
     if (rc == CC_OK && host) CC_CUDA_TRY(cudaStreamSynchronize(s));

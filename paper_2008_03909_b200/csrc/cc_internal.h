@@ -64,6 +64,20 @@ constexpr int kBlock = 256;
 // scheduled while the previous kernel of the stream still runs; it must execute
 // pdl_wait() before touching memory the previous kernel writes.
 template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStream_t s, Args... args);
+
+// launch_pdl, or an ordinary launch (full dependency on the previous work of the
+// stream, its writes visible from the kernel's first instruction) when !pdl
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl_if(bool pdl, void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStream_t s,
+                                 Args... args)
+{
+    if (pdl) return launch_pdl(kernel, grid, block, s, args...);
+    kernel<<<grid, block, 0, s>>>(static_cast<KArgs>(args)...);
+    return cudaGetLastError();
+}
+
+template <class... KArgs, class... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStream_t s, Args... args)
 {
     cudaLaunchConfig_t cfg = {};

@@ -21,6 +21,7 @@ if not torch.cuda.is_available():
 
 import paper_2008_03909_b200 as pkg  # noqa: E402
 from inputs import gpu as ggen  # noqa: E402
+from paper_2008_03909_b200 import cc  # noqa: E402
 
 
 def host(t, dtype):
@@ -83,6 +84,34 @@ def test_c4_no_sampling_and_hybrid(opt):
     every edge too, in the configuration profiles/r2_next3_sv_crfa.json times.  Labels
     bit-exact, forest validity triple."""
     check_static(inputs.C4, **opt)
+
+
+def test_incremental_config_multi_batch_call_bit_exact():
+    """C5 in the launch configuration bench.py times: the whole 256-batch stream in ONE
+    cc_incr_batches call on device-resident pairs (kernels after the first read their pairs
+    and first parents before their PDL wait).  Every answer and the final labels == oracle."""
+    _GRAPHS.clear()
+    torch.cuda.empty_cache()
+    cfg = inputs.C5
+    n = 1 << cfg.scale
+    nb = cfg.n_batches
+    ins = torch.empty((nb, cfg.n_ins, 2), dtype=torch.int32, device="cuda")
+    qs = torch.empty((nb, cfg.n_q, 2), dtype=torch.int32, device="cuda")
+    for b in range(nb):
+        ggen.incr_batch(cfg.seed, cfg.scale, b, cfg.n_ins, cfg.n_q, ins[b], qs[b])
+    ans = torch.empty((nb, cfg.n_q), dtype=torch.uint8, device="cuda")
+    h = cc.Incr(n)
+    h.batches(np.full(nb, cfg.n_ins, dtype=np.int64), ins, np.full(nb, cfg.n_q, dtype=np.int64), qs, ans)
+    lab = torch.empty(n, dtype=torch.int32, device="cuda")
+    h.labels(lab)
+    h.close()
+    h_ins, h_qs = host(ins, np.uint32), host(qs, np.uint32)
+    del ins, qs
+    want, want_lab = oracle.incr_run(n, [(h_ins[b], h_qs[b]) for b in range(nb)], want_labels=True)
+    got = ans.cpu().numpy().reshape(-1)
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, bad[:5]
+    assert np.array_equal(u32(lab), want_lab)
 
 
 def test_incremental_config_bit_exact():

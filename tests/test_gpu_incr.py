@@ -183,6 +183,33 @@ def test_multi_batch_call_bit_exact(batch, flags):
     assert np.array_equal(u32(lab), want_lab)
 
 
+@pytest.mark.parametrize("flags", [0, cc.FLAG_HALVE, cc.FLAG_FIND_SPLIT])
+def test_multi_batch_call_large_batches_mixed_shapes(flags):
+    """cc_incr_batches with batches above the single-CTA limit (two kernels per batch, the
+    pre-wait pair / first-parent reads after the first kernel): a queries-only first batch,
+    inserts-only batches, empty batches and uneven sizes; answers and labels == oracle."""
+    n = 1 << 14
+    rng = np.random.default_rng(5)
+    shapes = [(0, 9000), (12000, 0), (0, 0), (20000, 3000), (9001, 1), (1, 9001), (30000, 30000), (0, 0),
+              (15000, 5000)]
+    batches = []
+    for b, (ni, nq) in enumerate(shapes):
+        i, _ = gen.incr_batch(seed=21, scale=14, b=b, n_ins=max(ni, 1), n_q=1)
+        q = rng.integers(0, n, (nq, 2)).astype(np.uint32)
+        batches.append((i[:ni], q))
+    want, want_lab = oracle.incr_run(n, batches, want_labels=True)
+    ins = dev(np.concatenate([b[0] for b in batches]).reshape(-1, 2))
+    qs = dev(np.concatenate([b[1] for b in batches]).reshape(-1, 2))
+    ans = torch.empty(qs.shape[0], dtype=torch.uint8, device="cuda")
+    h = cc.Incr(n, flags)
+    h.batches(np.array([s[0] for s in shapes]), ins, np.array([s[1] for s in shapes]), qs, ans)
+    lab = torch.empty(n, dtype=torch.int32, device="cuda")
+    h.labels(lab)
+    h.close()
+    assert np.array_equal(ans.cpu().numpy(), want)
+    assert np.array_equal(u32(lab), want_lab)
+
+
 def test_adversarial_chain_queries():
     """A path inserted in id order builds one chain of length n (every hook puts
     i+1 under i); the default halving queries must answer it exactly and fast,
