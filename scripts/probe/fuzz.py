@@ -119,5 +119,19 @@ while time.time() - t0 < secs:
             print("INCR MISMATCH", name, ifl)
             sys.exit(1)
         runs["incr"] += 1
+        # the same batches through ONE cc_incr_batches call on device arrays (large batches:
+        # the kernels after the first read their pairs before their PDL wait)
+        ai = np.concatenate([i for i, _ in batches]).reshape(-1, 2)
+        aq = np.concatenate([q for _, q in batches]).reshape(-1, 2)
+        h = cc.Incr(n, ifl)
+        ans = torch.empty(max(1, aq.shape[0]), dtype=torch.uint8, device="cuda")
+        h.batches(np.array([i.shape[0] for i, _ in batches], dtype=np.int64), torch.from_numpy(ai.view(np.int32)).cuda(),
+                  np.array([q.shape[0] for _, q in batches], dtype=np.int64), torch.from_numpy(aq.view(np.int32)).cuda(),
+                  ans)
+        h.close()
+        if not np.array_equal(ans.cpu().numpy()[:aq.shape[0]], wa):
+            print("INCR BATCHES MISMATCH", name, ifl)
+            sys.exit(1)
+        runs["incr_batches"] = runs.get("incr_batches", 0) + 1
 cc.set_grid(0)
 print("fuzz ok", runs, f"{time.time() - t0:.0f}s")
