@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(kInsBlock) k_insert(uint32_t* P, const uint2* 
         // two first parent reads.  They may be stale w.r.t. that kernel's halving stores, which
         // the Rem loop tolerates (R5: every value a slot held is an ancestor in its set; the
         // hook CAS validates a root claim), so a block resident early starts its walk at once.
+        // `pre` is set only where the pairs are known to be in place (insert_query).
         uint2 e = make_uint2(0u, 0u);
         uint32_t pu = 0, pv = 0;
         if (i < n_ins) {
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(kQryBlock) k_query(uint32_t* P, const uint2* _
         // parent reads.  A stale value is an ancestor of the vertex (hooks and splits only move
         // a slot up its tree), so the walk may start there; only a stale ROOT claim (the vertex
         // itself) is re-read after the wait, and every root test below reads L2 after the wait.
+        // `pre` is set only where the pairs are known to be in place (insert_query).
         uint2 e = make_uint2(0u, 0u);
         uint32_t pa = 0, pb = 0;
         if (i < n_q) {
