@@ -436,6 +436,7 @@ cc_status pipelined_batches(cc_incr* h, int64_t nb, const std::vector<int64_t>& 
             CC_CUDA_TRY(cudaEventCreateWithFlags(&freed[k], cudaEventDisableTiming));
             CC_CUDA_TRY(cudaEventRecord(freed[k], s));   // buffers start free (after their allocation)
         }
+        bool launched = false;
         for (int64_t b = 0; b < nb; ++b) {
             const int k = (int)(b & 1);
             const uint32_t* pi = ins + 2 * oi[b];
@@ -451,7 +452,9 @@ cc_status pipelined_batches(cc_incr* h, int64_t nb, const std::vector<int64_t>& 
             }
             CC_CUDA_TRY(cudaEventRecord(ready[k], cs));
             CC_CUDA_TRY(cudaStreamWaitEvent(s, ready[k], 0));
-            cc_status r = insert_query(h, pi, ins_counts[b], pq, q_counts[b], ans + oq[b], s, b > 0, true);
+            // PDL (and the pre-wait reads it enables) once a non-empty batch has launched a kernel
+            cc_status r = insert_query(h, pi, ins_counts[b], pq, q_counts[b], ans + oq[b], s, launched, true);
+            launched |= ins_counts[b] + q_counts[b] > 0;
             if (r) return r;
             CC_CUDA_TRY(cudaEventRecord(freed[k], s));
         }
@@ -567,9 +570,14 @@ cc_status cc_incr_batches(cc_incr* h, int64_t nb, const int64_t* ins_counts, con
         rc = pipelined_batches(h, nb, oi, oq, ins_counts, q_counts, d_ins, k_ins == MEM_PINNED, d_q,
                                k_q == MEM_PINNED, d_ans, s);
     } else {
-        for (int64_t b = 0; b < nb && rc == CC_OK; ++b)
+        // the first non-empty batch's first kernel is an ordinary launch (all earlier work of the
+        // stream, which wrote the pairs, complete and visible); PDL and pre-wait reads after it
+        bool launched = false;
+        for (int64_t b = 0; b < nb && rc == CC_OK; ++b) {
             rc = insert_query(h, d_ins + 2 * oi[b], ins_counts[b], d_q + 2 * oq[b], q_counts[b], d_ans + oq[b], s,
-                              b > 0, true);
+                              launched, true);
+            launched |= ins_counts[b] + q_counts[b] > 0;
+        }
     }
     h->flags = saved;
     if (rc == CC_OK && host) CC_CUDA_TRY(cudaStreamSynchronize(s));

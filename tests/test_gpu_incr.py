@@ -186,11 +186,12 @@ def test_multi_batch_call_bit_exact(batch, flags):
 @pytest.mark.parametrize("flags", [0, cc.FLAG_HALVE, cc.FLAG_FIND_SPLIT])
 def test_multi_batch_call_large_batches_mixed_shapes(flags):
     """cc_incr_batches with batches above the single-CTA limit (two kernels per batch, the
-    pre-wait pair / first-parent reads after the first kernel): a queries-only first batch,
-    inserts-only batches, empty batches and uneven sizes; answers and labels == oracle."""
+    pre-wait pair / first-parent reads after the first kernel): an empty then a queries-only
+    first batch, inserts-only batches, empty batches and uneven sizes; answers and labels ==
+    oracle."""
     n = 1 << 14
     rng = np.random.default_rng(5)
-    shapes = [(0, 9000), (12000, 0), (0, 0), (20000, 3000), (9001, 1), (1, 9001), (30000, 30000), (0, 0),
+    shapes = [(0, 0), (0, 9000), (12000, 0), (0, 0), (20000, 3000), (9001, 1), (1, 9001), (30000, 30000), (0, 0),
               (15000, 5000)]
     batches = []
     for b, (ni, nq) in enumerate(shapes):
